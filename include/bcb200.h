@@ -1,0 +1,199 @@
+/*
+ * bcb200.h -- C-ABI of the B200-native Block Cascading hot path.
+ *
+ * The reference (`blockcascade`, pure Python/numpy) has no FFI; these entry
+ * points are what its numeric operator boundary would bind.  Each one names
+ * the reference interface it replaces (paths relative to
+ * /root/reference/pkg/src/blockcascade/).  Plain pointers and sizes only:
+ * device pointers are CUDA global-memory addresses, `stream` is a
+ * cudaStream_t passed as void*, host pointers are marked [host].
+ *
+ * Status codes (mapped onto the reference's exception classes by
+ * paper_2511_20426_b200/errors.py):
+ *   BC_OK 0, BC_ERR_CONTRACT 1 (ContractViolation), BC_ERR_NUMERIC 2
+ *   (NumericError), BC_ERR_CUDA 3 (CUDA/NCCL failure, or no device).
+ */
+#ifndef BCB200_H_
+#define BCB200_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define BC_OK 0
+#define BC_ERR_CONTRACT 1
+#define BC_ERR_NUMERIC 2
+#define BC_ERR_CUDA 3
+
+#define BC_MAX_ENTRIES 16 /* cascade width cap per launch (ceil(P/o) <= 16) */
+#define BC_MAX_VIS 32     /* visible key blocks per query block             */
+
+/* Human-readable text of the last error on this thread. */
+const char* bc_last_error(void);
+/* Library version / build flags string. */
+const char* bc_version(void);
+
+/* ---------------------------------------------------------------------------
+ * Noise: NoiseStream.draw / block_noise (core.py:161-186) and the Philox
+ * expansion of embed_prompt (core.py:144-158).  Bit-identical to numpy:
+ * Philox4x64-10 bit generator (key, 256-bit counter incremented before each
+ * 4-word block) feeding numpy's own ziggurat `random_standard_normal_fill`.
+ * Host-side, GIL-free, one thread per stream.
+ * ------------------------------------------------------------------------- */
+typedef struct {
+  uint64_t key[2];     /* Philox key words                           */
+  uint64_t counter[4]; /* Philox counter, e.g. {block, pass, frame, 0} */
+  int64_t n;           /* normals to draw                            */
+  void* out;           /* [host] float64 or float32 destination      */
+} bc_noise_task;
+
+/* dtype: 0 = float64, 1 = float32 (rounded from the float64 draw). */
+int bc_noise_run(const bc_noise_task* tasks /*[host]*/, int n_tasks, int dtype,
+                 int n_threads);
+
+/* Raw Philox4x64-10 output words (for known-answer tests). */
+int bc_philox4x64(const uint64_t key[2], const uint64_t counter[4], uint64_t out[4]);
+
+/* ---------------------------------------------------------------------------
+ * renoise (denoiser.py:360-368): out = (1 - s) * x0 + s * eps, s = level/1000,
+ * evaluated without FMA contraction (bit-identical to numpy for float64).
+ * out may alias x0.  `nonfinite` (device int32, may be NULL) is set to 1 if
+ * any output is non-finite.
+ * ------------------------------------------------------------------------- */
+int bc_renoise_f64(const double* x0, const double* eps, double level, double* out,
+                   int64_t n, int32_t* nonfinite, void* stream);
+int bc_renoise_f32(const float* x0, const float* eps, double level, float* out,
+                   int64_t n, int32_t* nonfinite, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * Batch description shared by both forwards: one entry per in-flight block
+ * (plan order = ascending block).  vis_slot[e][0..n_vis[e]) lists the KV
+ * arena slots the entry's queries attend to, in ascending block order --
+ * the gather order of denoiser._gather (denoiser.py:284-296) and the column
+ * order of build_mask (denoiser.py:172-194).  slot[e] is where the entry
+ * writes its fresh per-layer K/V.
+ * ------------------------------------------------------------------------- */
+typedef struct {
+  int32_t n_entries;
+  int32_t block_size; /* latent frames per block (S)              */
+  int32_t block_index[BC_MAX_ENTRIES];
+  double level[BC_MAX_ENTRIES];
+  int32_t slot[BC_MAX_ENTRIES];
+  int32_t n_vis[BC_MAX_ENTRIES];
+  int32_t vis_slot[BC_MAX_ENTRIES][BC_MAX_VIS];
+} bc_batch;
+
+/* ---------------------------------------------------------------------------
+ * Toy DiT forward (denoiser.py:299-357, embed_entry 234-250, layer_qkv
+ * 253-261, layer_attend 264-277, predict_head 280-281), float64 on device.
+ * KV arena layout: [layers][n_slots][2 (K,V)][S][D] float64.
+ * ------------------------------------------------------------------------- */
+typedef struct {
+  const double *w_in, *w_cond, *w_level, *w_q, *w_k, *w_v, *w_o, *w_head;
+  int32_t layers, heads, dim, cond_dim;
+} bc_toy_weights;
+
+int bc_toy_forward(const bc_toy_weights* w /*[host struct, device ptrs]*/,
+                   const bc_batch* batch /*[host]*/,
+                   const double* const* latents /*[host] n_entries device ptrs (S,D)*/,
+                   const double* const* cond /*[host] n_entries device ptrs (Dc)*/,
+                   double* kv_arena, int32_t n_slots,
+                   double* const* x0_out /*[host] n_entries device ptrs (S,D)*/,
+                   double* workspace /* >= 2*n*S*D doubles */,
+                   int32_t* status /* device int32: 1+block of first non-finite input */,
+                   void* stream);
+
+/* ---------------------------------------------------------------------------
+ * Wan2.1-shaped DiT (configs 2-5).  See wan_runtime.cu / DESIGN.md.
+ * ------------------------------------------------------------------------- */
+typedef struct bc_wan_ctx bc_wan_ctx;
+
+typedef struct {
+  int32_t layers, heads, head_dim, ffn_dim;
+  int32_t text_len, text_dim, freq_dim;
+  int32_t latent_h, latent_w;  /* latent grid (patch 1x2x2, 16 channels) */
+  int32_t block_size;          /* latent frames per block                 */
+  int32_t n_slots;             /* KV arena slots                          */
+  int32_t max_entries;         /* widest batch the workspace must hold    */
+} bc_wan_dims;
+
+/* Parameter block: device pointers into caller-owned (torch) storage.
+ * Linear weights are bf16 [out][in] (nn.Linear layout), vectors fp32. */
+typedef struct {
+  const void* patch_w;  const float* patch_b;    /* [d][64], [d]           */
+  const void* text_w1;  const float* text_b1;    /* [d][text_dim]          */
+  const void* text_w2;  const float* text_b2;    /* [d][d]                 */
+  const void* time_w1;  const float* time_b1;    /* [d][freq_dim]          */
+  const void* time_w2;  const float* time_b2;    /* [d][d]                 */
+  const void* tproj_w;  const float* tproj_b;    /* [6d][d]                */
+  const void* head_w;   const float* head_b;     /* [64][d]                */
+  const float* head_mod;                          /* [2][d]                 */
+  /* per layer, stacked over layers */
+  const void* qkv_w;    const float* qkv_b;      /* [L][3d][d], [L][3d]    */
+  const void* o_w;      const float* o_b;        /* [L][d][d]              */
+  const void* cq_w;     const float* cq_b;       /* cross q                */
+  const void* ckv_w;    const float* ckv_b;      /* [L][2d][d] cross k,v   */
+  const void* co_w;     const float* co_b;       /* cross out              */
+  const void* ffn1_w;   const float* ffn1_b;     /* [L][ffn][d]            */
+  const void* ffn2_w;   const float* ffn2_b;     /* [L][d][ffn]            */
+  const float* norm_q;  const float* norm_k;     /* [L][d] RMSNorm weights */
+  const float* cnorm_q; const float* cnorm_k;    /* [L][d] cross RMSNorm   */
+  const float* norm3_w; const float* norm3_b;    /* [L][d] cross-attn LN   */
+  const float* modulation;                        /* [L][6][d]              */
+} bc_wan_params;
+
+int bc_wan_create(const bc_wan_dims* dims, const bc_wan_params* params,
+                  void* kv_arena /* bf16 [L][n_slots][2][T][d] */,
+                  void* workspace, int64_t workspace_bytes, bc_wan_ctx** out);
+/* Bytes of workspace bc_wan_create needs for these dims. */
+int64_t bc_wan_workspace_bytes(const bc_wan_dims* dims);
+int bc_wan_destroy(bc_wan_ctx* ctx);
+
+/* Per prompt: text MLP over the synthetic encoder states (device fp32
+ * [text_len][text_dim]) and the per-layer cross-attention K/V. */
+int bc_wan_set_text(bc_wan_ctx* ctx, const float* text_states, void* stream);
+
+/* Per-entry fused update applied after the head (the "Euler/renoise step"):
+ *   x0 = x_t - sigma_t * v   (flow-matching head, sigma_t = level/1000)
+ *   post 0: x_next = (1-s') x0 + s' eps,  s' = next_level/1000
+ *   post 1: x_next = x0 and emit_out = x0 (emission)
+ *   post 2: nothing (cache pass; KV already written to the slot)
+ *   post 3: x0_out = x0 only (operator API: forward without update) */
+typedef struct {
+  int32_t post[BC_MAX_ENTRIES];
+  double next_level[BC_MAX_ENTRIES];
+  float* latents[BC_MAX_ENTRIES];     /* (S,16,H,W) fp32, updated in place */
+  const float* eps[BC_MAX_ENTRIES];   /* post 0 */
+  float* out[BC_MAX_ENTRIES];         /* post 1 / 3 */
+} bc_wan_update;
+
+/* One cascade iteration: batched forward of every entry + fused update. */
+int bc_wan_step(bc_wan_ctx* ctx, const bc_batch* batch, const bc_wan_update* upd,
+                int32_t* status, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * Building blocks, exported for the parity tests and the multi-GPU executor.
+ * ------------------------------------------------------------------------- */
+/* C[M,N] (+)= epilogue(A[M,K] . B[N,K]^T + bias); bf16 in, fp32 accumulate.
+ * mode 0: C bf16 = acc+bias;  1: C bf16 = gelu_tanh(acc+bias);
+ * 2: C fp32 = acc+bias;       3: C fp32 += gate[row/rows_per_gate] * (acc+bias)
+ * K % 64 == 0, N % 64 == 0; lda = ldb = K, ldc = N. */
+int bc_gemm_bf16(const void* A, const void* B, void* C, int32_t M, int32_t N, int32_t K,
+                 int32_t mode, const float* bias, const float* gate, int32_t gate_stride,
+                 int32_t rows_per_gate, void* stream);
+
+/* Paged flash attention over KV-arena slots (self-attention) or a dense
+ * K/V (cross-attention).  q: bf16 [rows][heads][128]; out: bf16 same.
+ * For entry e, query rows [e*q_per_entry, (e+1)*q_per_entry) attend to the
+ * concatenation of vis_slot[e][*] (each `kv_tokens` rows) in order. */
+int bc_attention_paged(const void* q, const void* k_arena, const void* v_arena,
+                       int64_t slot_stride_elems, int32_t kv_tokens,
+                       const bc_batch* batch, int32_t q_per_entry, int32_t heads,
+                       void* out, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BCB200_H_ */

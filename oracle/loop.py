@@ -1,0 +1,100 @@
+"""CPU session runtime for the product engine's session protocol -- TEST
+ORACLE ONLY.
+
+``paper_2511_20426_b200.engine`` asks its runtime for a session exposing
+``set_conditioning / step / kv_handle / release / emitted_host /
+fill_wall_times / close``.  Tests monkeypatch ``engine._runtime_for`` with
+:func:`oracle_runtime` to drive the product scheduler / pool / mask / switch
+logic on CPU with the numpy oracle forward, and compare against outputs the
+reference itself produced (tests/golden).  Never used by the product.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import toy as toy_oracle
+
+POST_RENOISE, POST_EMIT, POST_CACHE = 0, 1, 2
+
+
+@dataclass(frozen=True)
+class _KV:
+    block_index: int
+    layer_index: int
+    keys: np.ndarray
+    values: np.ndarray
+    noise_tag: float
+    conditioning_id: str
+
+    @property
+    def frame_count(self):
+        return self.keys.shape[0]
+
+
+class ToyOracleSession:
+    def __init__(self, weights, config, cond, session_seed):
+        from paper_2511_20426_b200.core import NoiseStream
+        self.W = toy_oracle.weights_from(weights)
+        self.S = config.block_size
+        self.noise = NoiseStream(session_seed, config.latent_dim)
+        self.latents, self.final, self.kv, self.tags = {}, {}, {}, {}
+        self.cond = cond
+
+    def set_conditioning(self, cond):
+        self.cond = cond
+
+    def step(self, plan, mask, pool, vis_lists, posts):
+        S = self.S
+        ents = []
+        for e in plan.entries:
+            b = e.block_index
+            if e.pass_index == 0 and b not in self.latents:
+                self.latents[b] = self.noise.block_noise(b, 0, b * S, S)
+            ents.append((b, self.latents[b], e.noise_level, self.cond.embedding))
+        visible = {b: lst for b, lst in zip(plan.blocks, vis_lists)}
+        pool_kv = {b: self.kv[b] for b in mask.pool_blocks}
+        outs = toy_oracle.forward(self.W, ents, pool_kv, visible)
+        for e, (x0, kv), (kind, next_pass, next_level) in zip(plan.entries, outs, posts):
+            b = e.block_index
+            self.kv[b] = kv
+            self.tags[b] = (e.noise_level, self.cond.id)
+            if kind == POST_RENOISE:
+                eps = self.noise.block_noise(b, next_pass, b * S, S)
+                self.latents[b] = toy_oracle.renoise(x0, eps, next_level)
+            elif kind == POST_EMIT:
+                self.final[b] = x0
+                self.latents[b] = x0
+            else:
+                self.latents.pop(b, None)
+
+    def kv_handle(self, block):
+        level, cid = self.tags[block]
+        return tuple(_KV(block, l, k, v, level, cid) for l, (k, v) in enumerate(self.kv[block]))
+
+    def release(self, block):
+        pass
+
+    def emitted_host(self, block):
+        return self.final[block]
+
+    def fill_wall_times(self, events):
+        pass
+
+    def close(self):
+        pass
+
+
+class _OracleRuntime:
+    def __init__(self, weights):
+        self.weights = weights
+
+    def open_session(self, config, cond, session_seed, noise_feed=None):
+        return ToyOracleSession(self.weights, config, cond, session_seed)
+
+
+def oracle_runtime(weights, config):
+    """Drop-in replacement for ``engine._runtime_for`` in CPU tests."""
+    return _OracleRuntime(weights)

@@ -1,0 +1,319 @@
+"""Session loops: the cascaded pipeline and the sequential block-causal
+rollout, with the reference signatures (``engine.py:69-342``).
+
+Both loops keep every block's latents and KV on the device:
+
+* the host runs the scheduler (``plan_iteration``/``advance``), the pool
+  index logic (``KVPool.insert``), mask construction and the slot table;
+* each iteration is ONE device step (:meth:`DeviceRuntime.step`): the
+  batched forward of all in-flight entries plus the fused per-entry update
+  -- renoise to the next level with counter-keyed noise (p < emit), emit
+  (p == emit), or nothing (cache pass: the KV already sits in the block's
+  arena slot, inserting it into the pool is bookkeeping);
+* emitted blocks are copied device -> host asynchronously; the trace's
+  ``wall_clock`` is CUDA-event time between iteration boundaries on the
+  launching stream.
+
+Outputs are a pure function of (config minus workers, seeds, prompt
+schedule) exactly as in the reference: the worker count only changes the
+trace's placement labels.
+"""
+
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from .config import CascadeConfig
+from .core import NoiseStream, embed_prompt
+from .denoiser import build_mask, init_model, visible_block_lists
+from .errors import ContractViolation, InvalidInputError
+from .executor import CostModel, assign_workers, exchanged_kv_frames
+from .interactive import CommandQueue, SwitchEvent, SwitchSpec
+from .kvpool import KVPool
+from .metrics import Trace, TraceEvent
+from .scheduler import CascadeState, advance, plan_iteration
+
+DEFAULT_SESSION_SEED = 20260809
+DEFAULT_WEIGHT_SEED = 7
+
+POST_RENOISE, POST_EMIT, POST_CACHE = 0, 1, 2
+
+
+@dataclass
+class RunResult:
+    outputs: dict
+    trace: Trace
+    pool: KVPool
+    emitted_order: list
+    switch_events: list = field(default_factory=list)
+
+    @property
+    def iterations(self) -> int:
+        return len(self.trace.events)
+
+    def stacked_outputs(self) -> np.ndarray:
+        return np.concatenate([self.outputs[k] for k in sorted(self.outputs)])
+
+
+def _default_weights(config: CascadeConfig, weight_seed: int):
+    if config.model == "toy":
+        return init_model(weight_seed, config.layers, config.heads,
+                          config.latent_dim, config.cond_dim)
+    from .wan import WanWeights
+    return WanWeights.random(config, weight_seed)
+
+
+def _runtime_for(weights, config: CascadeConfig):
+    if config.model == "toy":
+        from .toy import toy_runtime
+        return toy_runtime(weights)
+    return weights.runtime()
+
+
+def _switch_table(switches, config: CascadeConfig) -> dict:
+    table = {}
+    emit = config.schedule().emit_pass
+    for spec in switches or ():
+        if spec.at_block is not None and not 0 <= spec.at_block < config.num_blocks:
+            raise InvalidInputError(
+                f"switch block {spec.at_block} outside run of {config.num_blocks} blocks")
+        it = spec.boundary_iteration(config.offset, emit)
+        if it in table:
+            raise InvalidInputError(f"two switches scripted for iteration {it}")
+        table[it] = spec
+    return table
+
+
+class _Session:
+    """Device-side state of one run shared by both loops."""
+
+    def __init__(self, config, weights, conditioning, session_seed, noise_feed=None):
+        self.config = config
+        self.rt = _runtime_for(weights, config)
+        self.session = self.rt.open_session(config, conditioning, session_seed,
+                                            noise_feed=noise_feed)
+        self.noise = NoiseStream(session_seed, config.latent_dim)
+
+    def close(self):
+        self.session.close()
+
+
+def _pool_entry_frames(pool: KVPool) -> int:
+    return pool.frame_count()
+
+
+def run_cascade(config: CascadeConfig, prompt: str,
+                session_seed: int = DEFAULT_SESSION_SEED,
+                weight_seed: int = DEFAULT_WEIGHT_SEED,
+                switches=(), command_queue: CommandQueue | None = None,
+                event_sink=None, weights=None, pace_seconds: float = 0.0,
+                noise_feed=None) -> RunResult:
+    """Plan / execute / apply until every block has retired (Alg. 1)."""
+    config.validate()
+    if config.decode_overlap and config.workers < 2:
+        raise InvalidInputError("decode overlap needs at least 2 workers",
+                                fields=["decode_overlap", "workers"])
+    if config.refresh_sink_on_switch:
+        raise InvalidInputError(
+            "refresh_sink_on_switch re-runs a KV recache pass; the B200 build has "
+            "no KV-recache path", fields=["refresh_sink_on_switch"])
+    sched = config.schedule()
+    if weights is None:
+        weights = _default_weights(config, weight_seed)
+    cond = embed_prompt(prompt, config.cond_dim)
+    cost = CostModel.from_config(config)
+    pool = KVPool.empty(config.window_blocks, config.sink_blocks)
+    state = CascadeState(num_blocks=config.num_blocks, offset=config.offset,
+                         schedule=sched, workers=config.workers)
+    scripted = _switch_table(switches, config)
+    trace = Trace(meta={"kind": "cascade", "prompt": prompt, "session_seed": session_seed,
+                        "weight_seed": weight_seed, "config": config.to_dict()})
+    sess = _Session(config, weights, cond, session_seed, noise_feed)
+    dev = sess.session
+    switch_events = []
+    modeled = 0.0
+    decode_done_at = 0.0
+    pending = []           # (iteration-record) waiting for device timings
+    S = config.block_size
+    try:
+        while not state.done:
+            record = None
+            spec = scripted.pop(state.iteration, None)
+            live = None
+            if spec is None and command_queue is not None:
+                live = command_queue.pop()
+                if live is not None:
+                    spec = SwitchSpec(prompt=live.prompt, mode=live.mode,
+                                      at_iteration=state.iteration)
+            if spec is not None:
+                if spec.mode != "cascade":
+                    err = InvalidInputError(
+                        "recache switches are not on the B200 path (no KV-recache); "
+                        "use mode='cascade'")
+                    if live is not None:
+                        live.reject(err)
+                    raise err
+                cond = embed_prompt(spec.prompt, config.cond_dim)
+                dev.set_conditioning(cond)
+                ev = SwitchEvent(iteration=state.iteration, boundary_block=state.lead,
+                                 mode=spec.mode, extra_passes=0, conditioning_id=cond.id,
+                                 prompt=spec.prompt, stall_modeled=0.0)
+                switch_events.append(ev)
+                record = ev.to_dict()
+                if live is not None:
+                    live.resolve(ev)
+
+            plan = plan_iteration(state)
+            mask = build_mask(plan.blocks, pool.block_indices, config.attention_mode, S)
+            pre_pool = pool
+            posts = []
+            for e in plan.entries:
+                if e.pass_index < sched.emit_pass:
+                    posts.append((POST_RENOISE, e.pass_index + 1,
+                                  sched.level_for_pass(e.pass_index + 1)))
+                elif e.pass_index == sched.emit_pass:
+                    posts.append((POST_EMIT, None, None))
+                else:
+                    posts.append((POST_CACHE, None, None))
+            dev.step(plan, mask, pool, visible_block_lists(mask), posts)
+
+            emitted = advance(state, plan, plan.blocks)
+            for e, (kind, _, _) in zip(plan.entries, posts):
+                if kind == POST_CACHE:
+                    newer = pool.insert(e.block_index, dev.kv_handle(e.block_index))
+                    for gone in pool.evicted_by(newer):
+                        dev.release(gone)
+                    if e.block_index not in newer:
+                        dev.release(e.block_index)
+                    pool = newer
+            emitted_block = emitted[0] if emitted else None
+
+            # modeled clock: exactly the reference's accounting
+            placement = assign_workers(plan.width, config.workers)
+            busy = [0.0] * config.workers
+            entry_rows = []
+            for pos, e in enumerate(plan.entries):
+                frames = mask.visible_frames(e.block_index)
+                c = cost.pass_cost(frames)
+                busy[placement[pos]] += c
+                entry_rows.append({"block": e.block_index, "pass_index": e.pass_index,
+                                   "noise_level": e.noise_level, "worker": placement[pos],
+                                   "conditioning_id": cond.id, "queries": S,
+                                   "visible_frames": frames, "modeled_cost": c})
+            comm = cost.comm_cost(exchanged_kv_frames(plan.blocks, placement,
+                                                      config.attention_mode, S))
+            dec_charge = 0.0
+            dec_start = dec_done = None
+            if emitted_block is not None and cost.decode > 0.0:
+                if config.decode_overlap:
+                    dec_start = max(modeled + max(busy) + comm, decode_done_at)
+                    dec_done = dec_start + cost.decode_cost()
+                    decode_done_at = dec_done
+                else:
+                    dec_charge = cost.decode_cost()
+            modeled += max(busy) + comm + dec_charge
+
+            event = TraceEvent(
+                iteration=plan.iteration, entries=entry_rows, wall_seconds=0.0,
+                modeled_exec=max(busy), modeled_comm=comm, modeled_stall=0.0,
+                modeled_decode=dec_charge, modeled_clock=modeled, wall_clock=0.0,
+                pool_blocks=len(pre_pool.block_indices), pool_frames=pre_pool.frame_count(),
+                pool_state=pre_pool.state_dump(), emitted_block=emitted_block,
+                emitted_video_frames=(S * config.video_frames_per_latent
+                                      if emitted_block is not None else None),
+                decode_start=dec_start, decode_done=dec_done, switch=record)
+            trace.append(event)
+            pending.append(event)
+            if event_sink is not None:
+                dev.fill_wall_times(pending)
+                pending.clear()
+                out = dev.emitted_host(emitted_block) if emitted_block is not None else None
+                event_sink(event, out)
+            if pace_seconds > 0.0:
+                time.sleep(pace_seconds)
+        dev.fill_wall_times(pending)
+        outputs = {b: dev.emitted_host(b) for b in state.emitted}
+    finally:
+        sess.close()
+    if command_queue is not None:
+        command_queue.reject_all(InvalidInputError("session already finished"))
+    if sorted(outputs) != list(range(config.num_blocks)):
+        raise ContractViolation(
+            f"run finished with outputs for {sorted(outputs)}; expected all of "
+            f"0..{config.num_blocks - 1}")
+    return RunResult(outputs=outputs, trace=trace, pool=pool,
+                     emitted_order=list(state.emitted), switch_events=switch_events)
+
+
+def run_sequential_reference(config: CascadeConfig, prompt: str,
+                             session_seed: int = DEFAULT_SESSION_SEED,
+                             weight_seed: int = DEFAULT_WEIGHT_SEED,
+                             weights=None, noise_feed=None) -> RunResult:
+    """Plain block-causal rollout: every block runs all its passes against
+    its predecessors' cached KV before the next block starts.  Written as
+    nested loops over (block, pass), independent of the state machine, so
+    ``run_cascade(offset=passes)`` can be checked against it."""
+    config.validate()
+    sched = config.schedule()
+    if weights is None:
+        weights = _default_weights(config, weight_seed)
+    cond = embed_prompt(prompt, config.cond_dim)
+    cost = CostModel.from_config(config)
+    pool = KVPool.empty(config.window_blocks, config.sink_blocks)
+    S = config.block_size
+    trace = Trace(meta={"kind": "sequential", "prompt": prompt,
+                        "session_seed": session_seed, "weight_seed": weight_seed,
+                        "config": config.to_dict()})
+    sess = _Session(config, weights, cond, session_seed, noise_feed)
+    dev = sess.session
+    emitted_order = []
+    modeled = 0.0
+    it = 0
+    try:
+        for b in range(config.num_blocks):
+            for p in range(sched.passes):
+                level = sched.level_for_pass(p)
+                mask = build_mask([b], pool.block_indices, config.attention_mode, S)
+                if p < sched.emit_pass:
+                    post = (POST_RENOISE, p + 1, sched.level_for_pass(p + 1))
+                elif p == sched.emit_pass:
+                    post = (POST_EMIT, None, None)
+                else:
+                    post = (POST_CACHE, None, None)
+                from .scheduler import BatchPlan, PlanEntry
+                plan = BatchPlan(iteration=it, entries=(PlanEntry(b, p, level, 0),))
+                dev.step(plan, mask, pool, visible_block_lists(mask), [post])
+                frames = mask.visible_frames(b)
+                pc = cost.pass_cost(frames)
+                emitted_block = b if p == sched.emit_pass else None
+                if emitted_block is not None:
+                    emitted_order.append(b)
+                pre_pool = pool
+                if p == sched.cache_pass:
+                    newer = pool.insert(b, dev.kv_handle(b))
+                    for gone in pool.evicted_by(newer):
+                        dev.release(gone)
+                    pool = newer
+                dec = cost.decode_cost() if (emitted_block is not None and cost.decode > 0.0) else 0.0
+                modeled += pc + dec
+                trace.append(TraceEvent(
+                    iteration=it,
+                    entries=[{"block": b, "pass_index": p, "noise_level": level, "worker": 0,
+                              "conditioning_id": cond.id, "queries": S,
+                              "visible_frames": frames, "modeled_cost": pc}],
+                    wall_seconds=0.0, modeled_exec=pc, modeled_comm=0.0, modeled_stall=0.0,
+                    modeled_decode=dec, modeled_clock=modeled, wall_clock=0.0,
+                    pool_blocks=len(pre_pool.block_indices),
+                    pool_frames=pre_pool.frame_count(), pool_state=pre_pool.state_dump(),
+                    emitted_block=emitted_block,
+                    emitted_video_frames=(S * config.video_frames_per_latent
+                                          if emitted_block is not None else None)))
+                it += 1
+        dev.fill_wall_times(trace.events)
+        outputs = {blk: dev.emitted_host(blk) for blk in emitted_order}
+    finally:
+        sess.close()
+    return RunResult(outputs=outputs, trace=trace, pool=pool, emitted_order=emitted_order)
