@@ -1,0 +1,335 @@
+// tcgen05 bf16 GEMM with fused epilogues -- the QKV / O / cross-attn /
+// FFN / patch-embed / head / text projections of the Wan2.1-shaped DiT.
+//
+//   C[M,N] = epi( A[M,K] . B[N,K]^T + bias )      A, B bf16, K-major
+//
+// Persistent, warp-specialised, one CTA per SM:
+//   warp 0      TMA producer  (A tile 128x64, B tile BNx64, 128B swizzle)
+//   warp 1      MMA issuer    (tcgen05.mma kind::f16, M=128, N=BN, K=16)
+//               + TMEM owner  (2 accumulators x BN fp32 columns)
+//   warps 2..5  epilogue      (tcgen05.ld 32x32b -> fused op -> global)
+// Pipelines: smem ring full/empty (TMA <-> MMA), TMEM full/empty
+// (MMA <-> epilogue) so the epilogue of tile i overlaps the MMAs of i+1.
+// Tile order is M-fastest inside an N band so the 148 concurrent tiles
+// share B (weights) and stream A (activations) once from L2.
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+#include <stdint.h>
+
+#include "bc_common.h"
+#include "gemm.h"
+#include "sm100.cuh"
+
+namespace bc {
+
+namespace {
+
+constexpr int BM = 128;
+constexpr int BK = 64;  // 64 bf16 = 128 B = one swizzle atom row
+constexpr int kThreads = 192;
+
+template <int BN>
+struct GemmCfg {
+  static constexpr int kStages = BN >= 256 ? 4 : (BN >= 128 ? 6 : 8);
+  static constexpr int kABytes = BM * BK * 2;
+  static constexpr int kBBytes = BN * BK * 2;
+  static constexpr int kStageBytes = kABytes + kBBytes;
+  static constexpr int kTmemCols = 2 * BN >= 32 ? 2 * BN : 32;
+  static constexpr size_t kSmem = 1024 /*align slack*/ + (size_t)kStages * kStageBytes + 256;
+};
+
+__device__ __forceinline__ float gelu_tanh(float x) {
+  const float k0 = 0.7978845608028654f, k1 = 0.044715f;
+  return 0.5f * x * (1.0f + tanhf(k0 * (x + k1 * x * x * x)));
+}
+
+template <int BN, int MODE>
+__global__ void __launch_bounds__(kThreads, 1)
+    gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
+                void* __restrict__ c_ptr, int M, int N, int K, const float* __restrict__ bias,
+                const float* __restrict__ gate, int gate_stride, int rows_per_gate) {
+  using Cfg = GemmCfg<BN>;
+  constexpr int S = Cfg::kStages;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sa = smem;
+  uint8_t* sb = smem + S * Cfg::kABytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * Cfg::kStageBytes);
+  uint64_t* empty = full + S;
+  uint64_t* tfull = empty + S;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const uint32_t warp = warp_id();
+  const int num_m = (M + BM - 1) / BM;
+  const int num_n = N / BN;
+  const int num_tiles = num_m * num_n;
+  const int num_kb = K / BK;
+
+  if (warp == 0 && lane_id() == 0) {
+    tma_prefetch(&map_a);
+    tma_prefetch(&map_b);
+    for (int i = 0; i < S; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&tfull[i], 1);
+      mbar_init(&tempty[i], 128);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc<Cfg::kTmemCols>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane_id() == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+        const int m0 = (tile % num_m) * BM;
+        const int n0 = (tile / num_m) * BN;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_arrive_expect_tx(&full[stage], Cfg::kStageBytes);
+          tma_load_2d(sa + stage * Cfg::kABytes, &map_a, &full[stage], kb * BK, m0);
+          tma_load_2d(sb + stage * Cfg::kBBytes, &map_b, &full[stage], kb * BK, n0);
+          if (++stage == S) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    constexpr uint32_t idesc = idesc_bf16(BM, BN);
+    int stage = 0;
+    uint32_t phase = 0;
+    int it = 0;
+    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
+      const int acc = it & 1;
+      const uint32_t acc_phase = (it >> 1) & 1;
+      mbar_wait(&tempty[acc], acc_phase ^ 1);
+      tc_fence_after();
+      const uint32_t d_tmem = tmem_base + acc * BN;
+      for (int kb = 0; kb < num_kb; ++kb) {
+        mbar_wait(&full[stage], phase);
+        tc_fence_after();
+        if (elect_one()) {
+          const uint32_t a0 = smem_u32(sa + stage * Cfg::kABytes);
+          const uint32_t b0 = smem_u32(sb + stage * Cfg::kBBytes);
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) {
+            const uint64_t ad = desc_sw128(a0 + k * 32, 16, 1024);
+            const uint64_t bd = desc_sw128(b0 + k * 32, 16, 1024);
+            mma_bf16_ss(d_tmem, ad, bd, idesc, (kb | k) != 0);
+          }
+          mma_commit(&empty[stage]);
+          if (kb == num_kb - 1) mma_commit(&tfull[acc]);
+        }
+        __syncwarp();
+        if (++stage == S) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    }
+  } else {
+    // epilogue: warp w covers TMEM lanes 32*(w%4) .. +31  (rows of the tile)
+    const uint32_t quad = warp & 3;
+    const uint32_t row_in_tile = quad * 32 + lane_id();
+    int it = 0;
+    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
+      const int acc = it & 1;
+      const uint32_t acc_phase = (it >> 1) & 1;
+      const int m0 = (tile % num_m) * BM;
+      const int n0 = (tile / num_m) * BN;
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      const int row = m0 + (int)row_in_tile;
+      const bool live = row < M;
+#pragma unroll 1
+      for (int c = 0; c < BN; c += 32) {
+        uint32_t r[32];
+        __syncwarp();
+        tmem_ld32(tmem_base + ((quad * 32) << 16) + acc * BN + c, r);
+        tmem_ld_wait();
+        if (live) {
+        const int col = n0 + c;
+        float v[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]) + (bias ? __ldg(bias + col + j) : 0.0f);
+        if (MODE == kEpiStoreBf16 || MODE == kEpiGeluBf16) {
+          if (MODE == kEpiGeluBf16) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] = gelu_tanh(v[j]);
+          }
+          uint4* dst = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(c_ptr) + (size_t)row * N + col);
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            uint4 pk;
+            pk.x = pack_bf16(v[q * 8 + 0], v[q * 8 + 1]);
+            pk.y = pack_bf16(v[q * 8 + 2], v[q * 8 + 3]);
+            pk.z = pack_bf16(v[q * 8 + 4], v[q * 8 + 5]);
+            pk.w = pack_bf16(v[q * 8 + 6], v[q * 8 + 7]);
+            dst[q] = pk;
+          }
+        } else if (MODE == kEpiStoreF32) {
+          float4* dst = reinterpret_cast<float4*>(static_cast<float*>(c_ptr) + (size_t)row * N + col);
+#pragma unroll
+          for (int q = 0; q < 8; ++q) dst[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+        } else {  // kEpiResidualF32: C += gate * v
+          float4* dst = reinterpret_cast<float4*>(static_cast<float*>(c_ptr) + (size_t)row * N + col);
+          const float* g = gate ? gate + (size_t)(row / rows_per_gate) * gate_stride + col : nullptr;
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            float4 o = dst[q];
+            float g0 = 1.f, g1 = 1.f, g2 = 1.f, g3 = 1.f;
+            if (g) {
+              g0 = __ldg(g + 4 * q);
+              g1 = __ldg(g + 4 * q + 1);
+              g2 = __ldg(g + 4 * q + 2);
+              g3 = __ldg(g + 4 * q + 3);
+            }
+            o.x += g0 * v[4 * q];
+            o.y += g1 * v[4 * q + 1];
+            o.z += g2 * v[4 * q + 2];
+            o.w += g3 * v[4 * q + 3];
+            dst[q] = o;
+          }
+        }
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&tempty[acc]);
+    }
+  }
+  __syncthreads();
+  if (warp == 1) tmem_dealloc<Cfg::kTmemCols>(tmem_base);
+}
+
+// ---------------------------------------------------------------- host side
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+int sm_count() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+template <int BN, int MODE>
+int launch(const CUtensorMap& ma, const CUtensorMap& mb, void* C, int M, int N, int K,
+           const float* bias, const float* gate, int gate_stride, int rows_per_gate,
+           cudaStream_t st) {
+  using Cfg = GemmCfg<BN>;
+  static bool attr = false;
+  if (!attr) {
+    BC_CUDA(cudaFuncSetAttribute(gemm_kernel<BN, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)Cfg::kSmem));
+    attr = true;
+  }
+  const int tiles = ((M + BM - 1) / BM) * (N / BN);
+  const int grid = tiles < sm_count() ? tiles : sm_count();
+  gemm_kernel<BN, MODE><<<grid, kThreads, Cfg::kSmem, st>>>(ma, mb, C, M, N, K, bias, gate,
+                                                             gate_stride, rows_per_gate);
+  BC_LAUNCHED();
+  return BC_OK;
+}
+
+template <int BN>
+int dispatch_mode(int mode, const CUtensorMap& ma, const CUtensorMap& mb, void* C, int M, int N,
+                  int K, const float* bias, const float* gate, int gs, int rpg, cudaStream_t st) {
+  switch (mode) {
+    case kEpiStoreBf16: return launch<BN, kEpiStoreBf16>(ma, mb, C, M, N, K, bias, gate, gs, rpg, st);
+    case kEpiGeluBf16: return launch<BN, kEpiGeluBf16>(ma, mb, C, M, N, K, bias, gate, gs, rpg, st);
+    case kEpiStoreF32: return launch<BN, kEpiStoreF32>(ma, mb, C, M, N, K, bias, gate, gs, rpg, st);
+    case kEpiResidualF32: return launch<BN, kEpiResidualF32>(ma, mb, C, M, N, K, bias, gate, gs, rpg, st);
+  }
+  return bc_fail(BC_ERR_CONTRACT, "gemm: unknown epilogue mode %d", mode);
+}
+
+}  // namespace
+
+int make_tmap_2d(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer,
+                 uint64_t row_stride_bytes, uint32_t box_inner, uint32_t box_outer) {
+  auto fn = encode_fn();
+  if (!fn) return bc_fail(BC_ERR_CUDA, "cuTensorMapEncodeTiled unavailable (driver too old or no GPU)");
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {row_stride_bytes};
+  cuuint32_t box[2] = {box_inner, box_outer};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box,
+                  estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return bc_fail(BC_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  return BC_OK;
+}
+
+int num_sms() { return sm_count(); }
+
+int gemm_plan_bn(int M, int N) {
+  // choose the widest tile that still fills the machine reasonably
+  const int sms = sm_count();
+  const int mt = (M + BM - 1) / BM;
+  if (N % 256 == 0) {
+    const int t256 = mt * (N / 256);
+    const double waves256 = (double)t256 / sms;
+    const int t128 = mt * (N / 128);
+    const double waves128 = (double)t128 / sms;
+    // efficiency = work / (ceil(waves) * sms): prefer 256 unless 128 is clearly better
+    const double e256 = waves256 / (double)((t256 + sms - 1) / sms);
+    const double e128 = waves128 / (double)((t128 + sms - 1) / sms);
+    if (e256 >= e128 - 0.05) return 256;
+    return 128;
+  }
+  if (N % 128 == 0) return 128;
+  return 64;
+}
+
+int gemm_run(const GemmArgs& g, cudaStream_t st) {
+  if (g.K % BK || g.N % 64 || g.M < 1)
+    return bc_fail(BC_ERR_CONTRACT, "gemm: need K %% 64 == 0, N %% 64 == 0 (M=%d N=%d K=%d)", g.M, g.N, g.K);
+  const int bn = g.bn ? g.bn : gemm_plan_bn(g.M, g.N);
+  CUtensorMap ma, mb;
+  int rc = make_tmap_2d(&ma, g.A, g.K, g.M, (uint64_t)g.K * 2, BK, BM);
+  if (rc) return rc;
+  rc = make_tmap_2d(&mb, g.B, g.K, g.N, (uint64_t)g.K * 2, BK, bn);
+  if (rc) return rc;
+  switch (bn) {
+    case 256: return dispatch_mode<256>(g.mode, ma, mb, g.C, g.M, g.N, g.K, g.bias, g.gate, g.gate_stride, g.rows_per_gate, st);
+    case 128: return dispatch_mode<128>(g.mode, ma, mb, g.C, g.M, g.N, g.K, g.bias, g.gate, g.gate_stride, g.rows_per_gate, st);
+    case 64: return dispatch_mode<64>(g.mode, ma, mb, g.C, g.M, g.N, g.K, g.bias, g.gate, g.gate_stride, g.rows_per_gate, st);
+  }
+  return bc_fail(BC_ERR_CONTRACT, "gemm: bad tile width %d", bn);
+}
+
+}  // namespace bc
+
+extern "C" int bc_gemm_bf16(const void* A, const void* B, void* C, int32_t M, int32_t N, int32_t K,
+                            int32_t mode, const float* bias, const float* gate, int32_t gate_stride,
+                            int32_t rows_per_gate, void* stream) {
+  // mode bits 0-7: epilogue; bits 8-15: forced tile width (0 = auto)
+  bc::GemmArgs g{A, B, C, M, N, K, mode & 0xff, bias, gate, gate_stride,
+                 rows_per_gate > 0 ? rows_per_gate : 1, (mode >> 8) & 0xff ? ((mode >> 8) & 0xff) * 64 : 0};
+  return bc::gemm_run(g, (cudaStream_t)stream);
+}

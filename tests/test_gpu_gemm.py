@@ -1,0 +1,61 @@
+"""tcgen05 GEMM (csrc/gemm.cu) vs a plain PyTorch fp32 reference of the same
+op on the same bf16 inputs.  Tolerances: fp32 outputs rel-L2 <= 1e-5
+(accumulation order only); bf16 outputs rel-L2 <= 4e-3 (one bf16 rounding)."""
+
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+from paper_2511_20426_b200 import _native as N
+
+
+def gemm(A, B, C, mode, bias=None, gate=None, gate_stride=0, rows_per_gate=1, bn=0):
+    M, K = A.shape
+    Nn = B.shape[0]
+    N.check(N.lib().bc_gemm_bf16(N.ptr(A), N.ptr(B), N.ptr(C), M, Nn, K, mode | ((bn // 64) << 8),
+                                 N.ptr(bias), N.ptr(gate), gate_stride, rows_per_gate,
+                                 N.stream_ptr()), "gemm")
+
+
+def rel(a, b):
+    return float((a.float() - b.float()).norm() / b.float().norm().clamp_min(1e-30))
+
+
+SHAPES = [(128, 256, 64), (300, 128, 128), (4680, 1536, 1536), (1000, 768, 256),
+          (192, 64, 256), (4680, 4608, 1536), (512, 1536, 4096), (9360, 8960, 1536)]
+
+
+@pytest.mark.parametrize("M,Nn,K", SHAPES)
+@pytest.mark.parametrize("bn", [0, 64, 128, 256])
+def test_gemm_modes(M, Nn, K, bn):
+    if bn and Nn % bn:
+        pytest.skip("tile width does not divide N")
+    g = torch.Generator(device="cuda").manual_seed(M * 7 + Nn + K)
+    A = torch.randn(M, K, device="cuda", generator=g).bfloat16()
+    B = (torch.randn(Nn, K, device="cuda", generator=g) / K ** 0.5).bfloat16()
+    bias = torch.randn(Nn, device="cuda", generator=g)
+    ref = A.float() @ B.float().T + bias
+    C = torch.empty(M, Nn, device="cuda", dtype=torch.float32)
+    gemm(A, B, C, 2, bias, bn=bn)
+    assert rel(C, ref) < 1e-5
+    Cb = torch.empty(M, Nn, device="cuda", dtype=torch.bfloat16)
+    gemm(A, B, Cb, 0, bias, bn=bn)
+    assert rel(Cb, ref) < 4e-3
+    gemm(A, B, Cb, 1, bias, bn=bn)
+    assert rel(Cb, torch.nn.functional.gelu(ref, approximate="tanh")) < 4e-3
+    rows_per_gate = 97
+    groups = (M + rows_per_gate - 1) // rows_per_gate
+    gate = torch.randn(groups, Nn, device="cuda", generator=g)
+    X = torch.randn(M, Nn, device="cuda", generator=g)
+    want = X + gate.repeat_interleave(rows_per_gate, 0)[:M] * ref
+    gemm(A, B, X, 3, bias, gate, Nn, rows_per_gate, bn=bn)
+    assert rel(X, want) < 1e-5
+
+
+def test_gemm_rejects_bad_shapes():
+    A = torch.zeros(128, 96, device="cuda", dtype=torch.bfloat16)
+    B = torch.zeros(128, 96, device="cuda", dtype=torch.bfloat16)
+    C = torch.zeros(128, 128, device="cuda")
+    with pytest.raises(Exception):
+        gemm(A, B, C, 2)
