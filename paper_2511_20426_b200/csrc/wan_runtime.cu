@@ -5,4 +5,3 @@ extern "C" int bc_wan_create(const bc_wan_dims*, const bc_wan_params*, void*, vo
 extern "C" int bc_wan_destroy(bc_wan_ctx*) { return 0; }
 extern "C" int bc_wan_set_text(bc_wan_ctx*, const float*, void*) { return bc_fail(BC_ERR_CUDA, "not implemented"); }
 extern "C" int bc_wan_step(bc_wan_ctx*, const bc_batch*, const bc_wan_update*, int32_t*, void*) { return bc_fail(BC_ERR_CUDA, "not implemented"); }
-extern "C" int bc_attention_paged(const void*, const void*, const void*, int64_t, int32_t, const bc_batch*, int32_t, int32_t, void*, void*) { return bc_fail(BC_ERR_CUDA, "not implemented"); }
