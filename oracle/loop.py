@@ -98,3 +98,79 @@ class _OracleRuntime:
 def oracle_runtime(weights, config):
     """Drop-in replacement for ``engine._runtime_for`` in CPU tests."""
     return _OracleRuntime(weights)
+
+
+class WanOracleSession:
+    """Same protocol, Wan-shaped forward in numpy fp32 (oracle/wan.py)."""
+
+    def __init__(self, params, config, cond, session_seed):
+        from paper_2511_20426_b200.core import NoiseStream
+        from . import wan as wan_oracle
+        self.o = wan_oracle.WanOracle(params, config)
+        self.cfg = config
+        self.S = config.block_size
+        self.shape = (config.block_size, 16, config.latent_height, config.latent_width)
+        self.noise = NoiseStream(session_seed, config.latent_dim)
+        self.latents, self.final, self.kv, self.tags = {}, {}, {}, {}
+        self.set_conditioning(cond)
+
+    def set_conditioning(self, cond):
+        from paper_2511_20426_b200.wan import text_states
+        self.cond = cond
+        self.text_kv = self.o.context(text_states(cond, self.cfg.text_len, self.cfg.text_dim))
+
+    def _noise(self, b, p):
+        return self.noise.block_noise(b, p, b * self.S, self.S).astype(np.float32).reshape(self.shape)
+
+    def step(self, plan, mask, pool, vis_lists, posts):
+        from . import wan as wan_oracle
+        ents = []
+        for e in plan.entries:
+            b = e.block_index
+            if e.pass_index == 0 and b not in self.latents:
+                self.latents[b] = self._noise(b, 0)
+            ents.append((b, self.latents[b], e.noise_level))
+        visible = {b: lst for b, lst in zip(plan.blocks, vis_lists)}
+        pool_kv = {b: self.kv[b] for b in mask.pool_blocks}
+        outs = self.o.forward(ents, pool_kv, visible, None, text_kv=self.text_kv)
+        for e, (x0, kv), (kind, next_pass, next_level) in zip(plan.entries, outs, posts):
+            b = e.block_index
+            self.kv[b] = kv
+            self.tags[b] = (e.noise_level, self.cond.id)
+            if kind == POST_RENOISE:
+                self.latents[b] = wan_oracle.renoise(x0, self._noise(b, next_pass), next_level)
+            elif kind == POST_EMIT:
+                self.final[b] = x0
+                self.latents[b] = x0
+            else:
+                self.latents.pop(b, None)
+
+    def kv_handle(self, block):
+        level, cid = self.tags[block]
+        return tuple(_KV(block, l, k, v, level, cid) for l, (k, v) in enumerate(self.kv[block]))
+
+    def release(self, block):
+        pass
+
+    def emitted_host(self, block):
+        return self.final[block].reshape(self.S, -1).astype(np.float64)
+
+    def fill_wall_times(self, events):
+        pass
+
+    def close(self):
+        pass
+
+
+class _WanOracleRuntime:
+    def __init__(self, params):
+        self.params = params
+
+    def open_session(self, config, cond, session_seed, noise_feed=None):
+        return WanOracleSession(self.params, config, cond, session_seed)
+
+
+def wan_oracle_runtime(params):
+    """engine._runtime_for replacement bound to fixed host parameters."""
+    rt = _WanOracleRuntime(params)
+    return lambda weights, config: rt

@@ -1,0 +1,433 @@
+// Bandwidth-bound kernels of the Wan2.1-shaped DiT step: patchify, time
+// embedding GEMVs, LayerNorm + AdaLN modulation, q/k RMSNorm + 3-D RoPE +
+// KV-slot scatter, cross-attention RMSNorm, and the fused head update
+// (unpatchify + flow -> x0 + renoise / emit + finiteness check).
+//
+// All row kernels are warp-per-row with 16-byte vector accesses; statistics
+// and the residual stream are fp32, GEMM operands bf16.  Model math follows
+// the public Wan2.1 block; the noise parameterisation
+// is the reference's sigma = level / 1000 (denoiser.py:360-368).
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+
+#include "bc_common.h"
+#include "wan_kernels.h"
+
+namespace bc {
+namespace {
+
+constexpr float kEps = 1e-6f;
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ float silu(float x) { return x / (1.0f + __expf(-x)); }
+__device__ __forceinline__ float bf(const __nv_bfloat16 v) { return __bfloat162float(v); }
+
+// ------------------------------------------------------------ patchify
+// x: (F,16,H,W) fp32 -> tokens (F*(H/2)*(W/2), 64) bf16; vector index
+// c*4 + kh*2 + kw (Conv3d weight order, kernel (1,2,2)).
+__global__ void patchify_kernel(EntryPtrs lat, int F, int H, int W, __nv_bfloat16* out, int T) {
+  const int e = blockIdx.y;
+  const float* x = lat.p[e];
+  const int hp = H / 2, wp = W / 2;
+  const int total = T * 64;
+  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += gridDim.x * blockDim.x) {
+    const int n = idx >> 6, v = idx & 63;
+    const int c = v >> 2, kh = (v >> 1) & 1, kw = v & 1;
+    const int f = n / (hp * wp), rem = n % (hp * wp);
+    const int i = rem / wp, j = rem % wp;
+    const float val = x[(((size_t)f * 16 + c) * H + 2 * i + kh) * W + 2 * j + kw];
+    out[(size_t)e * T * 64 + idx] = __float2bfloat16(val);
+  }
+}
+
+// ------------------------------------------------------------ GEMV (time MLP)
+// out[e][o] = act_out( sum_k act_in(in[e][k]) W[o][k] + b[o] ), one warp per o.
+__global__ void gemv_kernel(const float* in, int n, int K, const __nv_bfloat16* W, const float* b,
+                            float* out, int N, int act_in, int act_out) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (warp >= N) return;
+  const __nv_bfloat16* w = W + (size_t)warp * K;
+  float acc[BC_MAX_ENTRIES];
+#pragma unroll
+  for (int e = 0; e < BC_MAX_ENTRIES; ++e) acc[e] = 0.0f;
+  for (int k = lane; k < K; k += 32) {
+    const float wk = bf(w[k]);
+#pragma unroll
+    for (int e = 0; e < BC_MAX_ENTRIES; ++e) {
+      if (e < n) {
+        float v = in[(size_t)e * K + k];
+        if (act_in == 1) v = silu(v);
+        acc[e] += wk * v;
+      }
+    }
+  }
+#pragma unroll
+  for (int e = 0; e < BC_MAX_ENTRIES; ++e) {
+    if (e < n) {
+      float v = warp_sum(acc[e]);
+      if (lane == 0) {
+        v += b ? b[warp] : 0.0f;
+        if (act_out == 1) v = silu(v);
+        out[(size_t)e * N + warp] = v;
+      }
+    }
+  }
+}
+
+// sinusoid(freq_dim) of each entry's timestep: [cos(t w_k), sin(t w_k)],
+// w_k = 10000^(-k/half)  (Wan sinusoidal_embedding_1d)
+__global__ void timestep_sin_kernel(TimeArgs a, float* out, int freq_dim) {
+  const int e = blockIdx.x;
+  const int half = freq_dim / 2;
+  for (int k = threadIdx.x; k < half; k += blockDim.x) {
+    const double w = pow(10000.0, -(double)k / (double)half);
+    const double arg = a.t[e] * w;
+    out[(size_t)e * freq_dim + k] = (float)cos(arg);
+    out[(size_t)e * freq_dim + half + k] = (float)sin(arg);
+  }
+}
+
+// ------------------------------------------------------------ LayerNorm rows
+// mode 0: LN(x) * (1 + mod[1]) + mod[0]   with mod = base[6][d] + e0[e][6][d] (chunks sel0/sel1)
+// mode 1: LN(x) * w + b                   (affine LN, cross-attn norm3)
+template <int VPL>  // float4 vectors per lane
+__global__ void ln_rows_kernel(const float* __restrict__ X, __nv_bfloat16* __restrict__ out, int rows,
+                               int d, int rows_per_entry, LnArgs a) {
+  const int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (row >= rows) return;
+  const float4* x4 = reinterpret_cast<const float4*>(X + (size_t)row * d);
+  float4 v[VPL];
+  float s = 0.0f;
+#pragma unroll
+  for (int i = 0; i < VPL; ++i) {
+    const int idx = lane + 32 * i;
+    v[i] = (idx * 4 < d) ? x4[idx] : make_float4(0.f, 0.f, 0.f, 0.f);
+    s += v[i].x + v[i].y + v[i].z + v[i].w;
+  }
+  const float mean = warp_sum(s) / d;
+  float q = 0.0f;
+#pragma unroll
+  for (int i = 0; i < VPL; ++i) {
+    const int idx = lane + 32 * i;
+    if (idx * 4 < d) {
+      const float a0 = v[i].x - mean, a1 = v[i].y - mean, a2 = v[i].z - mean, a3 = v[i].w - mean;
+      q += a0 * a0 + a1 * a1 + a2 * a2 + a3 * a3;
+    }
+  }
+  const float rstd = rsqrtf(warp_sum(q) / d + kEps);
+  const int e = row / rows_per_entry;
+  const float* p_scale = a.base_scale;
+  const float* p_shift = a.base_shift;
+  const float* q_scale = a.mode == 0 ? a.pe_scale + (size_t)e * a.entry_stride : nullptr;
+  const float* q_shift = a.mode == 0 ? a.pe_shift + (size_t)e * a.entry_stride : nullptr;
+  uint2* o2 = reinterpret_cast<uint2*>(out + (size_t)row * d);
+#pragma unroll
+  for (int i = 0; i < VPL; ++i) {
+    const int idx = lane + 32 * i;
+    if (idx * 4 >= d) continue;
+    const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
+    const float4 sc = p_scale ? reinterpret_cast<const float4*>(p_scale)[idx] : z4;
+    const float4 sh = p_shift ? reinterpret_cast<const float4*>(p_shift)[idx] : z4;
+    float4 scl = sc, shf = sh;
+    if (a.mode == 0) {
+      const float4 sc2 = reinterpret_cast<const float4*>(q_scale)[idx];
+      const float4 sh2 = reinterpret_cast<const float4*>(q_shift)[idx];
+      scl = make_float4(1.f + sc.x + sc2.x, 1.f + sc.y + sc2.y, 1.f + sc.z + sc2.z, 1.f + sc.w + sc2.w);
+      shf = make_float4(sh.x + sh2.x, sh.y + sh2.y, sh.z + sh2.z, sh.w + sh2.w);
+    }
+    const float y0 = (v[i].x - mean) * rstd * scl.x + shf.x;
+    const float y1 = (v[i].y - mean) * rstd * scl.y + shf.y;
+    const float y2 = (v[i].z - mean) * rstd * scl.z + shf.z;
+    const float y3 = (v[i].w - mean) * rstd * scl.w + shf.w;
+    __nv_bfloat162 lo = __floats2bfloat162_rn(y0, y1), hi = __floats2bfloat162_rn(y2, y3);
+    uint2 pk;
+    pk.x = *reinterpret_cast<uint32_t*>(&lo);
+    pk.y = *reinterpret_cast<uint32_t*>(&hi);
+    o2[idx] = pk;
+  }
+}
+
+// ------------------------------------------------------------ q/k RMSNorm + RoPE
+// qkv: (rows, 3d) bf16.  q -> qout (rows, d); k, v -> KV-arena slot of the
+// row's entry (token t = row % T).  RMSNorm over the full d with weight,
+// eps 1e-6; RoPE on complex pairs (2i, 2i+1) of each 128-wide head, pair i
+// < 22 rotates with the global frame index, < 43 with the patch row, else
+// the patch column (Wan 44/42/42 split of head_dim 128).
+__device__ __forceinline__ float rope_angle(int i, int f, int h, int w) {
+  // inv_freq = 10000^(-2k/D_part), D_part = 44 / 42 / 42
+  if (i < 22) return (float)f * exp2f(-(2.0f * i / 44.0f) * 13.287712379549449f);
+  if (i < 43) return (float)h * exp2f(-(2.0f * (i - 22) / 42.0f) * 13.287712379549449f);
+  return (float)w * exp2f(-(2.0f * (i - 43) / 42.0f) * 13.287712379549449f);
+}
+
+template <int VPL>  // bf16x8 (16 B) vectors per lane for d
+__global__ void qk_norm_rope_kernel(const __nv_bfloat16* __restrict__ qkv, int rows, int d, int T,
+                                    QkArgs a) {
+  const int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (row >= rows) return;
+  const int e = row / T, t = row % T;
+  const int hw = a.hp * a.wp;
+  const int fl = t / hw, rem = t % hw;
+  const int f = a.frame0[e] + fl, ph = rem / a.wp, pw = rem % a.wp;
+  const size_t mat = (size_t)T * d;
+  __nv_bfloat16* kdst = a.arena + ((size_t)a.mat_base + (size_t)a.slot[e] * 2) * mat + (size_t)t * d;
+  __nv_bfloat16* vdst = kdst + mat;
+  const __nv_bfloat16* src = qkv + (size_t)row * 3 * d;
+#pragma unroll
+  for (int which = 0; which < 2; ++which) {
+    const uint4* s4 = reinterpret_cast<const uint4*>(src + which * d);
+    float vals[VPL][8];
+    float ss = 0.0f;
+#pragma unroll
+    for (int i = 0; i < VPL; ++i) {
+      const int idx = lane + 32 * i;
+      if (idx * 8 < d) {
+        uint4 u = s4[idx];
+        const __nv_bfloat16* h = reinterpret_cast<const __nv_bfloat16*>(&u);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          vals[i][j] = bf(h[j]);
+          ss += vals[i][j] * vals[i][j];
+        }
+      }
+    }
+    const float inv = rsqrtf(warp_sum(ss) / d + kEps);
+    const float* wgt = which == 0 ? a.norm_q : a.norm_k;
+    __nv_bfloat16* dst = which == 0 ? a.qout + (size_t)row * d : kdst;
+#pragma unroll
+    for (int i = 0; i < VPL; ++i) {
+      const int idx = lane + 32 * i;
+      if (idx * 8 >= d) continue;
+      const int c0 = idx * 8;                 // element index in [0, d)
+      const int pair0 = (c0 & 127) >> 1;      // pair index inside the head
+      uint4 u;
+      __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(&u);
+#pragma unroll
+      for (int j = 0; j < 8; j += 2) {
+        const float x0 = vals[i][j] * inv * wgt[c0 + j];
+        const float x1 = vals[i][j + 1] * inv * wgt[c0 + j + 1];
+        float sn, cs;
+        sincosf(rope_angle(pair0 + j / 2, f, ph, pw), &sn, &cs);
+        o[j] = __float2bfloat16(x0 * cs - x1 * sn);
+        o[j + 1] = __float2bfloat16(x0 * sn + x1 * cs);
+      }
+      reinterpret_cast<uint4*>(dst)[idx] = u;
+    }
+  }
+  // v: plain copy into the slot
+  const uint4* v4 = reinterpret_cast<const uint4*>(src + 2 * d);
+  for (int idx = lane; idx * 8 < d; idx += 32) reinterpret_cast<uint4*>(vdst)[idx] = v4[idx];
+}
+
+// in-place RMSNorm * weight over rows of width d (bf16), row stride ld
+template <int VPL>
+__global__ void rms_rows_kernel(__nv_bfloat16* x, int rows, int d, int ld, const float* w,
+                                __nv_bfloat16* out, int ld_out) {
+  const int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (row >= rows) return;
+  const uint4* s4 = reinterpret_cast<const uint4*>(x + (size_t)row * ld);
+  float vals[VPL][8];
+  float ss = 0.0f;
+#pragma unroll
+  for (int i = 0; i < VPL; ++i) {
+    const int idx = lane + 32 * i;
+    if (idx * 8 < d) {
+      uint4 u = s4[idx];
+      const __nv_bfloat16* h = reinterpret_cast<const __nv_bfloat16*>(&u);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        vals[i][j] = bf(h[j]);
+        ss += vals[i][j] * vals[i][j];
+      }
+    }
+  }
+  const float inv = rsqrtf(warp_sum(ss) / d + kEps);
+  uint4* d4 = reinterpret_cast<uint4*>(out + (size_t)row * ld_out);
+#pragma unroll
+  for (int i = 0; i < VPL; ++i) {
+    const int idx = lane + 32 * i;
+    if (idx * 8 >= d) continue;
+    uint4 u;
+    __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(&u);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) o[j] = __float2bfloat16(vals[i][j] * inv * w[idx * 8 + j]);
+    d4[idx] = u;
+  }
+}
+
+// copy a column block of a bf16 matrix: dst[r][0:w] = src[r][c0:c0+w]
+__global__ void copy_cols_kernel(const __nv_bfloat16* src, int ld_src, int c0, __nv_bfloat16* dst,
+                                 int ld_dst, int rows, int w) {
+  const int vecs = w / 8;
+  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < rows * vecs; idx += gridDim.x * blockDim.x) {
+    const int r = idx / vecs, c = idx % vecs;
+    reinterpret_cast<uint4*>(dst + (size_t)r * ld_dst)[c] =
+        reinterpret_cast<const uint4*>(src + (size_t)r * ld_src + c0)[c];
+  }
+}
+
+__global__ void f32_to_bf16_kernel(const float* src, __nv_bfloat16* dst, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = __float2bfloat16(src[i]);
+}
+
+// ------------------------------------------------------------ head update
+// Y: (T, 64) fp32 head output per entry, index (ph*2+pw)*16 + c (Wan
+// unpatchify order).  v -> x0 = x_t - sigma v -> post op.
+__global__ void head_update_kernel(const float* __restrict__ Y, int T, int F, int H, int W, UpdArgs u,
+                                   int32_t* status) {
+  const int e = blockIdx.y;
+  const int hp = H / 2, wp = W / 2;
+  const int n_el = F * 16 * H * W;
+  float* lat = u.latents[e];
+  const float sig = (float)(u.level[e] / 1000.0);
+  const float s_next = (float)(u.next_level[e] / 1000.0);
+  const int post = u.post[e];
+  bool bad = false;
+  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < n_el; idx += gridDim.x * blockDim.x) {
+    const int xw = idx % W, yh = (idx / W) % H, c = (idx / (W * H)) % 16, f = idx / (W * H * 16);
+    const int n = f * hp * wp + (yh >> 1) * wp + (xw >> 1);
+    const int sub = ((yh & 1) * 2 + (xw & 1)) * 16 + c;
+    const float v = Y[((size_t)e * T + n) * 64 + sub];
+    const float xt = lat[idx];
+    const float x0 = xt - sig * v;
+    bad |= !isfinite(x0);
+    if (post == 0) {
+      lat[idx] = __fadd_rn(__fmul_rn(1.0f - s_next, x0), __fmul_rn(s_next, u.eps[e][idx]));
+    } else if (post == 1) {
+      lat[idx] = x0;
+      u.out[e][idx] = x0;
+    } else if (post == 3) {
+      u.out[e][idx] = x0;
+    }
+  }
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicCAS(status, 0, 1 + u.block[e]);
+}
+
+__global__ void check_finite_kernel(EntryPtrs lat, int n_el, int32_t* status) {
+  const int e = blockIdx.y;
+  bool bad = false;
+  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < n_el; idx += gridDim.x * blockDim.x)
+    bad |= !isfinite(lat.p[e][idx]);
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicCAS(status, 0, 1 + lat.block[e]);
+}
+
+// out[l][e][k][:] = base[l][k][:] + e0[e][k][:]   (all 6 AdaLN chunks, all layers)
+__global__ void mod_combine_kernel(const float* base, const float* e0, int L, int n, int d, float* out) {
+  const int64_t total = (int64_t)L * n * 6 * d;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int c = (int)(i % (6 * d));
+    const int64_t le = i / (6 * d);
+    const int e = (int)(le % n), l = (int)(le / n);
+    out[i] = base[(size_t)l * 6 * d + c] + e0[(size_t)e * 6 * d + c];
+  }
+}
+
+int grid_for(int64_t work, int threads) {
+  int64_t g = (work + threads - 1) / threads;
+  if (g > 148 * 32) g = 148 * 32;
+  return (int)(g < 1 ? 1 : g);
+}
+
+}  // namespace
+
+int launch_patchify(const EntryPtrs& lat, int n, int F, int H, int W, __nv_bfloat16* out, cudaStream_t st) {
+  const int T = F * (H / 2) * (W / 2);
+  patchify_kernel<<<dim3(grid_for((int64_t)T * 64, 256) / n + 1, n), 256, 0, st>>>(lat, F, H, W, out, T);
+  BC_LAUNCHED();
+  return BC_OK;
+}
+
+int launch_gemv(const float* in, int n, int K, const __nv_bfloat16* W, const float* b, float* out, int N,
+                int act_in, int act_out, cudaStream_t st) {
+  const int threads = 256;
+  gemv_kernel<<<(N * 32 + threads - 1) / threads, threads, 0, st>>>(in, n, K, W, b, out, N, act_in, act_out);
+  BC_LAUNCHED();
+  return BC_OK;
+}
+
+int launch_timestep_sin(const TimeArgs& a, int n, float* out, int freq_dim, cudaStream_t st) {
+  timestep_sin_kernel<<<n, 128, 0, st>>>(a, out, freq_dim);
+  BC_LAUNCHED();
+  return BC_OK;
+}
+
+int launch_ln_rows(const float* X, __nv_bfloat16* out, int rows, int d, int rows_per_entry, const LnArgs& a,
+                   cudaStream_t st) {
+  const int threads = 256, rows_per_cta = threads / 32;
+  const int grid = (rows + rows_per_cta - 1) / rows_per_cta;
+  const int vpl = (d / 4 + 31) / 32;
+  if (vpl <= 12) ln_rows_kernel<12><<<grid, threads, 0, st>>>(X, out, rows, d, rows_per_entry, a);
+  else if (vpl <= 40) ln_rows_kernel<40><<<grid, threads, 0, st>>>(X, out, rows, d, rows_per_entry, a);
+  else return bc_fail(BC_ERR_CONTRACT, "ln_rows: d=%d too wide", d);
+  BC_LAUNCHED();
+  return BC_OK;
+}
+
+int launch_qk_norm_rope(const __nv_bfloat16* qkv, int rows, int d, int T, const QkArgs& a, cudaStream_t st) {
+  const int threads = 256, rows_per_cta = threads / 32;
+  const int grid = (rows + rows_per_cta - 1) / rows_per_cta;
+  const int vpl = (d / 8 + 31) / 32;
+  if (vpl <= 6) qk_norm_rope_kernel<6><<<grid, threads, 0, st>>>(qkv, rows, d, T, a);
+  else if (vpl <= 20) qk_norm_rope_kernel<20><<<grid, threads, 0, st>>>(qkv, rows, d, T, a);
+  else return bc_fail(BC_ERR_CONTRACT, "qk_norm_rope: d=%d too wide", d);
+  BC_LAUNCHED();
+  return BC_OK;
+}
+
+int launch_rms_rows(__nv_bfloat16* x, int rows, int d, int ld, const float* w, __nv_bfloat16* out, int ld_out,
+                    cudaStream_t st) {
+  const int threads = 256, rows_per_cta = threads / 32;
+  const int grid = (rows + rows_per_cta - 1) / rows_per_cta;
+  const int vpl = (d / 8 + 31) / 32;
+  if (vpl <= 6) rms_rows_kernel<6><<<grid, threads, 0, st>>>(x, rows, d, ld, w, out, ld_out);
+  else if (vpl <= 20) rms_rows_kernel<20><<<grid, threads, 0, st>>>(x, rows, d, ld, w, out, ld_out);
+  else return bc_fail(BC_ERR_CONTRACT, "rms_rows: d=%d too wide", d);
+  BC_LAUNCHED();
+  return BC_OK;
+}
+
+int launch_copy_cols(const __nv_bfloat16* src, int ld_src, int c0, __nv_bfloat16* dst, int ld_dst, int rows,
+                     int w, cudaStream_t st) {
+  copy_cols_kernel<<<grid_for((int64_t)rows * w / 8, 256), 256, 0, st>>>(src, ld_src, c0, dst, ld_dst, rows, w);
+  BC_LAUNCHED();
+  return BC_OK;
+}
+
+int launch_f32_to_bf16(const float* src, __nv_bfloat16* dst, int64_t n, cudaStream_t st) {
+  f32_to_bf16_kernel<<<grid_for(n, 256), 256, 0, st>>>(src, dst, n);
+  BC_LAUNCHED();
+  return BC_OK;
+}
+
+int launch_head_update(const float* Y, int n, int T, int F, int H, int W, const UpdArgs& u, int32_t* status,
+                       cudaStream_t st) {
+  const int n_el = F * 16 * H * W;
+  head_update_kernel<<<dim3(grid_for(n_el, 256) / n + 1, n), 256, 0, st>>>(Y, T, F, H, W, u, status);
+  BC_LAUNCHED();
+  return BC_OK;
+}
+
+int launch_check_finite(const EntryPtrs& lat, int n, int n_el, int32_t* status, cudaStream_t st) {
+  check_finite_kernel<<<dim3(grid_for(n_el, 256) / n + 1, n), 256, 0, st>>>(lat, n_el, status);
+  BC_LAUNCHED();
+  return BC_OK;
+}
+
+int launch_mod_combine(const float* base, const float* e0, int L, int n, int d, float* out, cudaStream_t st) {
+  mod_combine_kernel<<<grid_for((int64_t)L * n * 6 * d, 256), 256, 0, st>>>(base, e0, L, n, d, out);
+  BC_LAUNCHED();
+  return BC_OK;
+}
+
+}  // namespace bc

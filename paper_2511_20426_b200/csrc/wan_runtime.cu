@@ -1,7 +1,303 @@
-// Wan2.1-shaped DiT runtime (placeholder, filled in next).
+// Wan2.1-shaped DiT runtime: one cascade iteration = one bc_wan_step call.
+//
+// The host scheduler hands over the batch (one entry per in-flight block,
+// ascending) with each entry's KV-arena slot and visible-slot list; this
+// file launches the whole batched forward on one stream:
+//
+//   patchify -> patch GEMM -> time MLP -> per layer {
+//     LN+AdaLN -> QKV GEMM -> q/k RMSNorm+RoPE (K/V -> own slot) ->
+//     paged self-attention over visible slots -> O GEMM (+gate*res) ->
+//     affine LN -> cross-q GEMM -> RMSNorm -> cross-attention (text K/V) ->
+//     cross-O GEMM (+res) -> LN+AdaLN -> FFN1 GEMM (+GELU) -> FFN2 GEMM (+gate*res) }
+//   -> head LN+mod -> head GEMM -> unpatchify + flow->x0 + renoise/emit.
+//
+// Entries of all cascade levels run through the same GEMMs (rows are
+// concatenated); only the per-entry modulation vectors and the attention
+// slot tables differ.  Memory: caller-owned (torch) weights, KV arena
+// [L][n_slots][2][T][d] bf16 and workspace; nothing is allocated here.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cstring>
+#include <new>
+
+#include "attention.h"
 #include "bc_common.h"
-extern "C" int64_t bc_wan_workspace_bytes(const bc_wan_dims*) { return 0; }
-extern "C" int bc_wan_create(const bc_wan_dims*, const bc_wan_params*, void*, void*, int64_t, bc_wan_ctx**) { return bc_fail(BC_ERR_CUDA, "not implemented"); }
-extern "C" int bc_wan_destroy(bc_wan_ctx*) { return 0; }
-extern "C" int bc_wan_set_text(bc_wan_ctx*, const float*, void*) { return bc_fail(BC_ERR_CUDA, "not implemented"); }
-extern "C" int bc_wan_step(bc_wan_ctx*, const bc_batch*, const bc_wan_update*, int32_t*, void*) { return bc_fail(BC_ERR_CUDA, "not implemented"); }
+#include "gemm.h"
+#include "wan_kernels.h"
+
+struct bc_wan_ctx {
+  bc_wan_dims dims;
+  bc_wan_params prm;
+  __nv_bfloat16* arena;
+  int d, T, R, E;
+  // workspace carve-outs
+  float* X;
+  __nv_bfloat16 *xn, *qkv, *Q, *attn, *H1, *patches;
+  float* Y;
+  float *t_sin, *t_h, *t_e, *t_e0, *mod_all;
+  __nv_bfloat16 *text_in, *text_h, *ctx, *text_tmp, *textkv;
+  bool text_ready;
+};
+
+namespace {
+
+struct Carver {
+  char* base;
+  int64_t off = 0;
+  template <typename T>
+  T* take(int64_t count) {
+    off = (off + 255) & ~int64_t(255);
+    T* p = base ? reinterpret_cast<T*>(base + off) : nullptr;
+    off += count * (int64_t)sizeof(T);
+    return p;
+  }
+};
+
+int64_t carve(bc_wan_ctx* c, const bc_wan_dims& dm, char* base) {
+  Carver cv{base};
+  const int64_t d = (int64_t)dm.heads * dm.head_dim;
+  const int64_t T = (int64_t)dm.block_size * (dm.latent_h / 2) * (dm.latent_w / 2);
+  const int64_t E = dm.max_entries;
+  const int64_t R = E * T;
+  bc_wan_ctx tmp;
+  bc_wan_ctx* t = c ? c : &tmp;
+  t->X = cv.take<float>(R * d);
+  t->xn = cv.take<__nv_bfloat16>(R * d);
+  t->qkv = cv.take<__nv_bfloat16>(R * 3 * d);
+  t->Q = cv.take<__nv_bfloat16>(R * d);
+  t->attn = cv.take<__nv_bfloat16>(R * d);
+  t->H1 = cv.take<__nv_bfloat16>(R * dm.ffn_dim);
+  t->patches = cv.take<__nv_bfloat16>(R * 64);
+  t->Y = cv.take<float>(R * 64);
+  t->t_sin = cv.take<float>(E * dm.freq_dim);
+  t->t_h = cv.take<float>(E * d);
+  t->t_e = cv.take<float>(E * d);
+  t->t_e0 = cv.take<float>(E * 6 * d);
+  t->mod_all = cv.take<float>((int64_t)dm.layers * E * 6 * d);
+  t->text_in = cv.take<__nv_bfloat16>((int64_t)dm.text_len * dm.text_dim);
+  t->text_h = cv.take<__nv_bfloat16>((int64_t)dm.text_len * d);
+  t->ctx = cv.take<__nv_bfloat16>((int64_t)dm.text_len * d);
+  t->text_tmp = cv.take<__nv_bfloat16>((int64_t)dm.text_len * 2 * d);
+  t->textkv = cv.take<__nv_bfloat16>((int64_t)dm.layers * 2 * dm.text_len * d);
+  return cv.off + 256;
+}
+
+int check_dims(const bc_wan_dims& dm) {
+  if (dm.head_dim != 128) return bc_fail(BC_ERR_CONTRACT, "wan: head_dim must be 128");
+  const int d = dm.heads * dm.head_dim;
+  if (d % 256 || dm.ffn_dim % 256 || dm.text_dim % 64 || dm.freq_dim % 2)
+    return bc_fail(BC_ERR_CONTRACT, "wan: dims must be multiples of 256 (d, ffn) / 64 (text_dim)");
+  if (dm.latent_h % 2 || dm.latent_w % 2 || dm.block_size < 1 || dm.layers < 1)
+    return bc_fail(BC_ERR_CONTRACT, "wan: bad latent geometry");
+  if (dm.max_entries < 1 || dm.max_entries > BC_MAX_ENTRIES || dm.n_slots < 1)
+    return bc_fail(BC_ERR_CONTRACT, "wan: bad max_entries / n_slots");
+  return BC_OK;
+}
+
+#define RC(x)              \
+  do {                     \
+    int _rc = (x);         \
+    if (_rc) return _rc;   \
+  } while (0)
+
+int gemm(const void* A, const void* B, void* C, int M, int N, int K, int mode, const float* bias,
+         const float* gate, int gate_stride, int rows_per_gate, cudaStream_t st) {
+  bc::GemmArgs g{A, B, C, M, N, K, mode, bias, gate, gate_stride, rows_per_gate, 0};
+  return bc::gemm_run(g, st);
+}
+
+template <typename T>
+const T* at(const void* base, int64_t elems) {
+  return static_cast<const T*>(base) + elems;
+}
+
+}  // namespace
+
+extern "C" int64_t bc_wan_workspace_bytes(const bc_wan_dims* dims) {
+  if (!dims || check_dims(*dims)) return -1;
+  return carve(nullptr, *dims, nullptr);
+}
+
+extern "C" int bc_wan_create(const bc_wan_dims* dims, const bc_wan_params* params, void* kv_arena,
+                             void* workspace, int64_t workspace_bytes, bc_wan_ctx** out) {
+  if (!dims || !params || !kv_arena || !workspace || !out)
+    return bc_fail(BC_ERR_CONTRACT, "bc_wan_create: null argument");
+  RC(check_dims(*dims));
+  const int64_t need = carve(nullptr, *dims, nullptr);
+  if (workspace_bytes < need)
+    return bc_fail(BC_ERR_CONTRACT, "bc_wan_create: workspace %lld < %lld bytes", (long long)workspace_bytes,
+                   (long long)need);
+  bc_wan_ctx* c = new (std::nothrow) bc_wan_ctx();
+  if (!c) return bc_fail(BC_ERR_CUDA, "bc_wan_create: out of host memory");
+  c->dims = *dims;
+  c->prm = *params;
+  c->arena = static_cast<__nv_bfloat16*>(kv_arena);
+  c->d = dims->heads * dims->head_dim;
+  c->T = dims->block_size * (dims->latent_h / 2) * (dims->latent_w / 2);
+  c->E = dims->max_entries;
+  c->R = c->E * c->T;
+  carve(c, *dims, static_cast<char*>(workspace));
+  c->text_ready = false;
+  *out = c;
+  return BC_OK;
+}
+
+extern "C" int bc_wan_destroy(bc_wan_ctx* ctx) {
+  delete ctx;
+  return BC_OK;
+}
+
+// Text encoder MLP (Linear(text_dim,d) -> GELU(tanh) -> Linear(d,d)) and the
+// per-layer cross-attention K = RMSNorm(ctx Wk + bk) * w, V = ctx Wv + bv.
+extern "C" int bc_wan_set_text(bc_wan_ctx* c, const float* states, void* stream) {
+  if (!c || !states) return bc_fail(BC_ERR_CONTRACT, "bc_wan_set_text: null argument");
+  cudaStream_t st = (cudaStream_t)stream;
+  const bc_wan_dims& dm = c->dims;
+  const bc_wan_params& p = c->prm;
+  const int d = c->d, Lt = dm.text_len;
+  RC(bc::launch_f32_to_bf16(states, c->text_in, (int64_t)Lt * dm.text_dim, st));
+  RC(gemm(c->text_in, p.text_w1, c->text_h, Lt, d, dm.text_dim, bc::kEpiGeluBf16, p.text_b1, nullptr, 0, 1, st));
+  RC(gemm(c->text_h, p.text_w2, c->ctx, Lt, d, d, bc::kEpiStoreBf16, p.text_b2, nullptr, 0, 1, st));
+  for (int l = 0; l < dm.layers; ++l) {
+    RC(gemm(c->ctx, at<__nv_bfloat16>(p.ckv_w, (int64_t)l * 2 * d * d), c->text_tmp, Lt, 2 * d, d,
+            bc::kEpiStoreBf16, p.ckv_b + (size_t)l * 2 * d, nullptr, 0, 1, st));
+    __nv_bfloat16* kdst = c->textkv + (size_t)l * 2 * Lt * d;
+    RC(bc::launch_rms_rows(c->text_tmp, Lt, d, 2 * d, p.cnorm_k + (size_t)l * d, kdst, d, st));
+    RC(bc::launch_copy_cols(c->text_tmp, 2 * d, d, kdst + (size_t)Lt * d, d, Lt, d, st));
+  }
+  c->text_ready = true;
+  return BC_OK;
+}
+
+extern "C" int bc_wan_step(bc_wan_ctx* c, const bc_batch* batch, const bc_wan_update* upd, int32_t* status,
+                           void* stream) {
+  if (!c || !batch || !upd || !status) return bc_fail(BC_ERR_CONTRACT, "bc_wan_step: null argument");
+  if (!c->text_ready) return bc_fail(BC_ERR_CONTRACT, "bc_wan_step: bc_wan_set_text not called");
+  const bc_wan_dims& dm = c->dims;
+  const bc_wan_params& p = c->prm;
+  const int n = batch->n_entries;
+  if (n < 1 || n > c->E) return bc_fail(BC_ERR_CONTRACT, "bc_wan_step: %d entries (max %d)", n, c->E);
+  if (batch->block_size != dm.block_size) return bc_fail(BC_ERR_CONTRACT, "bc_wan_step: block size mismatch");
+  for (int e = 0; e < n; ++e) {
+    if (batch->slot[e] < 0 || batch->slot[e] >= dm.n_slots || batch->n_vis[e] < 1 || batch->n_vis[e] > BC_MAX_VIS)
+      return bc_fail(BC_ERR_CONTRACT, "bc_wan_step: bad slot table (entry %d)", e);
+    for (int v = 0; v < batch->n_vis[e]; ++v)
+      if (batch->vis_slot[e][v] < 0 || batch->vis_slot[e][v] >= dm.n_slots)
+        return bc_fail(BC_ERR_CONTRACT, "bc_wan_step: visible slot out of range");
+    if (!(batch->level[e] >= 0.0 && batch->level[e] <= 1000.0) || !upd->latents[e])
+      return bc_fail(BC_ERR_CONTRACT, "bc_wan_step: bad level / latents (entry %d)", e);
+    if (upd->post[e] == 0 && (!upd->eps[e] || !(upd->next_level[e] >= 0.0 && upd->next_level[e] <= 1000.0)))
+      return bc_fail(BC_ERR_CONTRACT, "bc_wan_step: renoise entry %d needs eps and a level", e);
+    if ((upd->post[e] == 1 || upd->post[e] == 3) && !upd->out[e])
+      return bc_fail(BC_ERR_CONTRACT, "bc_wan_step: entry %d needs an output buffer", e);
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  const int d = c->d, T = c->T, R = n * T, L = dm.layers, F = dm.block_size;
+  const int H = dm.latent_h, W = dm.latent_w;
+
+  bc::EntryPtrs lat{};
+  for (int e = 0; e < n; ++e) {
+    lat.p[e] = upd->latents[e];
+    lat.block[e] = batch->block_index[e];
+  }
+  RC(bc::launch_check_finite(lat, n, F * 16 * H * W, status, st));
+  RC(bc::launch_patchify(lat, n, F, H, W, c->patches, st));
+  RC(gemm(c->patches, p.patch_w, c->X, R, d, 64, bc::kEpiStoreF32, p.patch_b, nullptr, 0, 1, st));
+
+  // time embedding: e = W2 silu(W1 sin(t) + b1) + b2 ; e0 = Wp silu(e) + bp
+  bc::TimeArgs ta{};
+  for (int e = 0; e < n; ++e) ta.t[e] = batch->level[e];
+  RC(bc::launch_timestep_sin(ta, n, c->t_sin, dm.freq_dim, st));
+  RC(bc::launch_gemv(c->t_sin, n, dm.freq_dim, static_cast<const __nv_bfloat16*>(p.time_w1), p.time_b1, c->t_h, d,
+                     0, 1, st));
+  RC(bc::launch_gemv(c->t_h, n, d, static_cast<const __nv_bfloat16*>(p.time_w2), p.time_b2, c->t_e, d, 0, 0, st));
+  RC(bc::launch_gemv(c->t_e, n, d, static_cast<const __nv_bfloat16*>(p.tproj_w), p.tproj_b, c->t_e0, 6 * d, 1, 0,
+                     st));
+  RC(bc::launch_mod_combine(p.modulation, c->t_e0, L, n, d, c->mod_all, st));
+
+  bc::AttnArgs sa{};
+  sa.kv_base = c->arena;
+  sa.n_mats = L * dm.n_slots * 2;
+  sa.n_entries = n;
+  sa.q_tokens = T;
+  sa.kv_tokens = T;
+  sa.heads = dm.heads;
+  sa.head_dim = 128;
+  sa.mat_stride = 2;
+  sa.v_offset = 1;
+  sa.scale = 0.08838834764831845f;  // 1/sqrt(128)
+  sa.q = c->Q;
+  sa.out = c->attn;
+  for (int e = 0; e < n; ++e) {
+    sa.n_vis[e] = batch->n_vis[e];
+    for (int v = 0; v < batch->n_vis[e]; ++v) sa.vis_slot[e][v] = batch->vis_slot[e][v];
+  }
+  bc::AttnArgs ca = sa;
+  ca.kv_base = c->textkv;
+  ca.n_mats = L * 2;
+  ca.kv_tokens = dm.text_len;
+  for (int e = 0; e < n; ++e) {
+    ca.n_vis[e] = 1;
+    ca.vis_slot[e][0] = 0;
+  }
+  bc::QkArgs qa{};
+  qa.qout = c->Q;
+  qa.arena = c->arena;
+  qa.hp = H / 2;
+  qa.wp = W / 2;
+  for (int e = 0; e < n; ++e) {
+    qa.slot[e] = batch->slot[e];
+    qa.frame0[e] = batch->block_index[e] * F;
+  }
+
+  for (int l = 0; l < L; ++l) {
+    const float* mod = c->mod_all + (size_t)l * n * 6 * d;  // [e][6][d]
+    bc::LnArgs ln{0, nullptr, nullptr, mod + 0 * d, mod + 1 * d, 6 * d};
+    RC(bc::launch_ln_rows(c->X, c->xn, R, d, T, ln, st));
+    RC(gemm(c->xn, at<__nv_bfloat16>(p.qkv_w, (int64_t)l * 3 * d * d), c->qkv, R, 3 * d, d, bc::kEpiStoreBf16,
+            p.qkv_b + (size_t)l * 3 * d, nullptr, 0, 1, st));
+    qa.mat_base = (int64_t)l * dm.n_slots * 2;
+    qa.norm_q = p.norm_q + (size_t)l * d;
+    qa.norm_k = p.norm_k + (size_t)l * d;
+    RC(bc::launch_qk_norm_rope(c->qkv, R, d, T, qa, st));
+    sa.mat_base = l * dm.n_slots * 2;
+    RC(bc::attention_run(sa, st));
+    RC(gemm(c->attn, at<__nv_bfloat16>(p.o_w, (int64_t)l * d * d), c->X, R, d, d, bc::kEpiResidualF32,
+            p.o_b + (size_t)l * d, mod + 2 * d, 6 * d, T, st));
+    // cross-attention
+    bc::LnArgs ln3{1, p.norm3_b + (size_t)l * d, p.norm3_w + (size_t)l * d, nullptr, nullptr, 0};
+    RC(bc::launch_ln_rows(c->X, c->xn, R, d, T, ln3, st));
+    RC(gemm(c->xn, at<__nv_bfloat16>(p.cq_w, (int64_t)l * d * d), c->Q, R, d, d, bc::kEpiStoreBf16,
+            p.cq_b + (size_t)l * d, nullptr, 0, 1, st));
+    RC(bc::launch_rms_rows(c->Q, R, d, d, p.cnorm_q + (size_t)l * d, c->Q, d, st));
+    ca.mat_base = l * 2;
+    RC(bc::attention_run(ca, st));
+    RC(gemm(c->attn, at<__nv_bfloat16>(p.co_w, (int64_t)l * d * d), c->X, R, d, d, bc::kEpiResidualF32,
+            p.co_b + (size_t)l * d, nullptr, 0, 1, st));
+    // FFN
+    bc::LnArgs ln2{0, nullptr, nullptr, mod + 3 * d, mod + 4 * d, 6 * d};
+    RC(bc::launch_ln_rows(c->X, c->xn, R, d, T, ln2, st));
+    RC(gemm(c->xn, at<__nv_bfloat16>(p.ffn1_w, (int64_t)l * dm.ffn_dim * d), c->H1, R, dm.ffn_dim, d,
+            bc::kEpiGeluBf16, p.ffn1_b + (size_t)l * dm.ffn_dim, nullptr, 0, 1, st));
+    RC(gemm(c->H1, at<__nv_bfloat16>(p.ffn2_w, (int64_t)l * d * dm.ffn_dim), c->X, R, d, dm.ffn_dim,
+            bc::kEpiResidualF32, p.ffn2_b + (size_t)l * d, mod + 5 * d, 6 * d, T, st));
+  }
+  // head: LN(x) * (1 + head_mod[1] + e) + head_mod[0] + e -> Linear(d, 64)
+  bc::LnArgs lh{0, p.head_mod, p.head_mod + d, c->t_e, c->t_e, d};
+  RC(bc::launch_ln_rows(c->X, c->xn, R, d, T, lh, st));
+  RC(gemm(c->xn, p.head_w, c->Y, R, 64, d, bc::kEpiStoreF32, p.head_b, nullptr, 0, 1, st));
+  bc::UpdArgs u{};
+  for (int e = 0; e < n; ++e) {
+    u.latents[e] = upd->latents[e];
+    u.eps[e] = upd->eps[e];
+    u.out[e] = upd->out[e];
+    u.level[e] = batch->level[e];
+    u.next_level[e] = upd->next_level[e];
+    u.post[e] = upd->post[e];
+    u.block[e] = batch->block_index[e];
+  }
+  RC(bc::launch_head_update(c->Y, n, T, F, H, W, u, status, st));
+  return BC_OK;
+}

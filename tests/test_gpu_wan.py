@@ -1,0 +1,160 @@
+"""Wan2.1-shaped DiT on the GPU (tcgen05 GEMM + flash attention + fused
+bandwidth kernels) vs the numpy fp32 oracle (oracle/wan.py).
+
+Tolerances (north_star): per step (teacher-forced, identical inputs and pool
+KV on both sides) x0 rel-L2 <= 2e-3; free-running final latents rel-L2 <=
+1e-2 against the oracle in the same attention mode and offset.  Device-vs-
+device equalities (P1, worker independence, causal truncation) are exact.
+"""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+STEP_TOL = 2e-3
+RUN_TOL = 1e-2
+
+
+def rel(a, b):
+    a, b = np.asarray(a, dtype=np.float64), np.asarray(b, dtype=np.float64)
+    return float(np.linalg.norm(a - b) / np.linalg.norm(b))
+
+
+@pytest.fixture(scope="module")
+def tiny():
+    import paper_2511_20426_b200 as bc
+    from paper_2511_20426_b200.wan import WanWeights
+    cfg = bc.wan_config("tiny", total_frames=18)
+    w = WanWeights.random(cfg, 7)
+    return cfg, w, w.host_params()
+
+
+def _pool(bc, cfg, w, blocks, cond, rng):
+    """GPU-computed cache-pass KV for `blocks` (used identically by both sides)."""
+    pool = []
+    for b in blocks:
+        lat = rng.standard_normal((cfg.block_size, cfg.latent_dim)).astype(np.float32)
+        mask = bc.build_mask([b], [x[0].block_index for x in pool], "causal", cfg.block_size)
+        out = bc.forward(w, [bc.EntryInput(b, lat, 0.0, cond)], pool, mask)[0]
+        pool.append(out.kv)
+    return pool
+
+
+@pytest.mark.parametrize("mode", ["bidirectional", "causal"])
+def test_wan_step_teacher_forced(tiny, mode):
+    import paper_2511_20426_b200 as bc
+    from oracle import wan as wo
+    from oracle.schedule import visible_blocks
+    from paper_2511_20426_b200.wan import text_states
+    cfg, w, params = tiny
+    cond = bc.embed_prompt("a lighthouse in a storm", cfg.cond_dim)
+    rng = np.random.default_rng(1)
+    pool = _pool(bc, cfg, w, [0, 1], cond, rng)
+    batch = [2, 3, 4]
+    levels = [250.0, 500.0, 1000.0]
+    lat = {b: rng.standard_normal((cfg.block_size, cfg.latent_dim)).astype(np.float32) for b in batch}
+    mask = bc.build_mask(batch, [0, 1], mode, cfg.block_size)
+    outs = bc.forward(w, [bc.EntryInput(b, lat[b], lv, cond) for b, lv in zip(batch, levels)], pool, mask)
+    d = cfg.model_dim
+    pool_kv = {kv[0].block_index: [(l.keys.reshape(-1, d), l.values.reshape(-1, d)) for l in kv]
+               for kv in pool}
+    ref = wo.WanOracle(params, cfg).forward(
+        [(b, lat[b], lv) for b, lv in zip(batch, levels)], pool_kv,
+        visible_blocks(batch, [0, 1], mode), text_states(cond, cfg.text_len, cfg.text_dim))
+    for o, (x0, kv) in zip(outs, ref):
+        assert rel(o.x0, x0.reshape(o.x0.shape)) < STEP_TOL
+        for l in range(cfg.layers):
+            assert rel(o.kv[l].keys.reshape(-1, d), kv[l][0]) < 1e-2
+            assert rel(o.kv[l].values.reshape(-1, d), kv[l][1]) < 1e-2
+
+
+def _stack(run):
+    return np.stack([run.outputs[k] for k in sorted(run.outputs)])
+
+
+@pytest.mark.parametrize("offset,mode", [(1, "bidirectional"), (1, "causal"), (5, "bidirectional")])
+def test_wan_full_run_vs_oracle(tiny, monkeypatch, offset, mode):
+    import paper_2511_20426_b200 as bc
+    from paper_2511_20426_b200 import engine
+    from oracle.loop import wan_oracle_runtime
+    cfg, w, params = tiny
+    cfg = bc.with_fields(cfg, offset=offset, attention_mode=mode, total_frames=15)
+    gpu = bc.run_cascade(cfg, "a red cube", weights=w)
+    with monkeypatch.context() as m:
+        m.setattr(engine, "_runtime_for", wan_oracle_runtime(params))
+        cpu = bc.run_cascade(cfg, "a red cube", weights=w)
+    assert gpu.emitted_order == cpu.emitted_order
+    for b in range(cfg.num_blocks):
+        assert rel(gpu.outputs[b], cpu.outputs[b]) < RUN_TOL, b
+    assert [e.pool_state for e in gpu.trace.events] == [e.pool_state for e in cpu.trace.events]
+
+
+def test_wan_p1_and_worker_independence_exact(tiny):
+    import paper_2511_20426_b200 as bc
+    cfg, w, _ = tiny
+    cfg = bc.with_fields(cfg, total_frames=12)
+    seq = bc.run_sequential_reference(cfg, "p", weights=w)
+    cas5 = bc.run_cascade(bc.with_fields(cfg, offset=5), "p", weights=w)
+    assert np.array_equal(_stack(seq), _stack(cas5))
+    a = bc.run_cascade(cfg, "p", weights=w)
+    b = bc.run_cascade(bc.with_fields(cfg, workers=5), "p", weights=w)
+    assert np.array_equal(_stack(a), _stack(b))
+
+
+def test_wan_causal_truncation_exact(tiny):
+    import paper_2511_20426_b200 as bc
+    cfg, w, _ = tiny
+    cfg = bc.with_fields(cfg, attention_mode="causal", total_frames=15)
+    full = bc.run_cascade(cfg, "p", weights=w)
+    trunc = bc.run_cascade(bc.with_fields(cfg, total_frames=9), "p", weights=w)
+    for b in range(3):
+        assert np.array_equal(full.outputs[b], trunc.outputs[b])
+
+
+def test_wan_prompt_switch_cascade_mode(tiny):
+    import paper_2511_20426_b200 as bc
+    cfg, w, _ = tiny
+    cfg = bc.with_fields(cfg, total_frames=18)
+    plain = bc.run_cascade(cfg, "first scene", weights=w)
+    sw = bc.run_cascade(cfg, "first scene", weights=w,
+                        switches=[bc.SwitchSpec("second scene", "cascade", at_block=3)])
+    same = bc.run_cascade(cfg, "first scene", weights=w,
+                          switches=[bc.SwitchSpec("first scene", "cascade", at_block=3)])
+    assert sw.switch_events[0].extra_passes == 0 and sw.iterations == plain.iterations
+    boundary = sw.switch_events[0].iteration
+    before = [e.emitted_block for e in plain.trace.events
+              if e.iteration < boundary and e.emitted_block is not None]
+    for b in before:
+        assert np.array_equal(sw.outputs[b], plain.outputs[b])
+    assert not np.array_equal(sw.outputs[5], plain.outputs[5])
+    for b in range(cfg.num_blocks):
+        assert np.array_equal(same.outputs[b], plain.outputs[b])
+    with pytest.raises(bc.InvalidInputError):
+        bc.run_cascade(cfg, "p", weights=w, switches=[bc.SwitchSpec("x", "recache", at_block=2)])
+
+
+def test_wan_13b_dims_step(monkeypatch):
+    """Full Wan2.1-1.3B layer geometry (d=1536, 12 heads, ffn 8960, 480x832
+    latents -> 4680 tokens/block, 512x4096 text), 2 layers, one cascade
+    step of width 2 over a 1-block pool, teacher-forced vs the oracle."""
+    import paper_2511_20426_b200 as bc
+    from oracle import wan as wo
+    from oracle.schedule import visible_blocks
+    from paper_2511_20426_b200.wan import WanWeights, text_states
+    cfg = bc.wan_config("1.3b", layers=2, total_frames=9)
+    w = WanWeights.random(cfg, 11)
+    cond = bc.embed_prompt("a lighthouse in a storm", cfg.cond_dim)
+    rng = np.random.default_rng(2)
+    pool = _pool(bc, cfg, w, [0], cond, rng)
+    batch, levels = [1, 2], [500.0, 1000.0]
+    lat = {b: rng.standard_normal((cfg.block_size, cfg.latent_dim)).astype(np.float32) for b in batch}
+    mask = bc.build_mask(batch, [0], "bidirectional", cfg.block_size)
+    outs = bc.forward(w, [bc.EntryInput(b, lat[b], lv, cond) for b, lv in zip(batch, levels)], pool, mask)
+    d = cfg.model_dim
+    pool_kv = {0: [(l.keys.reshape(-1, d), l.values.reshape(-1, d)) for l in pool[0]]}
+    ref = wo.WanOracle(w.host_params(), cfg).forward(
+        [(b, lat[b], lv) for b, lv in zip(batch, levels)], pool_kv,
+        visible_blocks(batch, [0], "bidirectional"), text_states(cond, cfg.text_len, cfg.text_dim))
+    for o, (x0, _) in zip(outs, ref):
+        assert rel(o.x0, x0.reshape(o.x0.shape)) < STEP_TOL
