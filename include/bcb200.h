@@ -34,6 +34,12 @@ extern "C" {
 const char* bc_last_error(void);
 /* Library version / build flags string. */
 const char* bc_version(void);
+/* Kernels launched by this library so far (process-wide). */
+long long bc_launch_count(void);
+/* Per-kernel-class CUDA-event timing of bc_wan_step launches (classes:
+ * 0 self-attention, 1 cross-attention, 2 GEMM, 3 bandwidth-bound). */
+int bc_profile_enable(int on);
+int bc_profile_collect(double* ms, double* flops, double* bytes, int64_t* launches, int n_classes);
 
 /* ---------------------------------------------------------------------------
  * Noise: NoiseStream.draw / block_noise (core.py:161-186) and the Philox

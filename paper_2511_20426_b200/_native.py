@@ -98,7 +98,30 @@ _SIGS = {
     "bc_attention_paged": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64,
                                      C.c_int32, C.POINTER(Batch), C.c_int32, C.c_int32,
                                      C.c_void_p, C.c_void_p]),
+    "bc_launch_count": (C.c_longlong, []),
+    "bc_profile_enable": (C.c_int, [C.c_int]),
+    "bc_profile_collect": (C.c_int, [C.POINTER(C.c_double), C.POINTER(C.c_double),
+                                     C.POINTER(C.c_double), C.POINTER(C.c_int64), C.c_int]),
 }
+
+PROFILE_CLASSES = ("self_attention", "cross_attention", "gemm", "bandwidth")
+
+
+def profile_enable(on: bool) -> None:
+    check(lib().bc_profile_enable(1 if on else 0), "bc_profile_enable")
+
+
+def profile_collect() -> dict:
+    """{class: (ms, flops, bytes, launches)} accumulated since the last call."""
+    n = len(PROFILE_CLASSES)
+    ms, fl, by = (C.c_double * n)(), (C.c_double * n)(), (C.c_double * n)()
+    cnt = (C.c_int64 * n)()
+    check(lib().bc_profile_collect(ms, fl, by, cnt, n), "bc_profile_collect")
+    return {name: (ms[i], fl[i], by[i], cnt[i]) for i, name in enumerate(PROFILE_CLASSES)}
+
+
+def launch_count() -> int:
+    return int(lib().bc_launch_count())
 
 
 def exported_symbols() -> list:

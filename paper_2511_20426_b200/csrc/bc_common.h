@@ -7,6 +7,8 @@
 
 // Records a formatted message for bc_last_error() and returns `code`.
 int bc_fail(int code, const char* fmt, ...);
+// Counts every kernel this library launches (bc_launch_count()).
+void bc_count_launch();
 
 #ifdef __CUDACC__
 #include <cuda_runtime.h>
@@ -19,6 +21,7 @@ int bc_fail(int code, const char* fmt, ...);
   } while (0)
 #define BC_LAUNCHED()                                                              \
   do {                                                                             \
+    bc_count_launch();                                                             \
     cudaError_t _e = cudaGetLastError();                                           \
     if (_e != cudaSuccess)                                                         \
       return bc_fail(BC_ERR_CUDA, "%s:%d launch -> %s", __FILE__, __LINE__,        \

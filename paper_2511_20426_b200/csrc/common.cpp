@@ -4,9 +4,16 @@
 
 #include "bc_common.h"
 
+#include <atomic>
+
 namespace {
 thread_local char g_last_error[512] = "";
+std::atomic<long long> g_launches{0};
 }
+
+void bc_count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+extern "C" long long bc_launch_count(void) { return g_launches.load(); }
 
 int bc_fail(int code, const char* fmt, ...) {
   va_list ap;

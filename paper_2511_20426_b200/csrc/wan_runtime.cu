@@ -21,6 +21,7 @@
 
 #include <cstring>
 #include <new>
+#include <vector>
 
 #include "attention.h"
 #include "bc_common.h"
@@ -108,12 +109,71 @@ int gemm(const void* A, const void* B, void* C, int M, int N, int K, int mode, c
   return bc::gemm_run(g, st);
 }
 
+// ---- optional per-kernel-class timing with CUDA events on the launch stream
+enum ProfClass { kSelfAttn = 0, kCrossAttn = 1, kGemm = 2, kBandwidth = 3, kNumProf = 4 };
+struct ProfRec {
+  cudaEvent_t a, b;
+  int cls;
+  double flops, bytes;
+};
+bool g_prof = false;
+std::vector<ProfRec> g_recs;
+std::vector<cudaEvent_t> g_free_events;
+
+cudaEvent_t ev_get() {
+  if (!g_free_events.empty()) {
+    cudaEvent_t e = g_free_events.back();
+    g_free_events.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  return e;
+}
+
+template <class F>
+int timed(int cls, double flops, double bytes, cudaStream_t st, F&& f) {
+  if (!g_prof) return f();
+  cudaEvent_t a = ev_get(), b = ev_get();
+  cudaEventRecord(a, st);
+  const int rc = f();
+  cudaEventRecord(b, st);
+  g_recs.push_back({a, b, cls, flops, bytes});
+  return rc;
+}
+
 template <typename T>
 const T* at(const void* base, int64_t elems) {
   return static_cast<const T*>(base) + elems;
 }
 
 }  // namespace
+
+extern "C" int bc_profile_enable(int on) {
+  g_prof = on != 0;
+  return BC_OK;
+}
+
+// Sums (ms, algorithmic flops, algorithmic bytes, launches) per class since
+// the last collect: 0 self-attention, 1 cross-attention, 2 GEMM, 3 others.
+extern "C" int bc_profile_collect(double* ms, double* flops, double* bytes, int64_t* count, int n_cls) {
+  for (int i = 0; i < n_cls; ++i) ms[i] = flops[i] = bytes[i] = 0.0, count[i] = 0;
+  for (auto& r : g_recs) {
+    BC_CUDA(cudaEventSynchronize(r.b));
+    float t = 0.f;
+    BC_CUDA(cudaEventElapsedTime(&t, r.a, r.b));
+    if (r.cls < n_cls) {
+      ms[r.cls] += t;
+      flops[r.cls] += r.flops;
+      bytes[r.cls] += r.bytes;
+      count[r.cls] += 1;
+    }
+    g_free_events.push_back(r.a);
+    g_free_events.push_back(r.b);
+  }
+  g_recs.clear();
+  return BC_OK;
+}
 
 extern "C" int64_t bc_wan_workspace_bytes(const bc_wan_dims* dims) {
   if (!dims || check_dims(*dims)) return -1;
@@ -202,9 +262,9 @@ extern "C" int bc_wan_step(bc_wan_ctx* c, const bc_batch* batch, const bc_wan_up
     lat.p[e] = upd->latents[e];
     lat.block[e] = batch->block_index[e];
   }
-  RC(bc::launch_check_finite(lat, n, F * 16 * H * W, status, st));
-  RC(bc::launch_patchify(lat, n, F, H, W, c->patches, st));
-  RC(gemm(c->patches, p.patch_w, c->X, R, d, 64, bc::kEpiStoreF32, p.patch_b, nullptr, 0, 1, st));
+  RC(timed(kBandwidth, 0.0, 4.0 * n * F * 16 * H * W, st, [&] { return bc::launch_check_finite(lat, n, F * 16 * H * W, status, st); }));
+  RC(timed(kBandwidth, 0.0, 6.0 * R * 64, st, [&] { return bc::launch_patchify(lat, n, F, H, W, c->patches, st); }));
+  RC(timed(kGemm, 2.0 * R * d * 64, 0.0, st, [&] { return gemm(c->patches, p.patch_w, c->X, R, d, 64, bc::kEpiStoreF32, p.patch_b, nullptr, 0, 1, st); }));
 
   // time embedding: e = W2 silu(W1 sin(t) + b1) + b2 ; e0 = Wp silu(e) + bp
   bc::TimeArgs ta{};
@@ -252,42 +312,44 @@ extern "C" int bc_wan_step(bc_wan_ctx* c, const bc_batch* batch, const bc_wan_up
     qa.frame0[e] = batch->block_index[e] * F;
   }
 
+  double self_flops = 0.0;
+  for (int e = 0; e < n; ++e) self_flops += 4.0 * T * ((double)batch->n_vis[e] * T) * d;
   for (int l = 0; l < L; ++l) {
     const float* mod = c->mod_all + (size_t)l * n * 6 * d;  // [e][6][d]
     bc::LnArgs ln{0, nullptr, nullptr, mod + 0 * d, mod + 1 * d, 6 * d};
-    RC(bc::launch_ln_rows(c->X, c->xn, R, d, T, ln, st));
-    RC(gemm(c->xn, at<__nv_bfloat16>(p.qkv_w, (int64_t)l * 3 * d * d), c->qkv, R, 3 * d, d, bc::kEpiStoreBf16,
-            p.qkv_b + (size_t)l * 3 * d, nullptr, 0, 1, st));
+    RC(timed(kBandwidth, 0.0, 6.0 * R * d, st, [&] { return bc::launch_ln_rows(c->X, c->xn, R, d, T, ln, st); }));
+    RC(timed(kGemm, 2.0 * R * 3.0 * d * d, 0.0, st, [&] { return gemm(c->xn, at<__nv_bfloat16>(p.qkv_w, (int64_t)l * 3 * d * d), c->qkv, R, 3 * d, d, bc::kEpiStoreBf16,
+            p.qkv_b + (size_t)l * 3 * d, nullptr, 0, 1, st); }));
     qa.mat_base = (int64_t)l * dm.n_slots * 2;
     qa.norm_q = p.norm_q + (size_t)l * d;
     qa.norm_k = p.norm_k + (size_t)l * d;
-    RC(bc::launch_qk_norm_rope(c->qkv, R, d, T, qa, st));
+    RC(timed(kBandwidth, 0.0, 12.0 * R * d, st, [&] { return bc::launch_qk_norm_rope(c->qkv, R, d, T, qa, st); }));
     sa.mat_base = l * dm.n_slots * 2;
-    RC(bc::attention_run(sa, st));
-    RC(gemm(c->attn, at<__nv_bfloat16>(p.o_w, (int64_t)l * d * d), c->X, R, d, d, bc::kEpiResidualF32,
-            p.o_b + (size_t)l * d, mod + 2 * d, 6 * d, T, st));
+    RC(timed(kSelfAttn, self_flops, 0.0, st, [&] { return bc::attention_run(sa, st); }));
+    RC(timed(kGemm, 2.0 * R * d * d, 0.0, st, [&] { return gemm(c->attn, at<__nv_bfloat16>(p.o_w, (int64_t)l * d * d), c->X, R, d, d, bc::kEpiResidualF32,
+            p.o_b + (size_t)l * d, mod + 2 * d, 6 * d, T, st); }));
     // cross-attention
     bc::LnArgs ln3{1, p.norm3_b + (size_t)l * d, p.norm3_w + (size_t)l * d, nullptr, nullptr, 0};
-    RC(bc::launch_ln_rows(c->X, c->xn, R, d, T, ln3, st));
-    RC(gemm(c->xn, at<__nv_bfloat16>(p.cq_w, (int64_t)l * d * d), c->Q, R, d, d, bc::kEpiStoreBf16,
-            p.cq_b + (size_t)l * d, nullptr, 0, 1, st));
-    RC(bc::launch_rms_rows(c->Q, R, d, d, p.cnorm_q + (size_t)l * d, c->Q, d, st));
+    RC(timed(kBandwidth, 0.0, 6.0 * R * d, st, [&] { return bc::launch_ln_rows(c->X, c->xn, R, d, T, ln3, st); }));
+    RC(timed(kGemm, 2.0 * R * d * d, 0.0, st, [&] { return gemm(c->xn, at<__nv_bfloat16>(p.cq_w, (int64_t)l * d * d), c->Q, R, d, d, bc::kEpiStoreBf16,
+            p.cq_b + (size_t)l * d, nullptr, 0, 1, st); }));
+    RC(timed(kBandwidth, 0.0, 4.0 * R * d, st, [&] { return bc::launch_rms_rows(c->Q, R, d, d, p.cnorm_q + (size_t)l * d, c->Q, d, st); }));
     ca.mat_base = l * 2;
-    RC(bc::attention_run(ca, st));
-    RC(gemm(c->attn, at<__nv_bfloat16>(p.co_w, (int64_t)l * d * d), c->X, R, d, d, bc::kEpiResidualF32,
-            p.co_b + (size_t)l * d, nullptr, 0, 1, st));
+    RC(timed(kCrossAttn, 4.0 * R * (double)dm.text_len * d, 0.0, st, [&] { return bc::attention_run(ca, st); }));
+    RC(timed(kGemm, 2.0 * R * d * d, 0.0, st, [&] { return gemm(c->attn, at<__nv_bfloat16>(p.co_w, (int64_t)l * d * d), c->X, R, d, d, bc::kEpiResidualF32,
+            p.co_b + (size_t)l * d, nullptr, 0, 1, st); }));
     // FFN
     bc::LnArgs ln2{0, nullptr, nullptr, mod + 3 * d, mod + 4 * d, 6 * d};
-    RC(bc::launch_ln_rows(c->X, c->xn, R, d, T, ln2, st));
-    RC(gemm(c->xn, at<__nv_bfloat16>(p.ffn1_w, (int64_t)l * dm.ffn_dim * d), c->H1, R, dm.ffn_dim, d,
-            bc::kEpiGeluBf16, p.ffn1_b + (size_t)l * dm.ffn_dim, nullptr, 0, 1, st));
-    RC(gemm(c->H1, at<__nv_bfloat16>(p.ffn2_w, (int64_t)l * d * dm.ffn_dim), c->X, R, d, dm.ffn_dim,
-            bc::kEpiResidualF32, p.ffn2_b + (size_t)l * d, mod + 5 * d, 6 * d, T, st));
+    RC(timed(kBandwidth, 0.0, 6.0 * R * d, st, [&] { return bc::launch_ln_rows(c->X, c->xn, R, d, T, ln2, st); }));
+    RC(timed(kGemm, 2.0 * R * (double)dm.ffn_dim * d, 0.0, st, [&] { return gemm(c->xn, at<__nv_bfloat16>(p.ffn1_w, (int64_t)l * dm.ffn_dim * d), c->H1, R, dm.ffn_dim, d,
+            bc::kEpiGeluBf16, p.ffn1_b + (size_t)l * dm.ffn_dim, nullptr, 0, 1, st); }));
+    RC(timed(kGemm, 2.0 * R * (double)dm.ffn_dim * d, 0.0, st, [&] { return gemm(c->H1, at<__nv_bfloat16>(p.ffn2_w, (int64_t)l * d * dm.ffn_dim), c->X, R, d, dm.ffn_dim,
+            bc::kEpiResidualF32, p.ffn2_b + (size_t)l * d, mod + 5 * d, 6 * d, T, st); }));
   }
   // head: LN(x) * (1 + head_mod[1] + e) + head_mod[0] + e -> Linear(d, 64)
   bc::LnArgs lh{0, p.head_mod, p.head_mod + d, c->t_e, c->t_e, d};
-  RC(bc::launch_ln_rows(c->X, c->xn, R, d, T, lh, st));
-  RC(gemm(c->xn, p.head_w, c->Y, R, 64, d, bc::kEpiStoreF32, p.head_b, nullptr, 0, 1, st));
+  RC(timed(kBandwidth, 0.0, 6.0 * R * d, st, [&] { return bc::launch_ln_rows(c->X, c->xn, R, d, T, lh, st); }));
+  RC(timed(kGemm, 2.0 * R * 64.0 * d, 0.0, st, [&] { return gemm(c->xn, p.head_w, c->Y, R, 64, d, bc::kEpiStoreF32, p.head_b, nullptr, 0, 1, st); }));
   bc::UpdArgs u{};
   for (int e = 0; e < n; ++e) {
     u.latents[e] = upd->latents[e];
@@ -298,6 +360,6 @@ extern "C" int bc_wan_step(bc_wan_ctx* c, const bc_batch* batch, const bc_wan_up
     u.post[e] = upd->post[e];
     u.block[e] = batch->block_index[e];
   }
-  RC(bc::launch_head_update(c->Y, n, T, F, H, W, u, status, st));
+  RC(timed(kBandwidth, 0.0, (4.0 * 64 + 16.0 * 16) * R, st, [&] { return bc::launch_head_update(c->Y, n, T, F, H, W, u, status, st); }));
   return BC_OK;
 }
