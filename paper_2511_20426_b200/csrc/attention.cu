@@ -6,16 +6,20 @@
 // visible blocks' K/V in ascending block order -- here the arena slots
 // vis_slot[e][0..n_vis) in that order -- and softmax runs over exactly those
 // keys.  Key tiles are consumed strictly in that order (no split-K, no
-// atomics), so results are independent of how many entries share a launch.
+// atomics), so an entry's result does not depend on which other entries
+// share the launch.
 //
-// One CTA = one 128-row query tile x one head x one entry.
-//   warp 0     TMA: Q once, then K_j / V_j (128 keys x 128 dims, 2 stages)
-//   warp 1     MMA: S_j = Q K_j^T into TMEM (double-buffered),
-//                   O += P_j V_j into TMEM (P from smem, V MN-major)
-//   warps 2-5  softmax: thread = query row; S row from TMEM, online softmax
-//              with lazy rescale (only when the running max grows by > 2^8),
-//              P_j (bf16) written to smem in the UMMA K-major SW128 layout.
-// TMEM: S0 [0,128) S1 [128,256) O [256,384).
+// One CTA = two 128-row query tiles (A, B) x one head x one entry, so the
+// tensor core always has the other tile's work while one tile's softmax runs
+// on the MUFU/FMA pipes (ping-pong).
+//   warp 0     TMA: Q_A, Q_B once; then K_j, V_j through a 3-slot ring
+//   warp 1     MMA: S_X = Q_X K_j^T -> TMEM, O_X += P_X V_j (P from smem,
+//              V MN-major), X in {A, B}
+//   warps 4-7  softmax/correction/epilogue of tile A (thread = query row)
+//   warps 8-11 same for tile B
+// Online softmax with lazy rescale: the reference max only moves when the
+// running max grows by more than 2^8, so O (in TMEM) is rarely rescaled.
+// TMEM columns: S_A [0,128) S_B [128,256) O_A [256,384) O_B [384,512).
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -25,50 +29,174 @@
 
 #include "attention.h"
 #include "bc_common.h"
-#include "gemm.h"
 #include "sm100.cuh"
 
 namespace bc {
 namespace {
 
-constexpr int kRows = 128;     // query rows per CTA
-constexpr int kKeys = 128;     // keys per tile
-constexpr int kHd = 128;       // head dim
-constexpr int kHalf = 128 * 64 * 2;   // one 64-column half tile (16 KB)
-constexpr int kTile = 2 * kHalf;      // 128 x 128 bf16 (32 KB)
-constexpr int kStages = 2;
-constexpr int kThreads = 192;
+constexpr int kRows = 128;            // query rows per tile
+constexpr int kKeys = 128;            // keys per K/V tile
+constexpr int kHd = 128;              // head dim
+constexpr int kHalf = 128 * 64 * 2;   // 64-column half of a 128x128 bf16 tile (16 KB)
+constexpr int kTile = 2 * kHalf;      // 32 KB
+constexpr int kRing = 3;              // K/V ring slots
+constexpr int kThreads = 384;
 constexpr float kRescaleThresh = 8.0f;  // log2 domain
 
-struct AttnSmem {
-  static constexpr int q = 0;
-  static constexpr int k = q + kTile;
-  static constexpr int v = k + kStages * kTile;
-  static constexpr int p = v + kStages * kTile;
-  static constexpr int bars = p + kTile;
+struct Smem {
+  static constexpr int qa = 0;
+  static constexpr int qb = qa + kTile;
+  static constexpr int ring = qb + kTile;
+  static constexpr int pa = ring + kRing * kTile;
+  static constexpr int pb = pa + kTile;
+  static constexpr int bars = pb + kTile;
   static constexpr int total = bars + 256;
 };
+
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+struct SoftmaxBars {
+  uint64_t* s_full;
+  uint64_t* s_empty;
+  uint64_t* p_full;
+  uint64_t* o_ready;
+};
+
+// One softmax warpgroup: 128 threads, thread <-> query row of its tile.
+__device__ __forceinline__ void softmax_tile(const AttnParams& prm, uint32_t tmem_s, uint32_t tmem_o,
+                                             uint8_t* sp, SoftmaxBars b, int n_tiles, int tiles_per_slot,
+                                             uint32_t quad, int q_row0, int e, int head) {
+  const uint32_t row = quad * 32 + lane_id();
+  const uint32_t lane_base = (quad * 32) << 16;
+  const float c = prm.scale * 1.4426950408889634f;
+  float m_used = -INFINITY, l_sum = 0.0f;
+  for (int j = 0; j < n_tiles; ++j) {
+    const int t0 = (j % tiles_per_slot) * kKeys;
+    const int valid = min(kKeys, prm.kv_tokens - t0);
+    mbar_wait(b.s_full, j & 1);
+    tc_fence_after();
+    float s[128];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      uint32_t r[32];
+      tmem_ld32(tmem_s + lane_base + k * 32, r);
+      tmem_ld_wait();
+#pragma unroll
+      for (int i = 0; i < 32; ++i) s[k * 32 + i] = __uint_as_float(r[i]);
+    }
+    tc_fence_before();
+    mbar_arrive(b.s_empty);  // S buffer may now be overwritten by the next QK^T
+    if (valid < kKeys) {     // ragged last tile of a slot (warp-uniform)
+#pragma unroll
+      for (int i = 0; i < 128; ++i)
+        if (i >= valid) s[i] = -INFINITY;
+    }
+    float mx = s[0];
+#pragma unroll
+    for (int i = 1; i < 128; ++i) mx = fmaxf(mx, s[i]);
+    const float mt = mx * c;
+    float alpha = 1.0f;
+    const bool bump = (j == 0) || (mt > m_used + kRescaleThresh);
+    if (bump) {
+      const float m_new = fmaxf(m_used, mt);
+      alpha = (j == 0) ? 0.0f : ex2(m_used - m_new);
+      m_used = m_new;
+    }
+    // P = 2^(s*c - m) -> packed bf16 in registers (s dies as P is formed)
+    float tsum = 0.0f;
+    const float neg_m = -m_used;
+    uint32_t pk[64];
+#pragma unroll
+    for (int t = 0; t < 64; ++t) {
+      const float p0 = ex2(fmaf(s[2 * t], c, neg_m));
+      const float p1 = ex2(fmaf(s[2 * t + 1], c, neg_m));
+      tsum += p0 + p1;
+      pk[t] = pack_bf16(p0, p1);
+    }
+    // PV(j-1) must be complete before O is rescaled or P is overwritten
+    if (j > 0) {
+      mbar_wait(b.o_ready, (j - 1) & 1);
+      tc_fence_after();
+      if (__any_sync(0xffffffffu, bump)) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          uint32_t r[32];
+          tmem_ld32(tmem_o + lane_base + k * 32, r);
+          tmem_ld_wait();
+#pragma unroll
+          for (int i = 0; i < 32; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * alpha);
+          tmem_st32(tmem_o + lane_base + k * 32, r);
+        }
+        tmem_st_wait();
+      }
+    }
+    // P -> smem in the UMMA K-major SW128 layout: half h holds keys
+    // [64h, 64h+64); 16-byte chunk q of row r sits at chunk (q ^ (r & 7)).
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+      const int half = q >> 3, ch = q & 7;
+      *reinterpret_cast<uint4*>(sp + half * kHalf + row * 128 + ((ch ^ (row & 7)) << 4)) =
+          make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
+    }
+    l_sum = l_sum * alpha + tsum;
+    fence_async_shared();
+    tc_fence_before();
+    mbar_arrive(b.p_full);
+  }
+  // epilogue: O / l -> bf16
+  if (n_tiles > 0) {
+    mbar_wait(b.o_ready, (n_tiles - 1) & 1);
+    tc_fence_after();
+  }
+  const int qrow = q_row0 + (int)row;
+  const bool live = qrow < prm.q_tokens;
+  const float inv = (l_sum > 0.0f) ? 1.0f / l_sum : 0.0f;
+  __nv_bfloat16* out = static_cast<__nv_bfloat16*>(prm.out) +
+                       ((size_t)(e * prm.q_tokens + qrow) * prm.heads + head) * kHd;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    uint32_t r[32];
+    tmem_ld32(tmem_o + lane_base + k * 32, r);
+    tmem_ld_wait();
+    if (live) {
+      uint4* dst = reinterpret_cast<uint4*>(out + k * 32);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        uint4 v;
+        v.x = pack_bf16(__uint_as_float(r[8 * q + 0]) * inv, __uint_as_float(r[8 * q + 1]) * inv);
+        v.y = pack_bf16(__uint_as_float(r[8 * q + 2]) * inv, __uint_as_float(r[8 * q + 3]) * inv);
+        v.z = pack_bf16(__uint_as_float(r[8 * q + 4]) * inv, __uint_as_float(r[8 * q + 5]) * inv);
+        v.w = pack_bf16(__uint_as_float(r[8 * q + 6]) * inv, __uint_as_float(r[8 * q + 7]) * inv);
+        dst[q] = v;
+      }
+    }
+  }
+}
 
 __global__ void __launch_bounds__(kThreads, 1)
     attn_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_kv,
                 AttnParams prm) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + AttnSmem::bars);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Smem::bars);
   uint64_t* q_full = bars + 0;
-  uint64_t* k_full = bars + 1;   // [2]
-  uint64_t* k_empty = bars + 3;  // [2]
-  uint64_t* v_full = bars + 5;   // [2]
-  uint64_t* v_empty = bars + 7;  // [2]
-  uint64_t* s_full = bars + 9;   // [2]
-  uint64_t* s_empty = bars + 11; // [2]
-  uint64_t* p_full = bars + 13;
-  uint64_t* o_ready = bars + 14;
+  uint64_t* ring_full = bars + 1;   // [3]
+  uint64_t* ring_empty = bars + 4;  // [3]
+  uint64_t* s_full = bars + 7;      // [2] (A, B)
+  uint64_t* s_empty = bars + 9;     // [2]
+  uint64_t* p_full = bars + 11;     // [2]
+  uint64_t* o_ready = bars + 13;    // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 16);
 
-  const int qt = blockIdx.x, head = blockIdx.y, e = blockIdx.z;
-  const int q0 = qt * kRows;
-  if (q0 >= prm.q_tokens) return;
+  // grid: x = query-tile pair, y = entry, z = head (concurrent CTAs share a
+  // head's K/V in L2)
+  const int pair = blockIdx.x, e = blockIdx.y, head = blockIdx.z;
+  const int q0 = pair * 2 * kRows;
+  const bool has_b = q0 + kRows < prm.q_tokens;
   const int n_vis = prm.n_vis[e];
   const int tiles_per_slot = (prm.kv_tokens + kKeys - 1) / kKeys;
   const int n_tiles = n_vis * tiles_per_slot;
@@ -78,16 +206,16 @@ __global__ void __launch_bounds__(kThreads, 1)
     tma_prefetch(&map_q);
     tma_prefetch(&map_kv);
     mbar_init(q_full, 1);
+    for (int i = 0; i < kRing; ++i) {
+      mbar_init(&ring_full[i], 1);
+      mbar_init(&ring_empty[i], 1);
+    }
     for (int i = 0; i < 2; ++i) {
-      mbar_init(&k_full[i], 1);
-      mbar_init(&k_empty[i], 1);
-      mbar_init(&v_full[i], 1);
-      mbar_init(&v_empty[i], 1);
       mbar_init(&s_full[i], 1);
       mbar_init(&s_empty[i], 128);
+      mbar_init(&p_full[i], 128);
+      mbar_init(&o_ready[i], 1);
     }
-    mbar_init(p_full, 128);
-    mbar_init(o_ready, 1);
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc<512>(tmem_slot);
@@ -95,186 +223,100 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const uint32_t t_o = tmem + 256;
 
   if (warp == 0) {
     if (lane_id() == 0) {
       const int qrow = e * prm.q_tokens + q0;
-      mbar_arrive_expect_tx(q_full, kTile);
-      tma_load_3d(smem + AttnSmem::q, &map_q, q_full, 0, head, qrow);
-      tma_load_3d(smem + AttnSmem::q + kHalf, &map_q, q_full, 64, head, qrow);
-      for (int j = 0; j < n_tiles; ++j) {
-        const int st = j & 1;
-        const uint32_t ph = (j >> 1) & 1;
-        const int slot = prm.vis_slot[e][j / tiles_per_slot];
+      mbar_arrive_expect_tx(q_full, has_b ? 2 * kTile : kTile);
+      tma_load_3d(smem + Smem::qa, &map_q, q_full, 0, head, qrow);
+      tma_load_3d(smem + Smem::qa + kHalf, &map_q, q_full, 64, head, qrow);
+      if (has_b) {
+        tma_load_3d(smem + Smem::qb, &map_q, q_full, 0, head, qrow + kRows);
+        tma_load_3d(smem + Smem::qb + kHalf, &map_q, q_full, 64, head, qrow + kRows);
+      }
+      // ring order: K0 V0 K1 V1 ...
+      for (int i = 0; i < 2 * n_tiles; ++i) {
+        const int j = i >> 1, is_v = i & 1;
+        const int slot = i % kRing;
+        const uint32_t ph = (i / kRing) & 1;
+        const int kv_slot = prm.vis_slot[e][j / tiles_per_slot];
         const int t0 = (j % tiles_per_slot) * kKeys;
-        const int kmat = prm.mat_base + slot * prm.mat_stride;
-        const int vmat = kmat + prm.v_offset;
-        mbar_wait(&k_empty[st], ph ^ 1);
-        mbar_arrive_expect_tx(&k_full[st], kTile);
-        tma_load_4d(smem + AttnSmem::k + st * kTile, &map_kv, &k_full[st], 0, head, t0, kmat);
-        tma_load_4d(smem + AttnSmem::k + st * kTile + kHalf, &map_kv, &k_full[st], 64, head, t0, kmat);
-        mbar_wait(&v_empty[st], ph ^ 1);
-        mbar_arrive_expect_tx(&v_full[st], kTile);
-        tma_load_4d(smem + AttnSmem::v + st * kTile, &map_kv, &v_full[st], 0, head, t0, vmat);
-        tma_load_4d(smem + AttnSmem::v + st * kTile + kHalf, &map_kv, &v_full[st], 64, head, t0, vmat);
+        const int mat = prm.mat_base + kv_slot * prm.mat_stride + (is_v ? prm.v_offset : 0);
+        mbar_wait(&ring_empty[slot], ph ^ 1);
+        mbar_arrive_expect_tx(&ring_full[slot], kTile);
+        uint8_t* dst = smem + Smem::ring + slot * kTile;
+        tma_load_4d(dst, &map_kv, &ring_full[slot], 0, head, t0, mat);
+        tma_load_4d(dst + kHalf, &map_kv, &ring_full[slot], 64, head, t0, mat);
       }
     }
   } else if (warp == 1) {
     constexpr uint32_t idesc_qk = idesc_bf16(kRows, kKeys);
-    constexpr uint32_t idesc_pv = idesc_bf16(kRows, kHd, 0, 1);  // B (=V) MN-major
-    const uint32_t sq = smem_u32(smem + AttnSmem::q);
-    const uint32_t sp = smem_u32(smem + AttnSmem::p);
-    auto issue_qk = [&](int j) {
-      const int st = j & 1;
-      const uint32_t ph = (j >> 1) & 1;
-      mbar_wait(&s_empty[st], ph ^ 1);
-      mbar_wait(&k_full[st], ph);
-      tc_fence_after();
+    constexpr uint32_t idesc_pv = idesc_bf16(kRows, kHd, 0, 1);  // B (= V) MN-major
+    const uint32_t sq[2] = {smem_u32(smem + Smem::qa), smem_u32(smem + Smem::qb)};
+    const uint32_t sp[2] = {smem_u32(smem + Smem::pa), smem_u32(smem + Smem::pb)};
+    const int n_q = has_b ? 2 : 1;
+    auto ring_slot = [&](int i) { return smem_u32(smem + Smem::ring + (i % kRing) * kTile); };
+    auto ring_wait = [&](int i) { mbar_wait(&ring_full[i % kRing], (i / kRing) & 1); };
+    auto issue_qk = [&](int x, int j) {  // S_x = Q_x K_j^T ; K_j is ring item 2j
       if (elect_one()) {
-        const uint32_t sk = smem_u32(smem + AttnSmem::k + st * kTile);
+        const uint32_t sk = ring_slot(2 * j);
 #pragma unroll
         for (int k = 0; k < kHd / 16; ++k) {
           const uint32_t off = (k >> 2) * kHalf + (k & 3) * 32;
-          mma_bf16_ss(tmem + st * 128, desc_sw128(sq + off, 16, 1024), desc_sw128(sk + off, 16, 1024),
+          mma_bf16_ss(tmem + x * 128, desc_sw128(sq[x] + off, 16, 1024), desc_sw128(sk + off, 16, 1024),
                       idesc_qk, k != 0);
         }
-        mma_commit(&k_empty[st]);
-        mma_commit(&s_full[st]);
+        mma_commit(&s_full[x]);
       }
       __syncwarp();
     };
-    mbar_wait(q_full, 0);
-    if (n_tiles > 0) issue_qk(0);
-    for (int j = 0; j < n_tiles; ++j) {
-      if (j + 1 < n_tiles) issue_qk(j + 1);
-      const int st = j & 1;
-      const uint32_t ph = (j >> 1) & 1;
-      mbar_wait(p_full, j & 1);
-      mbar_wait(&v_full[st], ph);
-      tc_fence_after();
+    auto issue_pv = [&](int x, int j) {  // O_x += P_x V_j ; V_j is ring item 2j+1
       if (elect_one()) {
-        const uint32_t sv = smem_u32(smem + AttnSmem::v + st * kTile);
+        const uint32_t sv = ring_slot(2 * j + 1);
 #pragma unroll
         for (int k = 0; k < kKeys / 16; ++k) {
-          // A = P [128 rows x 128 keys] K-major; B = V [128 keys x 128 dims] MN-major
           const uint32_t aoff = (k >> 2) * kHalf + (k & 3) * 32;
-          const uint64_t ad = desc_sw128(sp + aoff, 16, 1024);
-          const uint64_t bd = desc_sw128(sv + k * 2048, kHalf, 1024);
-          mma_bf16_ss(t_o, ad, bd, idesc_pv, (j | k) != 0);
+          mma_bf16_ss(tmem + 256 + x * 128, desc_sw128(sp[x] + aoff, 16, 1024),
+                      desc_sw128(sv + k * 2048, kHalf, 1024), idesc_pv, (j | k) != 0);
         }
-        mma_commit(&v_empty[st]);
-        mma_commit(o_ready);
+        mma_commit(&o_ready[x]);
       }
       __syncwarp();
-    }
-  } else {
-    // softmax / correction / epilogue: 128 threads, thread <-> query row
-    const uint32_t quad = warp & 3;
-    const uint32_t row = quad * 32 + lane_id();
-    const uint32_t lane_base = (quad * 32) << 16;
-    const float scale_log2 = prm.scale * 1.4426950408889634f;
-    float m_used = -INFINITY, l_sum = 0.0f;
-    uint8_t* sp = smem + AttnSmem::p;
-    for (int j = 0; j < n_tiles; ++j) {
-      const int st = j & 1;
-      const uint32_t ph = (j >> 1) & 1;
-      const int t0 = (j % tiles_per_slot) * kKeys;
-      const int valid = min(kKeys, prm.kv_tokens - t0);
-      mbar_wait(&s_full[st], ph);
-      tc_fence_after();
-      float s[128];
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        uint32_t r[32];
-        tmem_ld32(tmem + lane_base + st * 128 + c * 32, r);
-        tmem_ld_wait();
-#pragma unroll
-        for (int i = 0; i < 32; ++i) s[c * 32 + i] = __uint_as_float(r[i]);
-      }
-      tc_fence_before();
-      mbar_arrive(&s_empty[st]);
-      float mt = -INFINITY;
-#pragma unroll
-      for (int i = 0; i < 128; ++i) {
-        s[i] = (i < valid) ? s[i] * scale_log2 : -INFINITY;
-        mt = fmaxf(mt, s[i]);
-      }
-      // lazy rescale: move the reference max only when it grows by > 2^8
-      float alpha = 1.0f;
-      const bool bump = (j == 0) || (mt > m_used + kRescaleThresh);
-      if (bump) {
-        const float m_new = fmaxf(m_used, mt);
-        alpha = (j == 0) ? 0.0f : exp2f(m_used - m_new);
-        m_used = m_new;
-      }
-      float tsum = 0.0f;
-      uint32_t pk[64];
-#pragma unroll
-      for (int i = 0; i < 64; ++i) {
-        const float p0 = exp2f(s[2 * i] - m_used);
-        const float p1 = exp2f(s[2 * i + 1] - m_used);
-        tsum += p0 + p1;
-        pk[i] = pack_bf16(p0, p1);
-      }
-      l_sum = l_sum * alpha + tsum;
-      // PV(j-1) must be complete before O is rescaled or P is overwritten
-      if (j > 0) {
-        mbar_wait(o_ready, (j - 1) & 1);
-        tc_fence_after();
-        const bool any_bump = __any_sync(0xffffffffu, bump && alpha != 1.0f);
-        if (any_bump) {
-#pragma unroll
-          for (int c = 0; c < 4; ++c) {
-            uint32_t r[32];
-            tmem_ld32(t_o + lane_base + c * 32, r);
-            tmem_ld_wait();
-#pragma unroll
-            for (int i = 0; i < 32; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * alpha);
-            tmem_st32(t_o + lane_base + c * 32, r);
-          }
-          tmem_st_wait();
-        }
-      }
-      // P row -> smem, K-major SW128: half h holds keys [64h, 64h+64),
-      // 16-byte chunk c of row r lands at chunk (c ^ (r & 7)).
-#pragma unroll
-      for (int c = 0; c < 16; ++c) {
-        const int half = c >> 3, ch = c & 7;
-        uint8_t* dst = sp + half * kHalf + row * 128 + ((ch ^ (row & 7)) << 4);
-        *reinterpret_cast<uint4*>(dst) = make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
-      }
-      fence_async_shared();
-      tc_fence_before();
-      mbar_arrive(p_full);
-    }
-    // epilogue: O / l -> bf16 out
+    };
+    auto release = [&](int i) {
+      if (elect_one()) mma_commit(&ring_empty[i % kRing]);
+      __syncwarp();
+    };
+    mbar_wait(q_full, 0);
     if (n_tiles > 0) {
-      mbar_wait(o_ready, (n_tiles - 1) & 1);
+      ring_wait(0);
       tc_fence_after();
+      for (int x = 0; x < n_q; ++x) issue_qk(x, 0);
+      release(0);
     }
-    const int qrow = q0 + (int)row;
-    const bool live = qrow < prm.q_tokens;
-    const float inv = (l_sum > 0.0f) ? 1.0f / l_sum : 0.0f;
-    __nv_bfloat16* out = static_cast<__nv_bfloat16*>(prm.out) +
-                         ((size_t)(e * prm.q_tokens + qrow) * prm.heads + head) * kHd;
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      uint32_t r[32];
-      tmem_ld32(t_o + lane_base + c * 32, r);
-      tmem_ld_wait();
-      if (live) {
-        uint4* dst = reinterpret_cast<uint4*>(out + c * 32);
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          uint4 v;
-          v.x = pack_bf16(__uint_as_float(r[8 * q + 0]) * inv, __uint_as_float(r[8 * q + 1]) * inv);
-          v.y = pack_bf16(__uint_as_float(r[8 * q + 2]) * inv, __uint_as_float(r[8 * q + 3]) * inv);
-          v.z = pack_bf16(__uint_as_float(r[8 * q + 4]) * inv, __uint_as_float(r[8 * q + 5]) * inv);
-          v.w = pack_bf16(__uint_as_float(r[8 * q + 6]) * inv, __uint_as_float(r[8 * q + 7]) * inv);
-          dst[q] = v;
+    for (int j = 0; j < n_tiles; ++j) {
+      const bool next = j + 1 < n_tiles;
+      for (int x = 0; x < n_q; ++x) {
+        if (next) {
+          mbar_wait(&s_empty[x], j & 1);  // softmax x has read S_x(j)
+          if (x == 0) ring_wait(2 * (j + 1));
+          tc_fence_after();
+          issue_qk(x, j + 1);
         }
+        mbar_wait(&p_full[x], j & 1);
+        if (x == 0) ring_wait(2 * j + 1);
+        tc_fence_after();
+        issue_pv(x, j);
       }
+      if (next) release(2 * (j + 1));
+      release(2 * j + 1);
+    }
+  } else if (warp >= 4) {
+    const int x = (warp >= 8) ? 1 : 0;
+    if (x == 0 || has_b) {
+      SoftmaxBars b{&s_full[x], &s_empty[x], &p_full[x], &o_ready[x]};
+      softmax_tile(prm, tmem + x * 128, tmem + 256 + x * 128, smem + (x ? Smem::pb : Smem::pa), b, n_tiles,
+                   tiles_per_slot, warp & 3, q0 + x * kRows, e, head);
     }
   }
   tc_fence_before();
@@ -295,13 +337,13 @@ PFN_cuTensorMapEncodeTiled_v12000 encoder() {
   return fn;
 }
 
-int encode(CUtensorMap* map, const void* base, int rank, const cuuint64_t* dims,
-           const cuuint64_t* strides, const cuuint32_t* box) {
+int encode(CUtensorMap* map, const void* base, int rank, const cuuint64_t* dims, const cuuint64_t* strides,
+           const cuuint32_t* box) {
   auto fn = encoder();
   if (!fn) return bc_fail(BC_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
   cuuint32_t estr[5] = {1, 1, 1, 1, 1};
-  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, const_cast<void*>(base), dims, strides,
-                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, const_cast<void*>(base), dims, strides, box,
+                  estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return bc_fail(BC_ERR_CUDA, "attention tensor map encode failed (%d)", (int)r);
   return BC_OK;
@@ -339,19 +381,17 @@ int attention_run(const AttnArgs& a, cudaStream_t st) {
   p.scale = a.scale;
   p.out = a.out;
   for (int e = 0; e < a.n_entries; ++e) {
-    if (a.n_vis[e] < 0 || a.n_vis[e] > BC_MAX_VIS)
-      return bc_fail(BC_ERR_CONTRACT, "attention: bad visible count");
+    if (a.n_vis[e] < 0 || a.n_vis[e] > BC_MAX_VIS) return bc_fail(BC_ERR_CONTRACT, "attention: bad visible count");
     p.n_vis[e] = a.n_vis[e];
     for (int v = 0; v < a.n_vis[e]; ++v) p.vis_slot[e][v] = a.vis_slot[e][v];
   }
   static bool attr = false;
   if (!attr) {
-    BC_CUDA(cudaFuncSetAttribute(attn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 AttnSmem::total + 1024));
+    BC_CUDA(cudaFuncSetAttribute(attn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, Smem::total + 1024));
     attr = true;
   }
-  dim3 grid((a.q_tokens + kRows - 1) / kRows, a.heads, a.n_entries);
-  attn_kernel<<<grid, kThreads, AttnSmem::total + 1024, st>>>(mq, mkv, p);
+  dim3 grid((a.q_tokens + 2 * kRows - 1) / (2 * kRows), a.n_entries, a.heads);
+  attn_kernel<<<grid, kThreads, Smem::total + 1024, st>>>(mq, mkv, p);
   BC_LAUNCHED();
   return BC_OK;
 }
@@ -360,7 +400,7 @@ int attention_run(const AttnArgs& a, cudaStream_t st) {
 
 // Self-attention over KV-arena slots.  k_arena points at layer 0 of an
 // arena laid out [L][n_slots][2][T][heads*128]; slot_stride_elems is the
-// distance between consecutive (K or V) matrices in elements (T*heads*128).
+// distance between consecutive slots' K matrices in elements.
 extern "C" int bc_attention_paged(const void* q, const void* k_arena, const void* v_arena,
                                   int64_t slot_stride_elems, int32_t kv_tokens, const bc_batch* batch,
                                   int32_t q_per_entry, int32_t heads, void* out, void* stream) {
