@@ -29,6 +29,8 @@ namespace {
 constexpr int BM = 128;
 constexpr int BK = 64;  // 64 bf16 = 128 B = one swizzle atom row
 constexpr int kThreads = 192;
+constexpr int kStagePitch = 36;  // floats per staged row (32 + 4 pad, 16 B aligned)
+constexpr int kEpiStageBytes = 4 * 32 * kStagePitch * 4;
 
 template <int BN>
 struct GemmCfg {
@@ -37,8 +39,23 @@ struct GemmCfg {
   static constexpr int kBBytes = BN * BK * 2;
   static constexpr int kStageBytes = kABytes + kBBytes;
   static constexpr int kTmemCols = 2 * BN >= 32 ? 2 * BN : 32;
-  static constexpr size_t kSmem = 1024 /*align slack*/ + (size_t)kStages * kStageBytes + 256;
+  static constexpr size_t kSmem = 1024 /*align slack*/ + (size_t)kStages * kStageBytes + 256 + kEpiStageBytes;
 };
+
+// Grouped rasterisation: tiles run in bands of kGroupM M-tiles with N
+// fastest inside a band, so the ~148 concurrent tiles cover a compact
+// (M x N) rectangle and both operand panels stay L2-resident (with plain
+// M-fastest order a K=8960 GEMM re-reads A once per N column).
+constexpr int kGroupM = 16;
+__device__ __forceinline__ void tile_coords(int tile, int num_m, int num_n, int& m_blk, int& n_blk) {
+  const int per_group = kGroupM * num_n;
+  const int g = tile / per_group;
+  const int first = g * kGroupM;
+  const int gm = min(kGroupM, num_m - first);
+  const int r = tile - g * per_group;
+  m_blk = first + r % gm;
+  n_blk = r / gm;
+}
 
 __device__ __forceinline__ float gelu_tanh(float x) {
   const float k0 = 0.7978845608028654f, k1 = 0.044715f;
@@ -56,7 +73,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sa = smem;
   uint8_t* sb = smem + S * Cfg::kABytes;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * Cfg::kStageBytes);
+  float* epi_stage = reinterpret_cast<float*>(smem + S * Cfg::kStageBytes);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * Cfg::kStageBytes + kEpiStageBytes);
   uint64_t* empty = full + S;
   uint64_t* tfull = empty + S;
   uint64_t* tempty = tfull + 2;
@@ -92,8 +110,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       int stage = 0;
       uint32_t phase = 0;
       for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-        const int m0 = (tile % num_m) * BM;
-        const int n0 = (tile / num_m) * BN;
+        int mb, nb;
+        tile_coords(tile, num_m, num_n, mb, nb);
+        const int m0 = mb * BM, n0 = nb * BN;
         for (int kb = 0; kb < num_kb; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           mbar_arrive_expect_tx(&full[stage], Cfg::kStageBytes);
@@ -140,69 +159,73 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else {
-    // epilogue: warp w covers TMEM lanes 32*(w%4) .. +31  (rows of the tile)
+    // epilogue: warp w covers TMEM lanes 32*(w%4) .. +31 (rows of the tile).
+    // Each 32x32 chunk goes TMEM -> registers (row per lane, + bias / GELU)
+    // -> a padded per-warp smem stage -> coalesced global access, 4 rows x
+    // 32 columns per warp instruction (full 128 B lines for fp32).
     const uint32_t quad = warp & 3;
-    const uint32_t row_in_tile = quad * 32 + lane_id();
+    float* stage = epi_stage + (warp - 2) * (32 * kStagePitch);
+    const int sub_row = lane_id() >> 3;          // 0..3
+    const int sub_col = (lane_id() & 7) * 4;     // 0..28
     int it = 0;
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
       const int acc = it & 1;
       const uint32_t acc_phase = (it >> 1) & 1;
-      const int m0 = (tile % num_m) * BM;
-      const int n0 = (tile / num_m) * BN;
+      int mb, nb;
+      tile_coords(tile, num_m, num_n, mb, nb);
+      const int m0 = mb * BM, n0 = nb * BN;
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
-      const int row = m0 + (int)row_in_tile;
-      const bool live = row < M;
+      const int row_base = m0 + (int)quad * 32;
 #pragma unroll 1
       for (int c = 0; c < BN; c += 32) {
         uint32_t r[32];
         __syncwarp();
         tmem_ld32(tmem_base + ((quad * 32) << 16) + acc * BN + c, r);
         tmem_ld_wait();
-        if (live) {
         const int col = n0 + c;
-        float v[32];
+        float* srow = stage + lane_id() * kStagePitch;
 #pragma unroll
-        for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]) + (bias ? __ldg(bias + col + j) : 0.0f);
-        if (MODE == kEpiStoreBf16 || MODE == kEpiGeluBf16) {
+        for (int j = 0; j < 32; j += 4) {
+          float4 v;
+          v.x = __uint_as_float(r[j]) + (bias ? __ldg(bias + col + j) : 0.0f);
+          v.y = __uint_as_float(r[j + 1]) + (bias ? __ldg(bias + col + j + 1) : 0.0f);
+          v.z = __uint_as_float(r[j + 2]) + (bias ? __ldg(bias + col + j + 2) : 0.0f);
+          v.w = __uint_as_float(r[j + 3]) + (bias ? __ldg(bias + col + j + 3) : 0.0f);
           if (MODE == kEpiGeluBf16) {
-#pragma unroll
-            for (int j = 0; j < 32; ++j) v[j] = gelu_tanh(v[j]);
+            v.x = gelu_tanh(v.x);
+            v.y = gelu_tanh(v.y);
+            v.z = gelu_tanh(v.z);
+            v.w = gelu_tanh(v.w);
           }
-          uint4* dst = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(c_ptr) + (size_t)row * N + col);
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            uint4 pk;
-            pk.x = pack_bf16(v[q * 8 + 0], v[q * 8 + 1]);
-            pk.y = pack_bf16(v[q * 8 + 2], v[q * 8 + 3]);
-            pk.z = pack_bf16(v[q * 8 + 4], v[q * 8 + 5]);
-            pk.w = pack_bf16(v[q * 8 + 6], v[q * 8 + 7]);
-            dst[q] = pk;
-          }
-        } else if (MODE == kEpiStoreF32) {
-          float4* dst = reinterpret_cast<float4*>(static_cast<float*>(c_ptr) + (size_t)row * N + col);
-#pragma unroll
-          for (int q = 0; q < 8; ++q) dst[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
-        } else {  // kEpiResidualF32: C += gate * v
-          float4* dst = reinterpret_cast<float4*>(static_cast<float*>(c_ptr) + (size_t)row * N + col);
-          const float* g = gate ? gate + (size_t)(row / rows_per_gate) * gate_stride + col : nullptr;
-#pragma unroll
-          for (int q = 0; q < 8; ++q) {
-            float4 o = dst[q];
-            float g0 = 1.f, g1 = 1.f, g2 = 1.f, g3 = 1.f;
-            if (g) {
-              g0 = __ldg(g + 4 * q);
-              g1 = __ldg(g + 4 * q + 1);
-              g2 = __ldg(g + 4 * q + 2);
-              g3 = __ldg(g + 4 * q + 3);
-            }
-            o.x += g0 * v[4 * q];
-            o.y += g1 * v[4 * q + 1];
-            o.z += g2 * v[4 * q + 2];
-            o.w += g3 * v[4 * q + 3];
-            dst[q] = o;
-          }
+          *reinterpret_cast<float4*>(srow + j) = v;
         }
+        __syncwarp();
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int lr = i * 4 + sub_row;
+          const int row = row_base + lr;
+          const float4 v = *reinterpret_cast<const float4*>(stage + lr * kStagePitch + sub_col);
+          if (row < M) {
+            if (MODE == kEpiStoreBf16 || MODE == kEpiGeluBf16) {
+              uint2 pk;
+              pk.x = pack_bf16(v.x, v.y);
+              pk.y = pack_bf16(v.z, v.w);
+              *reinterpret_cast<uint2*>(static_cast<__nv_bfloat16*>(c_ptr) + (size_t)row * N + col + sub_col) = pk;
+            } else if (MODE == kEpiStoreF32) {
+              *reinterpret_cast<float4*>(static_cast<float*>(c_ptr) + (size_t)row * N + col + sub_col) = v;
+            } else {  // kEpiResidualF32: C += gate * v
+              float4* dst = reinterpret_cast<float4*>(static_cast<float*>(c_ptr) + (size_t)row * N + col + sub_col);
+              float4 g = make_float4(1.f, 1.f, 1.f, 1.f);
+              if (gate) g = __ldg(reinterpret_cast<const float4*>(gate + (size_t)(row / rows_per_gate) * gate_stride + col + sub_col));
+              float4 o = *dst;
+              o.x += g.x * v.x;
+              o.y += g.y * v.y;
+              o.z += g.z * v.z;
+              o.w += g.w * v.w;
+              *dst = o;
+            }
+          }
         }
       }
       tc_fence_before();
@@ -288,20 +311,11 @@ int make_tmap_2d(CUtensorMap* map, const void* base, uint64_t inner, uint64_t ou
 int num_sms() { return sm_count(); }
 
 int gemm_plan_bn(int M, int N) {
-  // choose the widest tile that still fills the machine reasonably
-  const int sms = sm_count();
+  // 128x256 tiles amortise the A panel over twice the columns and measured
+  // 10-20% faster per tile than 128x128; fall back to narrower tiles only
+  // when N does not divide or the wide tiling cannot fill one wave.
   const int mt = (M + BM - 1) / BM;
-  if (N % 256 == 0) {
-    const int t256 = mt * (N / 256);
-    const double waves256 = (double)t256 / sms;
-    const int t128 = mt * (N / 128);
-    const double waves128 = (double)t128 / sms;
-    // efficiency = work / (ceil(waves) * sms): prefer 256 unless 128 is clearly better
-    const double e256 = waves256 / (double)((t256 + sms - 1) / sms);
-    const double e128 = waves128 / (double)((t128 + sms - 1) / sms);
-    if (e256 >= e128 - 0.05) return 256;
-    return 128;
-  }
+  if (N % 256 == 0 && mt * (N / 256) >= sm_count()) return 256;
   if (N % 128 == 0) return 128;
   return 64;
 }
