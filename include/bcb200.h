@@ -179,6 +179,43 @@ typedef struct {
 int bc_wan_step(bc_wan_ctx* ctx, const bc_batch* batch, const bc_wan_update* upd,
                 int32_t* status, void* stream);
 
+/* ---- multi-GPU temporal parallelism (one process per GPU, NVLink P2P) ----
+ * Every rank holds a full KV-arena replica.  The q/k kernel writes each
+ * fresh K/V row into the local slot AND into every peer's replica (P2P
+ * stores), then publishes epoch into peers' flags[layer][slot]; attention
+ * waits (per visible slot) for flags >= need before its first tile of that
+ * slot; the head kernel publishes iteration-done epochs, which the next
+ * iteration's first K/V write waits for (no reader of a slot is overtaken).
+ * Pointers are device (IPC-mapped) addresses. */
+#define BC_MAX_PEERS 8
+typedef struct {
+  int32_t n_peers, my_rank, n_ranks;             /* n_ranks = n_peers + 1      */
+  void* peer_arena[BC_MAX_PEERS];
+  uint32_t* peer_flags[BC_MAX_PEERS];            /* peers' [L][n_slots]        */
+  uint32_t* peer_done[BC_MAX_PEERS];             /* peers' [n_ranks]           */
+  uint32_t* my_flags;                            /* ours, written by peers     */
+  uint32_t* my_done;
+  uint32_t* counters;                            /* >= 1 zeroed u32 (scratch)  */
+} bc_wan_peers;
+int bc_wan_set_peers(bc_wan_ctx* ctx, const bc_wan_peers* peers);
+
+typedef struct {
+  uint32_t epoch;                                 /* iteration epoch, >= 1     */
+  uint32_t need[BC_MAX_ENTRIES][BC_MAX_VIS];      /* wait epoch per visible slot (0 = none) */
+  int32_t stage;                                  /* -1 whole step; 0 begin; 1 layer part A; 2 part B; 3 end */
+  int32_t layer;
+} bc_wan_dist;
+int bc_wan_step_dist(bc_wan_ctx* ctx, const bc_batch* batch, const bc_wan_update* upd,
+                     const bc_wan_dist* dist, int32_t* status, void* stream);
+int bc_wan_signal_done(bc_wan_ctx* ctx, uint32_t epoch, void* stream);
+
+/* Device memory that can be shared with the other ranks' processes. */
+int bc_ipc_malloc(int64_t bytes, void** ptr, char handle[64]);
+int bc_ipc_open(const char handle[64], void** ptr);
+int bc_ipc_close(void* ptr);
+int bc_free(void* ptr);
+int bc_memset_async(void* ptr, int value, int64_t bytes, void* stream);
+
 /* ---------------------------------------------------------------------------
  * Building blocks, exported for the parity tests and the multi-GPU executor.
  * ------------------------------------------------------------------------- */

@@ -71,6 +71,21 @@ class WanUpdate(C.Structure):
                 ("out", C.c_void_p * MAX_ENTRIES)]
 
 
+MAX_PEERS = 8
+
+
+class WanPeers(C.Structure):
+    _fields_ = [("n_peers", C.c_int32), ("my_rank", C.c_int32), ("n_ranks", C.c_int32),
+                ("peer_arena", C.c_void_p * MAX_PEERS), ("peer_flags", C.c_void_p * MAX_PEERS),
+                ("peer_done", C.c_void_p * MAX_PEERS), ("my_flags", C.c_void_p),
+                ("my_done", C.c_void_p), ("counters", C.c_void_p)]
+
+
+class WanDist(C.Structure):
+    _fields_ = [("epoch", C.c_uint32), ("need", (C.c_uint32 * MAX_VIS) * MAX_ENTRIES),
+                ("stage", C.c_int32), ("layer", C.c_int32)]
+
+
 _SIGS = {
     "bc_last_error": (C.c_char_p, []),
     "bc_version": (C.c_char_p, []),
@@ -99,6 +114,15 @@ _SIGS = {
                                      C.c_int32, C.POINTER(Batch), C.c_int32, C.c_int32,
                                      C.c_void_p, C.c_void_p]),
     "bc_launch_count": (C.c_longlong, []),
+    "bc_wan_set_peers": (C.c_int, [C.c_void_p, C.POINTER(WanPeers)]),
+    "bc_wan_step_dist": (C.c_int, [C.c_void_p, C.POINTER(Batch), C.POINTER(WanUpdate),
+                                   C.POINTER(WanDist), C.c_void_p, C.c_void_p]),
+    "bc_wan_signal_done": (C.c_int, [C.c_void_p, C.c_uint32, C.c_void_p]),
+    "bc_ipc_malloc": (C.c_int, [C.c_int64, C.POINTER(C.c_void_p), C.c_char_p]),
+    "bc_ipc_open": (C.c_int, [C.c_char_p, C.POINTER(C.c_void_p)]),
+    "bc_ipc_close": (C.c_int, [C.c_void_p]),
+    "bc_free": (C.c_int, [C.c_void_p]),
+    "bc_memset_async": (C.c_int, [C.c_void_p, C.c_int, C.c_int64, C.c_void_p]),
     "bc_profile_enable": (C.c_int, [C.c_int]),
     "bc_profile_collect": (C.c_int, [C.POINTER(C.c_double), C.POINTER(C.c_double),
                                      C.POINTER(C.c_double), C.POINTER(C.c_int64), C.c_int]),

@@ -242,6 +242,19 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int kv_slot = prm.vis_slot[e][j / tiles_per_slot];
         const int t0 = (j % tiles_per_slot) * kKeys;
         const int mat = prm.mat_base + kv_slot * prm.mat_stride + (is_v ? prm.v_offset : 0);
+        if (!is_v && prm.flags && (j % tiles_per_slot) == 0) {
+          const uint32_t need = prm.need[e][j / tiles_per_slot];
+          if (need) {  // K/V of this block is pushed by a peer GPU: wait for it
+            const uint32_t* f = prm.flags + prm.flag_base + kv_slot;
+            uint32_t v;
+            for (;;) {
+              asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
+              if (v >= need) break;
+              __nanosleep(256);
+            }
+            asm volatile("fence.proxy.async.global;" ::: "memory");
+          }
+        }
         mbar_wait(&ring_empty[slot], ph ^ 1);
         mbar_arrive_expect_tx(&ring_full[slot], kTile);
         uint8_t* dst = smem + Smem::ring + slot * kTile;
@@ -383,8 +396,13 @@ int attention_run(const AttnArgs& a, cudaStream_t st) {
   for (int e = 0; e < a.n_entries; ++e) {
     if (a.n_vis[e] < 0 || a.n_vis[e] > BC_MAX_VIS) return bc_fail(BC_ERR_CONTRACT, "attention: bad visible count");
     p.n_vis[e] = a.n_vis[e];
-    for (int v = 0; v < a.n_vis[e]; ++v) p.vis_slot[e][v] = a.vis_slot[e][v];
+    for (int v = 0; v < a.n_vis[e]; ++v) {
+      p.vis_slot[e][v] = a.vis_slot[e][v];
+      p.need[e][v] = a.flags ? a.need[e][v] : 0u;
+    }
   }
+  p.flags = a.flags;
+  p.flag_base = a.flag_base;
   static bool attr = false;
   if (!attr) {
     BC_CUDA(cudaFuncSetAttribute(attn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, Smem::total + 1024));

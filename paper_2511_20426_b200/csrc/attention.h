@@ -19,6 +19,11 @@ struct AttnParams {
   void* out;       // bf16 [n_entries*q_tokens][heads*128]
   int n_vis[BC_MAX_ENTRIES];
   int vis_slot[BC_MAX_ENTRIES][BC_MAX_VIS];
+  // multi-GPU: before the first tile of visible slot v, wait until
+  // flags[flag_base + slot] >= need[e][v] (0 = no wait; peers publish)
+  const uint32_t* flags;
+  int flag_base;
+  uint32_t need[BC_MAX_ENTRIES][BC_MAX_VIS];
 };
 
 struct AttnArgs {
@@ -31,6 +36,9 @@ struct AttnArgs {
   void* out;
   int n_vis[BC_MAX_ENTRIES];
   int vis_slot[BC_MAX_ENTRIES][BC_MAX_VIS];
+  const uint32_t* flags;
+  int flag_base;
+  uint32_t need[BC_MAX_ENTRIES][BC_MAX_VIS];
 };
 
 int attention_run(const AttnArgs& a, cudaStream_t st);

@@ -26,6 +26,39 @@ __device__ __forceinline__ float warp_sum(float v) {
   return v;
 }
 __device__ __forceinline__ float silu(float x) { return x / (1.0f + __expf(-x)); }
+__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+// thread 0 of each CTA: wait until every peer reported iteration `want` done
+__device__ __forceinline__ void wait_peers_done(const PeerArgs& pa) {
+  if (pa.n_peers == 0 || pa.wait_done == 0) return;
+  if (threadIdx.x == 0) {
+    for (int r = 0; r < pa.n_ranks; ++r) {
+      if (r == pa.my_rank) continue;
+      while (ld_acquire_sys(pa.my_done + r) < pa.wait_done) __nanosleep(128);
+    }
+  }
+  __syncthreads();
+}
+// after all CTAs' stores: the last CTA to finish runs `fn` (publication)
+template <class F>
+__device__ __forceinline__ void last_cta_publish(uint32_t* ctr, F&& fn) {
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const uint32_t prev = atomicAdd(ctr, 1u);
+    if (prev == gridDim.x * gridDim.y - 1) {
+      __threadfence_system();
+      fn();
+      *ctr = 0;  // ready for the next launch on this stream
+    }
+  }
+}
 __device__ __forceinline__ float bf(const __nv_bfloat16 v) { return __bfloat162float(v); }
 
 // ------------------------------------------------------------ patchify
@@ -173,7 +206,8 @@ __global__ void qk_norm_rope_kernel(const __nv_bfloat16* __restrict__ qkv, int r
                                     QkArgs a) {
   const int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
-  if (row >= rows) return;
+  wait_peers_done(a.peer);
+  if (row < rows) {
   const int e = row / T, t = row % T;
   const int hw = a.hp * a.wp;
   const int fl = t / hw, rem = t % hw;
@@ -221,11 +255,27 @@ __global__ void qk_norm_rope_kernel(const __nv_bfloat16* __restrict__ qkv, int r
         o[j + 1] = __float2bfloat16(x0 * sn + x1 * cs);
       }
       reinterpret_cast<uint4*>(dst)[idx] = u;
+      if (which == 1) {  // fresh K -> every peer's replica (NVLink P2P store)
+        for (int p = 0; p < a.peer.n_peers; ++p)
+          reinterpret_cast<uint4*>(a.peer.arena[p] + (dst - a.arena))[idx] = u;
+      }
     }
   }
-  // v: plain copy into the slot
+  // v: plain copy into the slot (and the peers' replicas)
   const uint4* v4 = reinterpret_cast<const uint4*>(src + 2 * d);
-  for (int idx = lane; idx * 8 < d; idx += 32) reinterpret_cast<uint4*>(vdst)[idx] = v4[idx];
+  for (int idx = lane; idx * 8 < d; idx += 32) {
+    const uint4 u = v4[idx];
+    reinterpret_cast<uint4*>(vdst)[idx] = u;
+    for (int p = 0; p < a.peer.n_peers; ++p) reinterpret_cast<uint4*>(a.peer.arena[p] + (vdst - a.arena))[idx] = u;
+  }
+  }
+  if (a.peer.n_peers > 0) {
+    last_cta_publish(a.peer.ctr, [&] {
+      const int n = rows / T;
+      for (int p = 0; p < a.peer.n_peers; ++p)
+        for (int e2 = 0; e2 < n; ++e2) st_release_sys(a.peer.flags[p] + a.peer.flag_base + a.slot[e2], a.peer.epoch);
+    });
+  }
 }
 
 // in-place RMSNorm * weight over rows of width d (bf16), row stride ld
@@ -312,6 +362,17 @@ __global__ void head_update_kernel(const float* __restrict__ Y, int T, int F, in
     }
   }
   if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicCAS(status, 0, 1 + u.block[e]);
+  if (u.peer.n_peers > 0) {
+    last_cta_publish(u.peer.ctr, [&] {
+      for (int p = 0; p < u.peer.n_peers; ++p) st_release_sys(u.peer.done[p] + u.peer.my_rank, u.peer.epoch);
+    });
+  }
+}
+
+// idle rank (no entries this iteration): still publish iteration-done
+__global__ void signal_done_kernel(PeerArgs pa) {
+  __threadfence_system();
+  for (int p = 0; p < pa.n_peers; ++p) st_release_sys(pa.done[p] + pa.my_rank, pa.epoch);
 }
 
 __global__ void check_finite_kernel(EntryPtrs lat, int n_el, int32_t* status) {
@@ -414,6 +475,12 @@ int launch_head_update(const float* Y, int n, int T, int F, int H, int W, const 
                        cudaStream_t st) {
   const int n_el = F * 16 * H * W;
   head_update_kernel<<<dim3(grid_for(n_el, 256) / n + 1, n), 256, 0, st>>>(Y, T, F, H, W, u, status);
+  BC_LAUNCHED();
+  return BC_OK;
+}
+
+int launch_signal_done(const PeerArgs& p, cudaStream_t st) {
+  signal_done_kernel<<<1, 1, 0, st>>>(p);
   BC_LAUNCHED();
   return BC_OK;
 }

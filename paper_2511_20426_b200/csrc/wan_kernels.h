@@ -28,6 +28,24 @@ struct LnArgs {
   int entry_stride;
 };
 
+// Multi-GPU temporal parallelism: every rank keeps a full KV-arena replica;
+// the q/k kernel pushes each fresh K/V row to every peer's arena over
+// NVLink (P2P stores) and the last CTA publishes (layer, slot) ready epochs
+// into each peer's flag array; iteration-done epochs guard slot reuse.
+#define BC_MAX_PEERS 8
+struct PeerArgs {
+  int n_peers;                          // 0 = single GPU
+  __nv_bfloat16* arena[BC_MAX_PEERS];   // peers' arenas (same layout as ours)
+  uint32_t* flags[BC_MAX_PEERS];        // peers' [L][n_slots] ready epochs
+  uint32_t* done[BC_MAX_PEERS];         // peers' [n_ranks] iteration-done epochs
+  const uint32_t* my_done;              // ours, written by peers
+  int my_rank, n_ranks;
+  uint32_t epoch;                       // this iteration's epoch
+  uint32_t wait_done;                   // wait until every peer's done >= this (0 = no wait)
+  int flag_base;                        // layer * n_slots
+  uint32_t* ctr;                        // zeroed launch counter (last-CTA detection)
+};
+
 struct QkArgs {
   __nv_bfloat16* qout;
   __nv_bfloat16* arena;
@@ -37,6 +55,7 @@ struct QkArgs {
   int hp, wp;
   const float* norm_q;
   const float* norm_k;
+  PeerArgs peer;
 };
 
 struct UpdArgs {
@@ -47,6 +66,7 @@ struct UpdArgs {
   double next_level[BC_MAX_ENTRIES];
   int post[BC_MAX_ENTRIES];
   int block[BC_MAX_ENTRIES];
+  PeerArgs peer;  // iteration-done signal (flags/arena unused)
 };
 
 int launch_patchify(const EntryPtrs& lat, int n, int F, int H, int W, __nv_bfloat16* out, cudaStream_t st);
@@ -64,6 +84,7 @@ int launch_f32_to_bf16(const float* src, __nv_bfloat16* dst, int64_t n, cudaStre
 int launch_head_update(const float* Y, int n, int T, int F, int H, int W, const UpdArgs& u, int32_t* status,
                        cudaStream_t st);
 int launch_mod_combine(const float* base, const float* e0, int L, int n, int d, float* out, cudaStream_t st);
+int launch_signal_done(const PeerArgs& p, cudaStream_t st);
 int launch_check_finite(const EntryPtrs& lat, int n, int n_el, int32_t* status, cudaStream_t st);
 
 }  // namespace bc

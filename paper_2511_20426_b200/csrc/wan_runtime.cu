@@ -40,7 +40,19 @@ struct bc_wan_ctx {
   float *t_sin, *t_h, *t_e, *t_e0, *mod_all;
   __nv_bfloat16 *text_in, *text_h, *ctx, *text_tmp, *textkv;
   bool text_ready;
+  bc_wan_peers peers;
+  struct StepState {
+    bc_batch batch;
+    bc_wan_update upd;
+    int32_t* status;
+    uint32_t epoch;
+    int n, R;
+    double self_flops;
+    bc::AttnArgs sa, ca;
+    bc::QkArgs qa;
+  } step;
 };
+using StepState = bc_wan_ctx::StepState;
 
 namespace {
 
@@ -231,12 +243,11 @@ extern "C" int bc_wan_set_text(bc_wan_ctx* c, const float* states, void* stream)
   return BC_OK;
 }
 
-extern "C" int bc_wan_step(bc_wan_ctx* c, const bc_batch* batch, const bc_wan_update* upd, int32_t* status,
-                           void* stream) {
-  if (!c || !batch || !upd || !status) return bc_fail(BC_ERR_CONTRACT, "bc_wan_step: null argument");
-  if (!c->text_ready) return bc_fail(BC_ERR_CONTRACT, "bc_wan_step: bc_wan_set_text not called");
+// ---------------------------------------------------------------- stepping
+namespace {
+
+int validate_step(const bc_wan_ctx* c, const bc_batch* batch, const bc_wan_update* upd) {
   const bc_wan_dims& dm = c->dims;
-  const bc_wan_params& p = c->prm;
   const int n = batch->n_entries;
   if (n < 1 || n > c->E) return bc_fail(BC_ERR_CONTRACT, "bc_wan_step: %d entries (max %d)", n, c->E);
   if (batch->block_size != dm.block_size) return bc_fail(BC_ERR_CONTRACT, "bc_wan_step: block size mismatch");
@@ -253,9 +264,41 @@ extern "C" int bc_wan_step(bc_wan_ctx* c, const bc_batch* batch, const bc_wan_up
     if ((upd->post[e] == 1 || upd->post[e] == 3) && !upd->out[e])
       return bc_fail(BC_ERR_CONTRACT, "bc_wan_step: entry %d needs an output buffer", e);
   }
-  cudaStream_t st = (cudaStream_t)stream;
+  return BC_OK;
+}
+
+bc::PeerArgs peer_args(const bc_wan_ctx* c, uint32_t epoch) {
+  bc::PeerArgs pa{};
+  pa.n_peers = c->peers.n_peers;
+  for (int p = 0; p < pa.n_peers; ++p) {
+    pa.arena[p] = static_cast<__nv_bfloat16*>(c->peers.peer_arena[p]);
+    pa.flags[p] = c->peers.peer_flags[p];
+    pa.done[p] = c->peers.peer_done[p];
+  }
+  pa.my_done = c->peers.my_done;
+  pa.my_rank = c->peers.my_rank;
+  pa.n_ranks = c->peers.n_ranks;
+  pa.epoch = epoch;
+  pa.ctr = c->peers.counters;
+  return pa;
+}
+
+// stage 0: validation, patch embedding, time MLP, per-step argument blocks
+int stage_begin(bc_wan_ctx* c, const bc_batch* batch, const bc_wan_update* upd, const bc_wan_dist* dist,
+                int32_t* status, cudaStream_t st) {
+  RC(validate_step(c, batch, upd));
+  StepState& S = c->step;
+  S.batch = *batch;
+  S.upd = *upd;
+  S.status = status;
+  S.epoch = dist ? dist->epoch : 0u;
+  const bc_wan_dims& dm = c->dims;
+  const bc_wan_params& p = c->prm;
+  const int n = batch->n_entries;
   const int d = c->d, T = c->T, R = n * T, L = dm.layers, F = dm.block_size;
   const int H = dm.latent_h, W = dm.latent_w;
+  S.n = n;
+  S.R = R;
 
   bc::EntryPtrs lat{};
   for (int e = 0; e < n; ++e) {
@@ -277,7 +320,8 @@ extern "C" int bc_wan_step(bc_wan_ctx* c, const bc_batch* batch, const bc_wan_up
                      st));
   RC(bc::launch_mod_combine(p.modulation, c->t_e0, L, n, d, c->mod_all, st));
 
-  bc::AttnArgs sa{};
+  bc::AttnArgs& sa = S.sa;
+  sa = bc::AttnArgs{};
   sa.kv_base = c->arena;
   sa.n_mats = L * dm.n_slots * 2;
   sa.n_entries = n;
@@ -290,19 +334,27 @@ extern "C" int bc_wan_step(bc_wan_ctx* c, const bc_batch* batch, const bc_wan_up
   sa.scale = 0.08838834764831845f;  // 1/sqrt(128)
   sa.q = c->Q;
   sa.out = c->attn;
+  const bool multi = c->peers.n_peers > 0 && dist;
+  sa.flags = multi ? c->peers.my_flags : nullptr;
   for (int e = 0; e < n; ++e) {
     sa.n_vis[e] = batch->n_vis[e];
-    for (int v = 0; v < batch->n_vis[e]; ++v) sa.vis_slot[e][v] = batch->vis_slot[e][v];
+    for (int v = 0; v < batch->n_vis[e]; ++v) {
+      sa.vis_slot[e][v] = batch->vis_slot[e][v];
+      sa.need[e][v] = multi ? dist->need[e][v] : 0u;
+    }
   }
-  bc::AttnArgs ca = sa;
+  bc::AttnArgs& ca = S.ca;
+  ca = sa;
   ca.kv_base = c->textkv;
   ca.n_mats = L * 2;
   ca.kv_tokens = dm.text_len;
+  ca.flags = nullptr;
   for (int e = 0; e < n; ++e) {
     ca.n_vis[e] = 1;
     ca.vis_slot[e][0] = 0;
   }
-  bc::QkArgs qa{};
+  bc::QkArgs& qa = S.qa;
+  qa = bc::QkArgs{};
   qa.qout = c->Q;
   qa.arena = c->arena;
   qa.hp = H / 2;
@@ -311,55 +363,190 @@ extern "C" int bc_wan_step(bc_wan_ctx* c, const bc_batch* batch, const bc_wan_up
     qa.slot[e] = batch->slot[e];
     qa.frame0[e] = batch->block_index[e] * F;
   }
+  if (multi) qa.peer = peer_args(c, S.epoch);
+  S.self_flops = 0.0;
+  for (int e = 0; e < n; ++e) S.self_flops += 4.0 * T * ((double)batch->n_vis[e] * T) * d;
+  return BC_OK;
+}
 
-  double self_flops = 0.0;
-  for (int e = 0; e < n; ++e) self_flops += 4.0 * T * ((double)batch->n_vis[e] * T) * d;
-  for (int l = 0; l < L; ++l) {
-    const float* mod = c->mod_all + (size_t)l * n * 6 * d;  // [e][6][d]
-    bc::LnArgs ln{0, nullptr, nullptr, mod + 0 * d, mod + 1 * d, 6 * d};
-    RC(timed(kBandwidth, 0.0, 6.0 * R * d, st, [&] { return bc::launch_ln_rows(c->X, c->xn, R, d, T, ln, st); }));
-    RC(timed(kGemm, 2.0 * R * 3.0 * d * d, 0.0, st, [&] { return gemm(c->xn, at<__nv_bfloat16>(p.qkv_w, (int64_t)l * 3 * d * d), c->qkv, R, 3 * d, d, bc::kEpiStoreBf16,
-            p.qkv_b + (size_t)l * 3 * d, nullptr, 0, 1, st); }));
-    qa.mat_base = (int64_t)l * dm.n_slots * 2;
-    qa.norm_q = p.norm_q + (size_t)l * d;
-    qa.norm_k = p.norm_k + (size_t)l * d;
-    RC(timed(kBandwidth, 0.0, 12.0 * R * d, st, [&] { return bc::launch_qk_norm_rope(c->qkv, R, d, T, qa, st); }));
-    sa.mat_base = l * dm.n_slots * 2;
-    RC(timed(kSelfAttn, self_flops, 0.0, st, [&] { return bc::attention_run(sa, st); }));
-    RC(timed(kGemm, 2.0 * R * d * d, 0.0, st, [&] { return gemm(c->attn, at<__nv_bfloat16>(p.o_w, (int64_t)l * d * d), c->X, R, d, d, bc::kEpiResidualF32,
-            p.o_b + (size_t)l * d, mod + 2 * d, 6 * d, T, st); }));
-    // cross-attention
-    bc::LnArgs ln3{1, p.norm3_b + (size_t)l * d, p.norm3_w + (size_t)l * d, nullptr, nullptr, 0};
-    RC(timed(kBandwidth, 0.0, 6.0 * R * d, st, [&] { return bc::launch_ln_rows(c->X, c->xn, R, d, T, ln3, st); }));
-    RC(timed(kGemm, 2.0 * R * d * d, 0.0, st, [&] { return gemm(c->xn, at<__nv_bfloat16>(p.cq_w, (int64_t)l * d * d), c->Q, R, d, d, bc::kEpiStoreBf16,
-            p.cq_b + (size_t)l * d, nullptr, 0, 1, st); }));
-    RC(timed(kBandwidth, 0.0, 4.0 * R * d, st, [&] { return bc::launch_rms_rows(c->Q, R, d, d, p.cnorm_q + (size_t)l * d, c->Q, d, st); }));
-    ca.mat_base = l * 2;
-    RC(timed(kCrossAttn, 4.0 * R * (double)dm.text_len * d, 0.0, st, [&] { return bc::attention_run(ca, st); }));
-    RC(timed(kGemm, 2.0 * R * d * d, 0.0, st, [&] { return gemm(c->attn, at<__nv_bfloat16>(p.co_w, (int64_t)l * d * d), c->X, R, d, d, bc::kEpiResidualF32,
-            p.co_b + (size_t)l * d, nullptr, 0, 1, st); }));
-    // FFN
-    bc::LnArgs ln2{0, nullptr, nullptr, mod + 3 * d, mod + 4 * d, 6 * d};
-    RC(timed(kBandwidth, 0.0, 6.0 * R * d, st, [&] { return bc::launch_ln_rows(c->X, c->xn, R, d, T, ln2, st); }));
-    RC(timed(kGemm, 2.0 * R * (double)dm.ffn_dim * d, 0.0, st, [&] { return gemm(c->xn, at<__nv_bfloat16>(p.ffn1_w, (int64_t)l * dm.ffn_dim * d), c->H1, R, dm.ffn_dim, d,
-            bc::kEpiGeluBf16, p.ffn1_b + (size_t)l * dm.ffn_dim, nullptr, 0, 1, st); }));
-    RC(timed(kGemm, 2.0 * R * (double)dm.ffn_dim * d, 0.0, st, [&] { return gemm(c->H1, at<__nv_bfloat16>(p.ffn2_w, (int64_t)l * d * dm.ffn_dim), c->X, R, d, dm.ffn_dim,
-            bc::kEpiResidualF32, p.ffn2_b + (size_t)l * d, mod + 5 * d, 6 * d, T, st); }));
-  }
-  // head: LN(x) * (1 + head_mod[1] + e) + head_mod[0] + e -> Linear(d, 64)
+// stage 1: LN+AdaLN -> QKV GEMM -> q/k RMSNorm + RoPE, K/V into the own slot
+// (and pushed to every peer replica in multi-GPU mode)
+int stage_layer_a(bc_wan_ctx* c, int l, cudaStream_t st) {
+  StepState& S = c->step;
+  const bc_wan_dims& dm = c->dims;
+  const bc_wan_params& p = c->prm;
+  const int d = c->d, T = c->T, R = S.R, n = S.n;
+  const float* mod = c->mod_all + (size_t)l * n * 6 * d;  // [e][6][d]
+  bc::LnArgs ln{0, nullptr, nullptr, mod + 0 * d, mod + 1 * d, 6 * d};
+  RC(timed(kBandwidth, 0.0, 6.0 * R * d, st, [&] { return bc::launch_ln_rows(c->X, c->xn, R, d, T, ln, st); }));
+  RC(timed(kGemm, 2.0 * R * 3.0 * d * d, 0.0, st, [&] { return gemm(c->xn, at<__nv_bfloat16>(p.qkv_w, (int64_t)l * 3 * d * d), c->qkv, R, 3 * d, d, bc::kEpiStoreBf16,
+          p.qkv_b + (size_t)l * 3 * d, nullptr, 0, 1, st); }));
+  bc::QkArgs& qa = S.qa;
+  qa.mat_base = (int64_t)l * dm.n_slots * 2;
+  qa.norm_q = p.norm_q + (size_t)l * d;
+  qa.norm_k = p.norm_k + (size_t)l * d;
+  qa.peer.flag_base = l * dm.n_slots;
+  // the first K/V write of an iteration waits until every peer finished
+  // reading the previous iteration's KV (slot reuse / in-place rewrite)
+  qa.peer.wait_done = (l == 0 && S.epoch > 1) ? S.epoch - 1 : 0u;
+  RC(timed(kBandwidth, 0.0, 12.0 * R * d, st, [&] { return bc::launch_qk_norm_rope(c->qkv, R, d, T, qa, st); }));
+  return BC_OK;
+}
+
+// stage 2: self-attention -> O GEMM (+gate) -> cross-attention -> FFN
+int stage_layer_b(bc_wan_ctx* c, int l, cudaStream_t st) {
+  StepState& S = c->step;
+  const bc_wan_dims& dm = c->dims;
+  const bc_wan_params& p = c->prm;
+  const int d = c->d, T = c->T, R = S.R, n = S.n;
+  const float* mod = c->mod_all + (size_t)l * n * 6 * d;
+  S.sa.mat_base = l * dm.n_slots * 2;
+  S.sa.flag_base = l * dm.n_slots;
+  RC(timed(kSelfAttn, S.self_flops, 0.0, st, [&] { return bc::attention_run(S.sa, st); }));
+  RC(timed(kGemm, 2.0 * R * d * d, 0.0, st, [&] { return gemm(c->attn, at<__nv_bfloat16>(p.o_w, (int64_t)l * d * d), c->X, R, d, d, bc::kEpiResidualF32,
+          p.o_b + (size_t)l * d, mod + 2 * d, 6 * d, T, st); }));
+  bc::LnArgs ln3{1, p.norm3_b + (size_t)l * d, p.norm3_w + (size_t)l * d, nullptr, nullptr, 0};
+  RC(timed(kBandwidth, 0.0, 6.0 * R * d, st, [&] { return bc::launch_ln_rows(c->X, c->xn, R, d, T, ln3, st); }));
+  RC(timed(kGemm, 2.0 * R * d * d, 0.0, st, [&] { return gemm(c->xn, at<__nv_bfloat16>(p.cq_w, (int64_t)l * d * d), c->Q, R, d, d, bc::kEpiStoreBf16,
+          p.cq_b + (size_t)l * d, nullptr, 0, 1, st); }));
+  RC(timed(kBandwidth, 0.0, 4.0 * R * d, st, [&] { return bc::launch_rms_rows(c->Q, R, d, d, p.cnorm_q + (size_t)l * d, c->Q, d, st); }));
+  S.ca.mat_base = l * 2;
+  RC(timed(kCrossAttn, 4.0 * R * (double)dm.text_len * d, 0.0, st, [&] { return bc::attention_run(S.ca, st); }));
+  RC(timed(kGemm, 2.0 * R * d * d, 0.0, st, [&] { return gemm(c->attn, at<__nv_bfloat16>(p.co_w, (int64_t)l * d * d), c->X, R, d, d, bc::kEpiResidualF32,
+          p.co_b + (size_t)l * d, nullptr, 0, 1, st); }));
+  bc::LnArgs ln2{0, nullptr, nullptr, mod + 3 * d, mod + 4 * d, 6 * d};
+  RC(timed(kBandwidth, 0.0, 6.0 * R * d, st, [&] { return bc::launch_ln_rows(c->X, c->xn, R, d, T, ln2, st); }));
+  RC(timed(kGemm, 2.0 * R * (double)dm.ffn_dim * d, 0.0, st, [&] { return gemm(c->xn, at<__nv_bfloat16>(p.ffn1_w, (int64_t)l * dm.ffn_dim * d), c->H1, R, dm.ffn_dim, d,
+          bc::kEpiGeluBf16, p.ffn1_b + (size_t)l * dm.ffn_dim, nullptr, 0, 1, st); }));
+  RC(timed(kGemm, 2.0 * R * (double)dm.ffn_dim * d, 0.0, st, [&] { return gemm(c->H1, at<__nv_bfloat16>(p.ffn2_w, (int64_t)l * d * dm.ffn_dim), c->X, R, d, dm.ffn_dim,
+          bc::kEpiResidualF32, p.ffn2_b + (size_t)l * d, mod + 5 * d, 6 * d, T, st); }));
+  return BC_OK;
+}
+
+// stage 3: head LN + modulation -> head GEMM -> unpatchify + x0 + renoise/emit
+int stage_end(bc_wan_ctx* c, cudaStream_t st) {
+  StepState& S = c->step;
+  const bc_wan_dims& dm = c->dims;
+  const bc_wan_params& p = c->prm;
+  const int d = c->d, T = c->T, R = S.R, n = S.n, F = dm.block_size;
   bc::LnArgs lh{0, p.head_mod, p.head_mod + d, c->t_e, c->t_e, d};
   RC(timed(kBandwidth, 0.0, 6.0 * R * d, st, [&] { return bc::launch_ln_rows(c->X, c->xn, R, d, T, lh, st); }));
   RC(timed(kGemm, 2.0 * R * 64.0 * d, 0.0, st, [&] { return gemm(c->xn, p.head_w, c->Y, R, 64, d, bc::kEpiStoreF32, p.head_b, nullptr, 0, 1, st); }));
   bc::UpdArgs u{};
   for (int e = 0; e < n; ++e) {
-    u.latents[e] = upd->latents[e];
-    u.eps[e] = upd->eps[e];
-    u.out[e] = upd->out[e];
-    u.level[e] = batch->level[e];
-    u.next_level[e] = upd->next_level[e];
-    u.post[e] = upd->post[e];
-    u.block[e] = batch->block_index[e];
+    u.latents[e] = S.upd.latents[e];
+    u.eps[e] = S.upd.eps[e];
+    u.out[e] = S.upd.out[e];
+    u.level[e] = S.batch.level[e];
+    u.next_level[e] = S.upd.next_level[e];
+    u.post[e] = S.upd.post[e];
+    u.block[e] = S.batch.block_index[e];
   }
-  RC(timed(kBandwidth, 0.0, (4.0 * 64 + 16.0 * 16) * R, st, [&] { return bc::launch_head_update(c->Y, n, T, F, H, W, u, status, st); }));
+  if (c->peers.n_peers > 0 && S.epoch > 0) u.peer = peer_args(c, S.epoch);
+  RC(timed(kBandwidth, 0.0, (4.0 * 64 + 16.0 * 16) * R, st, [&] { return bc::launch_head_update(c->Y, n, T, F, dm.latent_h, dm.latent_w, u, S.status, st); }));
+  return BC_OK;
+}
+
+}  // namespace
+
+extern "C" int bc_wan_step(bc_wan_ctx* c, const bc_batch* batch, const bc_wan_update* upd, int32_t* status,
+                           void* stream) {
+  if (!c || !batch || !upd || !status) return bc_fail(BC_ERR_CONTRACT, "bc_wan_step: null argument");
+  if (!c->text_ready) return bc_fail(BC_ERR_CONTRACT, "bc_wan_step: bc_wan_set_text not called");
+  if (c->peers.n_peers > 0) return bc_fail(BC_ERR_CONTRACT, "bc_wan_step: peers attached, use bc_wan_step_dist");
+  cudaStream_t st = (cudaStream_t)stream;
+  RC(stage_begin(c, batch, upd, nullptr, status, st));
+  for (int l = 0; l < c->dims.layers; ++l) {
+    RC(stage_layer_a(c, l, st));
+    RC(stage_layer_b(c, l, st));
+  }
+  return stage_end(c, st);
+}
+
+extern "C" int bc_wan_set_peers(bc_wan_ctx* c, const bc_wan_peers* peers) {
+  if (!c || !peers) return bc_fail(BC_ERR_CONTRACT, "bc_wan_set_peers: null argument");
+  if (peers->n_peers < 0 || peers->n_peers > BC_MAX_PEERS || peers->n_ranks != peers->n_peers + 1 ||
+      peers->my_rank < 0 || peers->my_rank >= peers->n_ranks)
+    return bc_fail(BC_ERR_CONTRACT, "bc_wan_set_peers: bad rank geometry");
+  if (peers->n_peers > 0 && (!peers->my_flags || !peers->my_done || !peers->counters))
+    return bc_fail(BC_ERR_CONTRACT, "bc_wan_set_peers: flags / done / counters required");
+  for (int p = 0; p < peers->n_peers; ++p)
+    if (!peers->peer_arena[p] || !peers->peer_flags[p] || !peers->peer_done[p])
+      return bc_fail(BC_ERR_CONTRACT, "bc_wan_set_peers: null peer pointer");
+  c->peers = *peers;
+  return BC_OK;
+}
+
+// Multi-GPU step of this rank's entries (or one stage of it, for drivers
+// that interleave several ranks on one device).
+extern "C" int bc_wan_step_dist(bc_wan_ctx* c, const bc_batch* batch, const bc_wan_update* upd,
+                                const bc_wan_dist* dist, int32_t* status, void* stream) {
+  if (!c || !dist || !status) return bc_fail(BC_ERR_CONTRACT, "bc_wan_step_dist: null argument");
+  if (!c->text_ready) return bc_fail(BC_ERR_CONTRACT, "bc_wan_step_dist: bc_wan_set_text not called");
+  if (dist->epoch < 1) return bc_fail(BC_ERR_CONTRACT, "bc_wan_step_dist: epoch must be >= 1");
+  cudaStream_t st = (cudaStream_t)stream;
+  switch (dist->stage) {
+    case -1:
+      if (!batch || !upd) return bc_fail(BC_ERR_CONTRACT, "bc_wan_step_dist: null batch");
+      RC(stage_begin(c, batch, upd, dist, status, st));
+      for (int l = 0; l < c->dims.layers; ++l) {
+        RC(stage_layer_a(c, l, st));
+        RC(stage_layer_b(c, l, st));
+      }
+      return stage_end(c, st);
+    case 0:
+      if (!batch || !upd) return bc_fail(BC_ERR_CONTRACT, "bc_wan_step_dist: null batch");
+      return stage_begin(c, batch, upd, dist, status, st);
+    case 1:
+      return stage_layer_a(c, dist->layer, st);
+    case 2:
+      return stage_layer_b(c, dist->layer, st);
+    case 3:
+      return stage_end(c, st);
+  }
+  return bc_fail(BC_ERR_CONTRACT, "bc_wan_step_dist: bad stage %d", dist->stage);
+}
+
+// A rank with no entries this iteration still publishes iteration-done.
+extern "C" int bc_wan_signal_done(bc_wan_ctx* c, uint32_t epoch, void* stream) {
+  if (!c) return bc_fail(BC_ERR_CONTRACT, "bc_wan_signal_done: null ctx");
+  if (c->peers.n_peers == 0) return BC_OK;
+  return bc::launch_signal_done(peer_args(c, epoch), (cudaStream_t)stream);
+}
+
+// ---------------------------------------------------------------- IPC memory
+extern "C" int bc_ipc_malloc(int64_t bytes, void** ptr, char handle[64]) {
+  if (!ptr || bytes <= 0) return bc_fail(BC_ERR_CONTRACT, "bc_ipc_malloc: bad arguments");
+  BC_CUDA(cudaMalloc(ptr, (size_t)bytes));
+  BC_CUDA(cudaMemset(*ptr, 0, (size_t)bytes));
+  if (handle) {
+    cudaIpcMemHandle_t h;
+    BC_CUDA(cudaIpcGetMemHandle(&h, *ptr));
+    static_assert(sizeof(h) == 64, "IPC handle size");
+    std::memcpy(handle, &h, 64);
+  }
+  return BC_OK;
+}
+
+extern "C" int bc_ipc_open(const char handle[64], void** ptr) {
+  if (!handle || !ptr) return bc_fail(BC_ERR_CONTRACT, "bc_ipc_open: null argument");
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle, 64);
+  BC_CUDA(cudaIpcOpenMemHandle(ptr, h, cudaIpcMemLazyEnablePeerAccess));
+  return BC_OK;
+}
+
+extern "C" int bc_ipc_close(void* ptr) {
+  BC_CUDA(cudaIpcCloseMemHandle(ptr));
+  return BC_OK;
+}
+
+extern "C" int bc_free(void* ptr) {
+  BC_CUDA(cudaFree(ptr));
+  return BC_OK;
+}
+
+extern "C" int bc_memset_async(void* ptr, int value, int64_t bytes, void* stream) {
+  BC_CUDA(cudaMemsetAsync(ptr, value, (size_t)bytes, (cudaStream_t)stream));
   return BC_OK;
 }

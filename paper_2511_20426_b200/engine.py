@@ -101,8 +101,13 @@ class _Session:
         self.session.close()
 
 
-def _pool_entry_frames(pool: KVPool) -> int:
-    return pool.frame_count()
+def _collect_outputs(dev, blocks) -> dict:
+    """Emitted blocks as host arrays; multi-GPU sessions gather them from
+    their owner ranks."""
+    gather = getattr(dev, "gather_outputs", None)
+    if gather is not None:
+        return gather(list(blocks))
+    return {b: dev.emitted_host(b) for b in blocks}
 
 
 def run_cascade(config: CascadeConfig, prompt: str,
@@ -235,7 +240,7 @@ def run_cascade(config: CascadeConfig, prompt: str,
             if pace_seconds > 0.0:
                 time.sleep(pace_seconds)
         dev.fill_wall_times(pending)
-        outputs = {b: dev.emitted_host(b) for b in state.emitted}
+        outputs = _collect_outputs(dev, state.emitted)
     finally:
         sess.close()
     if command_queue is not None:
@@ -313,7 +318,7 @@ def run_sequential_reference(config: CascadeConfig, prompt: str,
                                           if emitted_block is not None else None)))
                 it += 1
         dev.fill_wall_times(trace.events)
-        outputs = {blk: dev.emitted_host(blk) for blk in emitted_order}
+        outputs = _collect_outputs(dev, emitted_order)
     finally:
         sess.close()
     return RunResult(outputs=outputs, trace=trace, pool=pool, emitted_order=emitted_order)

@@ -125,7 +125,7 @@ def text_states(cond, text_len: int, text_dim: int) -> np.ndarray:
 class _Ctx:
     """One bc_wan_ctx plus the arena / workspace it was created over."""
 
-    def __init__(self, weights: WanWeights, max_entries: int, n_slots: int):
+    def __init__(self, weights: WanWeights, max_entries: int, n_slots: int, arena=None):
         torch = N.torch_mod()
         cfg = weights.config
         self.cfg, self.weights = cfg, weights
@@ -141,8 +141,8 @@ class _Ctx:
         need = N.lib().bc_wan_workspace_bytes(dims)
         if need < 0:
             raise ContractViolation("bc_wan_workspace_bytes rejected the dims")
-        self.arena = torch.zeros((cfg.layers, n_slots, 2, self.T, self.d), dtype=torch.bfloat16,
-                                 device="cuda")
+        self.arena = arena if arena is not None else torch.zeros(
+            (cfg.layers, n_slots, 2, self.T, self.d), dtype=torch.bfloat16, device="cuda")
         self.workspace = torch.empty(int(need), dtype=torch.uint8, device="cuda")
         prm = N.WanParams()
         for name in N.WAN_PARAM_FIELDS:
@@ -264,6 +264,17 @@ class WanRuntime:
             ctx.close()
 
     def open_session(self, config, conditioning, session_seed, noise_feed=None):
+        from . import distributed
+        try:
+            import torch.distributed as dist
+            multi = dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1
+        except ImportError:  # pragma: no cover
+            multi = False
+        if multi:
+            return distributed.DistWanSession(self, config, conditioning, session_seed, noise_feed)
+        if distributed.EMULATE and config.workers > 1:
+            return distributed.EmulatedRanks(self, config, conditioning, session_seed,
+                                             config.workers, noise_feed)
         return WanSession(self, config, conditioning, session_seed, noise_feed)
 
 

@@ -1,0 +1,87 @@
+"""Host-side logic of the multi-GPU path with world_size 2 over gloo on CPU:
+every rank derives the same slot tables and wait epochs from the shared
+schedule, and the ranks' entry sets partition every plan."""
+
+import os
+import socket
+
+import pytest
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_2511_20426_b200 as bc
+        from paper_2511_20426_b200.distributed import SlotEpochs, need_table, owner, rank_entries
+        from paper_2511_20426_b200.kvpool import SlotAllocator
+        from paper_2511_20426_b200.denoiser import visible_block_lists
+        cfg = bc.wan_config("tiny", total_frames=39, workers=world)
+        st = bc.CascadeState(num_blocks=cfg.num_blocks, offset=cfg.offset, schedule=cfg.schedule())
+        pool = bc.KVPool.empty(cfg.window_blocks, cfg.sink_blocks)
+        n_slots = cfg.window_blocks + cfg.sink_blocks + cfg.cascade_width + 1
+        slots, epochs = SlotAllocator(n_slots), SlotEpochs(n_slots)
+        log = []
+        while not st.done:
+            plan = bc.plan_iteration(st)
+            epoch = plan.iteration + 1
+            for b in plan.blocks:
+                slots.acquire(b)
+            mask = bc.build_mask(plan.blocks, pool.block_indices, "bidirectional", cfg.block_size)
+            vis = visible_block_lists(mask)
+            local = rank_entries(plan.blocks, world, rank)
+            need = need_table([plan.blocks[i] for i in local], [vis[i] for i in local], plan.blocks,
+                              epochs, epoch, world, rank, slots.slot_of)
+            log.append({"local": [plan.blocks[i] for i in local], "need": need,
+                        "slots": [slots.slot_of(b) for b in plan.blocks],
+                        "vis": [vis[i] for i in local]})
+            epochs.wrote([slots.slot_of(b) for b in plan.blocks], epoch)
+            bc.advance(st, plan)
+            for e in plan.entries:
+                if e.pass_index == cfg.schedule().cache_pass:
+                    kv = (bc.LayerKV(e.block_index, 0, None, None, 0.0, "c"),)
+                    newer = pool.insert(e.block_index, kv)
+                    for gone in pool.evicted_by(newer):
+                        slots.release(gone)
+                    pool = newer
+        everyone = [None] * world
+        dist.all_gather_object(everyone, log)
+        if rank == 0:
+            q.put(everyone)
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_rank_host_agreement():
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    logs = q.get(timeout=120)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    a, b = logs
+    assert len(a) == len(b) == 17
+    for it, (ra, rb) in enumerate(zip(a, b)):
+        assert ra["slots"] == rb["slots"]                       # same slot table on every rank
+        assert sorted(ra["local"] + rb["local"]) == sorted(set(ra["local"] + rb["local"]))
+        assert all(x % 2 == 0 for x in ra["local"]) and all(x % 2 == 1 for x in rb["local"])
+        for r, log in ((0, ra), (1, rb)):
+            for blk_vis, row in zip(log["vis"], log["need"]):
+                for vb, need in zip(blk_vis, row):
+                    if vb % 2 == r:
+                        assert need == 0                          # own writes are stream-ordered
+                    else:
+                        assert 1 <= need <= it + 1               # a peer published it

@@ -1,0 +1,181 @@
+"""Host-side logic: config, scheduler, pool, masks, metrics, switches
+(reference tests test_config/test_core/test_scheduler/test_kvpool/
+test_metrics/test_interactive restated against this package)."""
+
+import math
+import random
+
+import numpy as np
+import pytest
+
+import paper_2511_20426_b200 as bc
+from oracle.schedule import enumerate_schedule, replay_pool
+
+
+def drive(num_blocks, offset, workers=1):
+    st = bc.CascadeState(num_blocks=num_blocks, offset=offset,
+                         schedule=bc.make_schedule([1000, 750, 500, 250]), workers=workers)
+    plans = []
+    while not st.done:
+        p = bc.plan_iteration(st)
+        plans.append(p)
+        bc.advance(st, p, p.blocks)
+    return st, plans
+
+
+def test_schedule_examples():
+    s = bc.make_schedule([1000, 750, 500, 250])
+    assert (s.passes, s.emit_pass, s.cache_pass) == (5, 3, 4)
+    assert s.table() == [1000, 750, 500, 250, 0.0]
+    for bad in ([], [1200], [1000, 0], [500, 500], [float("nan")], [500, 750]):
+        with pytest.raises(bc.InvalidInputError):
+            bc.make_schedule(bad)
+
+
+def test_steady_state_plan_and_counts():
+    _, plans = drive(13, 1)
+    assert [(e.block_index, e.noise_level) for e in plans[9].entries] == \
+        [(5, 0.0), (6, 250.0), (7, 500.0), (8, 750.0), (9, 1000.0)]
+    for o in range(1, 6):
+        for b in range(1, 25):
+            _, plans = drive(b, o)
+            assert len(plans) == (b - 1) * o + 5
+            assert [[(e.block_index, e.pass_index) for e in p.entries] for p in plans] == \
+                enumerate_schedule(b, 5, o)
+
+
+def test_phases_and_snapshot_resume():
+    st = bc.CascadeState(num_blocks=13, offset=1, schedule=bc.make_schedule([1000, 750, 500, 250]))
+    seen = []
+    for _ in range(9):
+        seen.append(st.phase)
+        p = bc.plan_iteration(st)
+        bc.advance(st, p)
+    assert seen[0] == "fill" and "steady" in seen
+    clone = bc.CascadeState.from_snapshot(st.to_snapshot())
+    while not st.done:
+        a, b = bc.plan_iteration(st), bc.plan_iteration(clone)
+        assert a == b
+        bc.advance(st, a)
+        bc.advance(clone, b)
+    assert clone.done and clone.phase == "done"
+    with pytest.raises(bc.ContractViolation):
+        bc.plan_iteration(st)
+
+
+def test_pool_eviction_against_replay_oracle():
+    rng = random.Random(7)
+    for _ in range(300):
+        window, sink = rng.randint(1, 6), rng.choice([0, 1])
+        inserts = [rng.randint(0, 15) for _ in range(rng.randint(0, 25))]
+        pool = bc.KVPool.empty(window, sink)
+        for b in inserts:
+            pool = pool.insert(b, (bc.LayerKV(b, 0, np.zeros((3, 1, 1)), np.zeros((3, 1, 1)), 0.0, "c"),))
+        assert pool.block_indices == replay_pool(inserts, window, sink)[0]
+
+
+def test_pool_evicted_by_and_mismatch():
+    kv = lambda b: (bc.LayerKV(b, 0, np.zeros((3, 1, 1)), np.zeros((3, 1, 1)), 0.0, "c"),)
+    pool = bc.KVPool.empty(2, 1)
+    for b in range(3):
+        pool = pool.insert(b, kv(b))
+    newer = pool.insert(3, kv(3))
+    assert pool.evicted_by(newer) == [1] and newer.block_indices == [0, 2, 3]
+    with pytest.raises(bc.ContractViolation):
+        pool.insert(2, kv(3))
+
+
+def test_slot_allocator_reuse():
+    from paper_2511_20426_b200.kvpool import SlotAllocator
+    a = SlotAllocator(3)
+    s0, s1 = a.acquire(10), a.acquire(11)
+    assert a.acquire(10) == s0 and s0 != s1
+    a.release(10)
+    assert a.acquire(12) == s0
+    a.acquire(13)
+    with pytest.raises(bc.ContractViolation):
+        a.acquire(14)
+
+
+def test_config_rules_and_wan_presets(tmp_path):
+    assert bc.CascadeConfig().validate().cascade_width == 5
+    with pytest.raises(bc.InvalidInputError):
+        bc.CascadeConfig(window_blocks=2, sink_blocks=1, offset=1).validate()
+    with pytest.raises(bc.InvalidInputError) as err:
+        bc.CascadeConfig(block_size=0, workers=-1).validate()
+    assert {"block_size", "workers"} <= set(err.value.fields)
+    c = bc.wan_config("1.3b")
+    assert (c.model_dim, c.tokens_per_block, c.latent_dim, c.num_blocks) == (1536, 4680, 99840, 13)
+    c14 = bc.wan_config("14b")
+    assert (c14.model_dim, c14.layers, c14.ffn_dim) == (5120, 40, 13824)
+    with pytest.raises(bc.InvalidInputError):
+        bc.with_fields(c, latent_dim=16)
+    path = tmp_path / "cfg.yaml"
+    bc.dump_config(c, path)
+    assert bc.load_config(path) == c
+    env = {"CASCADE_OFFSET": "2", "CASCADE_ATTENTION_MODE": "causal"}
+    assert bc.load_config(path, environ=env).offset == 2
+    with pytest.raises(bc.InvalidInputError):
+        bc.load_config(overrides={"nonsense": 1})
+
+
+def test_mask_lists_are_prefixes_in_engine_shapes():
+    from paper_2511_20426_b200.denoiser import visible_block_lists
+    m = bc.build_mask([5, 6, 7], [0, 2, 3, 4], "causal", 3)
+    assert visible_block_lists(m) == [[0, 2, 3, 4, 5], [0, 2, 3, 4, 5, 6], [0, 2, 3, 4, 5, 6, 7]]
+    m = bc.build_mask([5, 6], [4], "bidirectional", 3)
+    assert m.visible_frames(5) == 9
+
+
+def test_metrics_definitions():
+    tr = bc.Trace()
+    clock = 0.0
+    for i in range(13):
+        step = {7: 0.5, 8: 0.375}.get(i, 1.0)
+        frames = {7: 14}.get(i, 12)
+        clock += step
+        tr.append(bc.TraceEvent(iteration=i, entries=[], wall_seconds=step, modeled_exec=1.0,
+                                modeled_comm=0.0, modeled_stall=0.0, modeled_decode=0.0,
+                                modeled_clock=clock, wall_clock=clock, pool_blocks=0, pool_frames=0,
+                                pool_state=[], emitted_block=i, emitted_video_frames=frames))
+    assert bc.streaming_fps(tr) == 30.0
+    assert bc.streaming_fps(tr, clock="wall") == 30.0
+    assert math.isclose(bc.end_to_end_fps(tr), (12 * 12 + 14) / clock)
+    with pytest.raises(bc.ContractViolation):
+        tr.append(tr.events[0])
+
+
+def test_switch_spec_and_queue():
+    s = bc.SwitchSpec("x", "cascade", at_block=8)
+    assert s.boundary_iteration(1, 3) == 11
+    with pytest.raises(bc.InvalidInputError):
+        bc.SwitchSpec("x", "cascade")
+    q = bc.CommandQueue()
+    r = q.submit(bc.LiveSwitchRequest("p"))
+    assert q.pop() is r and q.pop() is None
+    q.submit(r)
+    q.reject_all(bc.InvalidInputError("done"))
+    with pytest.raises(bc.InvalidInputError):
+        r.wait(0.1)
+
+
+def test_engine_rejects_recache_paths(oracle_engine, default_config):
+    with pytest.raises(bc.InvalidInputError):
+        bc.run_cascade(default_config, "p", switches=[bc.SwitchSpec("q", "recache", at_block=2)])
+    with pytest.raises(bc.InvalidInputError):
+        bc.run_cascade(bc.with_fields(default_config, refresh_sink_on_switch=True), "p")
+
+
+def test_engine_properties_on_oracle(oracle_engine, default_config):
+    """Reference acceptance properties through the product engine (CPU oracle forward)."""
+    cfg = bc.with_fields(default_config, total_frames=18)
+    base = bc.run_cascade(cfg, "determinism")
+    multi = bc.run_cascade(bc.with_fields(cfg, workers=5), "determinism")
+    for k in base.outputs:
+        assert np.array_equal(base.outputs[k], multi.outputs[k])
+    seq = bc.run_sequential_reference(cfg, "p")
+    cas = bc.run_cascade(bc.with_fields(cfg, offset=5), "p")
+    for k in seq.outputs:
+        assert np.array_equal(seq.outputs[k], cas.outputs[k])
+    assert bc.attention_cost(bc.run_cascade(bc.with_fields(cfg, total_frames=3), "p").trace) == 45
+    bc.verify_schedule_consistency(base.trace, cfg)
