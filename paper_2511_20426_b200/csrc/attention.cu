@@ -26,6 +26,7 @@
 #include <cudaTypedefs.h>
 #include <math.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "attention.h"
 #include "bc_common.h"
@@ -59,6 +60,19 @@ __device__ __forceinline__ float ex2(float x) {
   return y;
 }
 
+// 2^x on the FMA pipe (Cody-Waite split + degree-3 minimax on [-0.5, 0.5],
+// max rel. error 7.7e-5 << bf16's 3.9e-3) to offload part of the MUFU work:
+// the softmax is MUFU-bound at 16 ex2/clk/SM otherwise.
+__device__ __forceinline__ float ex2_poly(float x) {
+  x = fmaxf(x, -126.0f);
+  const float t = x + 12582912.0f;  // 1.5 * 2^23: round-to-nearest integer in the low mantissa bits
+  const float n = t - 12582912.0f;
+  const float f = x - n;
+  const float p = fmaf(fmaf(fmaf(0.05508868380751114f, f, 0.24260405145947936f), f, 0.6932762416819607f), f,
+                       0.9999289403695112f);
+  return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
+}
+
 struct SoftmaxBars {
   uint64_t* s_full;
   uint64_t* s_empty;
@@ -67,6 +81,7 @@ struct SoftmaxBars {
 };
 
 // One softmax warpgroup: 128 threads, thread <-> query row of its tile.
+template <int kPolyEvery>
 __device__ __forceinline__ void softmax_tile(const AttnParams& prm, uint32_t tmem_s, uint32_t tmem_o,
                                              uint8_t* sp, SoftmaxBars b, int n_tiles, int tiles_per_slot,
                                              uint32_t quad, int q_row0, int e, int head) {
@@ -110,12 +125,29 @@ __device__ __forceinline__ void softmax_tile(const AttnParams& prm, uint32_t tme
     float tsum = 0.0f;
     const float neg_m = -m_used;
     uint32_t pk[64];
+    if (valid == kKeys) {
+      // full tile: every 4th pair of exponentials on the FMA pipe
 #pragma unroll
-    for (int t = 0; t < 64; ++t) {
-      const float p0 = ex2(fmaf(s[2 * t], c, neg_m));
-      const float p1 = ex2(fmaf(s[2 * t + 1], c, neg_m));
-      tsum += p0 + p1;
-      pk[t] = pack_bf16(p0, p1);
+      for (int t = 0; t < 64; ++t) {
+        float p0, p1;
+        if (kPolyEvery > 0 && (t % kPolyEvery) == kPolyEvery - 1) {
+          p0 = ex2_poly(fmaf(s[2 * t], c, neg_m));
+          p1 = ex2_poly(fmaf(s[2 * t + 1], c, neg_m));
+        } else {
+          p0 = ex2(fmaf(s[2 * t], c, neg_m));
+          p1 = ex2(fmaf(s[2 * t + 1], c, neg_m));
+        }
+        tsum += p0 + p1;
+        pk[t] = pack_bf16(p0, p1);
+      }
+    } else {
+#pragma unroll
+      for (int t = 0; t < 64; ++t) {
+        const float p0 = ex2(fmaf(s[2 * t], c, neg_m));
+        const float p1 = ex2(fmaf(s[2 * t + 1], c, neg_m));
+        tsum += p0 + p1;
+        pk[t] = pack_bf16(p0, p1);
+      }
     }
     // PV(j-1) must be complete before O is rescaled or P is overwritten
     if (j > 0) {
@@ -177,6 +209,7 @@ __device__ __forceinline__ void softmax_tile(const AttnParams& prm, uint32_t tme
   }
 }
 
+template <int kPolyEvery>
 __global__ void __launch_bounds__(kThreads, 1)
     attn_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_kv,
                 AttnParams prm) {
@@ -269,7 +302,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t sp[2] = {smem_u32(smem + Smem::pa), smem_u32(smem + Smem::pb)};
     const int n_q = has_b ? 2 : 1;
     auto ring_slot = [&](int i) { return smem_u32(smem + Smem::ring + (i % kRing) * kTile); };
-    auto ring_wait = [&](int i) { mbar_wait(&ring_full[i % kRing], (i / kRing) & 1); };
     auto issue_qk = [&](int x, int j) {  // S_x = Q_x K_j^T ; K_j is ring item 2j
       if (elect_one()) {
         const uint32_t sk = ring_slot(2 * j);
@@ -300,6 +332,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (elect_one()) mma_commit(&ring_empty[i % kRing]);
       __syncwarp();
     };
+    // Issue order per key tile j: S_A(j+1), O_A += P_A(j) V_j, S_B(j+1),
+    // O_B += P_B(j) V_j.  Issuing PV_A before QK_B lets softmax A (which waits
+    // for PV_A(j) before overwriting P_A) start tile j+1 earlier; measured
+    // faster than issuing both QKs first or an event-driven polling issuer.
+    auto ring_wait = [&](int i) { mbar_wait(&ring_full[i % kRing], (i / kRing) & 1); };
     mbar_wait(q_full, 0);
     if (n_tiles > 0) {
       ring_wait(0);
@@ -328,7 +365,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int x = (warp >= 8) ? 1 : 0;
     if (x == 0 || has_b) {
       SoftmaxBars b{&s_full[x], &s_empty[x], &p_full[x], &o_ready[x]};
-      softmax_tile(prm, tmem + x * 128, tmem + 256 + x * 128, smem + (x ? Smem::pb : Smem::pa), b, n_tiles,
+      softmax_tile<kPolyEvery>(prm, tmem + x * 128, tmem + 256 + x * 128, smem + (x ? Smem::pb : Smem::pa), b, n_tiles,
                    tiles_per_slot, warp & 3, q0 + x * kRows, e, head);
     }
   }
@@ -403,13 +440,20 @@ int attention_run(const AttnArgs& a, cudaStream_t st) {
   }
   p.flags = a.flags;
   p.flag_base = a.flag_base;
-  static bool attr = false;
-  if (!attr) {
-    BC_CUDA(cudaFuncSetAttribute(attn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, Smem::total + 1024));
-    attr = true;
+  static int poly = -1;
+  if (poly < 0) {
+    const char* env = getenv("BC_ATTN_POLY");  // tuning knob: 0 = all MUFU
+    poly = env ? atoi(env) : 0;
+    BC_CUDA(cudaFuncSetAttribute(attn_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, Smem::total + 1024));
+    BC_CUDA(cudaFuncSetAttribute(attn_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, Smem::total + 1024));
+    BC_CUDA(cudaFuncSetAttribute(attn_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, Smem::total + 1024));
+    BC_CUDA(cudaFuncSetAttribute(attn_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, Smem::total + 1024));
   }
   dim3 grid((a.q_tokens + 2 * kRows - 1) / (2 * kRows), a.n_entries, a.heads);
-  attn_kernel<<<grid, kThreads, Smem::total + 1024, st>>>(mq, mkv, p);
+  if (poly == 0) attn_kernel<0><<<grid, kThreads, Smem::total + 1024, st>>>(mq, mkv, p);
+  else if (poly == 3) attn_kernel<3><<<grid, kThreads, Smem::total + 1024, st>>>(mq, mkv, p);
+  else if (poly == 8) attn_kernel<8><<<grid, kThreads, Smem::total + 1024, st>>>(mq, mkv, p);
+  else attn_kernel<4><<<grid, kThreads, Smem::total + 1024, st>>>(mq, mkv, p);
   BC_LAUNCHED();
   return BC_OK;
 }
