@@ -213,8 +213,13 @@ def run_ours(args, cfg):
             import torch.distributed as dist
             dist.barrier()
 
+    switches = [bc.SwitchSpec(f"{PROMPT}, scene {k}", "cascade", at_block=k)
+                for k in range(args.switch_every, cfg.num_blocks, args.switch_every)] \
+        if args.switch_every else []
+
     def one_run(c=cfg, noise=feed):
-        return bc.run_cascade(c, PROMPT, session_seed=SESSION_SEED, weights=weights, noise_feed=noise)
+        return bc.run_cascade(c, PROMPT, session_seed=SESSION_SEED, weights=weights, noise_feed=noise,
+                              switches=switches)
 
     for _ in range(args.warmup):
         one_run()
@@ -246,18 +251,19 @@ def run_ours(args, cfg):
     stream_fps = statistics.mean(streaming_fps(r.trace, clock="wall") for r in runs)
 
     # ---- sequential block-causal rollout, same weights / inputs ----
-    seq = bc.run_sequential_reference(seq_cfg, PROMPT, session_seed=SESSION_SEED, weights=weights,
-                                      noise_feed=feed)
-    seq = bc.run_sequential_reference(seq_cfg, PROMPT, session_seed=SESSION_SEED, weights=weights,
-                                      noise_feed=feed)
-    seq_e2e = end_to_end_fps(seq.trace)
-    seq_stream = streaming_fps(seq.trace, clock="wall")
+    seq_e2e = seq_stream = None
+    if not args.no_seq:
+        for _ in range(2):
+            seq = bc.run_sequential_reference(seq_cfg, PROMPT, session_seed=SESSION_SEED,
+                                              weights=weights, noise_feed=feed)
+        seq_e2e = end_to_end_fps(seq.trace)
+        seq_stream = streaming_fps(seq.trace, clock="wall")
 
     # ---- e2e through the public API with host buffers (noise H2D, outputs D2H) ----
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    e2e_runs = [bc.run_cascade(cfg, PROMPT, session_seed=SESSION_SEED, weights=weights)
-                for _ in range(args.steps)]
+    e2e_runs = [bc.run_cascade(cfg, PROMPT, session_seed=SESSION_SEED, weights=weights,
+                               switches=switches) for _ in range(args.steps)]
     torch.cuda.synchronize()
     e2e_s = time.perf_counter() - t0
     if world > 1:
@@ -296,20 +302,23 @@ def run_ours(args, cfg):
         cpu = {"value": cpu_fps_from_sample(cfg, samp), "unit": "frames/s", "cores": os.cpu_count(),
                "kind": "port", "sample": cpu_sample_desc(cfg), "sample_seconds": samp}
     line = {
-        "metric": "generated frames/sec (cascaded, Wan2.1-1.3B-shaped, 480x832)",
+        "metric": f"generated frames/sec (cascaded, Wan2.1-{args.preset.upper()}-shaped, 480x832)",
         "value": value, "unit": "frames/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic (random-init Wan2.1-1.3B-shaped weights, counter-keyed N(0,1) noise, "
                 "hash-expanded 512x4096 text states)",
-        "config": {"workload": "wan2.1-1.3b cascade o=1, 13 blocks (156 frames), 480x832, 4-step, "
-                               "3 latent frames/block, bidirectional, W=7 sink=1",
-                   "model": "wan2.1-1.3b-shaped", "global_batch": 1,
+        "config": {"workload": f"wan2.1-{args.preset} cascade o=1, {cfg.num_blocks} blocks "
+                               f"({cfg.num_blocks * FRAMES_PER_BLOCK} frames), 480x832, 4-step, "
+                               f"3 latent frames/block, bidirectional, W=7 sink={args.sink}"
+                               + (f", cascade prompt switch every {args.switch_every} blocks"
+                                  if args.switch_every else ""),
+                   "model": f"wan2.1-{args.preset}-shaped", "global_batch": 1,
                    "seq_len": cfg.tokens_per_block, "parallelism": f"temporal{world}",
                    "l2": "working set (2.6 GB weights + 11 GB KV arena) >> 126 MB L2; no flush"},
         "streaming_fps": stream_fps,
         "sequential": {"e2e_fps": seq_e2e, "streaming_fps": seq_stream},
-        "cascade_over_sequential_streaming": stream_fps / seq_stream,
+        "cascade_over_sequential_streaming": stream_fps / seq_stream if seq_stream else None,
         "roofline": {"bound": "tensor", "kernel": dom, "achieved": achieved, "peak": peak,
                      "unit": "TFLOP/s", "frac": achieved / peak if achieved else None,
                      "traffic": traffic, "peak_kind": f"{peak_kind} bf16 sustained",
@@ -333,10 +342,14 @@ def main():
     ap.add_argument("--preset", default="1.3b")
     ap.add_argument("--blocks", type=int, default=13)
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline sample")
+    ap.add_argument("--sink", type=int, default=1, help="sink blocks (LongLive-style: 0)")
+    ap.add_argument("--switch-every", type=int, default=0,
+                    help="cascade-mode prompt switch every N blocks (LongLive-style config 5)")
+    ap.add_argument("--no-seq", action="store_true", help="skip the sequential rollout")
     args = ap.parse_args()
     from paper_2511_20426_b200 import wan_config
     cfg = wan_config(args.preset, total_frames=3 * args.blocks, offset=1,
-                     attention_mode="bidirectional", window_blocks=7, sink_blocks=1)
+                     attention_mode="bidirectional", window_blocks=7, sink_blocks=args.sink)
     if args.impl == "reference":
         run_reference(args, cfg)
     else:
