@@ -28,9 +28,11 @@ namespace {
 
 constexpr int BM = 128;
 constexpr int BK = 64;  // 64 bf16 = 128 B = one swizzle atom row
-constexpr int kThreads = 192;
-constexpr int kStagePitch = 36;  // floats per staged row (32 + 4 pad, 16 B aligned)
-constexpr int kEpiStageBytes = 4 * 32 * kStagePitch * 4;
+constexpr int kEpiWarps = 8;      // 2 per TMEM lane quadrant (column halves)
+constexpr int kThreads = 64 + 32 * kEpiWarps;
+constexpr int kChunk = 16;        // columns per TMEM load / staging round
+constexpr int kStagePitch = 20;   // floats per staged row (16 + 4 pad, 16 B aligned)
+constexpr int kEpiStageBytes = kEpiWarps * 32 * kStagePitch * 4;
 
 template <int BN>
 struct GemmCfg {
@@ -95,7 +97,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
-      mbar_init(&tempty[i], 128);
+      mbar_init(&tempty[i], 32 * kEpiWarps);
     }
     fence_barrier_init();
   }
@@ -159,14 +161,18 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else {
-    // epilogue: warp w covers TMEM lanes 32*(w%4) .. +31 (rows of the tile).
-    // Each 32x32 chunk goes TMEM -> registers (row per lane, + bias / GELU)
-    // -> a padded per-warp smem stage -> coalesced global access, 4 rows x
-    // 32 columns per warp instruction (full 128 B lines for fp32).
+    // epilogue: 8 warps; warp w covers TMEM lanes 32*(w%4)..+31 (tile rows)
+    // and one column half.  Each 32x16 chunk goes TMEM -> registers (row per
+    // lane, + bias / GELU) -> a padded per-warp smem stage -> coalesced
+    // global access (8 rows x 64 B per warp instruction).  For the residual
+    // mode all of a chunk's C / gate loads are issued before any use, so the
+    // read-modify-write runs at memory-level parallelism, not latency.
+    const int ew = (int)warp - 2;
     const uint32_t quad = warp & 3;
-    float* stage = epi_stage + (warp - 2) * (32 * kStagePitch);
-    const int sub_row = lane_id() >> 3;          // 0..3
-    const int sub_col = (lane_id() & 7) * 4;     // 0..28
+    const int c_begin = (ew >> 2) * (BN / 2);
+    float* stage = epi_stage + ew * (32 * kStagePitch);
+    const int sub_row = lane_id() >> 2;        // 0..7
+    const int sub_col = (lane_id() & 3) * 4;   // 0..12
     int it = 0;
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
       const int acc = it & 1;
@@ -178,15 +184,15 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_after();
       const int row_base = m0 + (int)quad * 32;
 #pragma unroll 1
-      for (int c = 0; c < BN; c += 32) {
-        uint32_t r[32];
+      for (int c = c_begin; c < c_begin + BN / 2; c += kChunk) {
+        uint32_t r[16];
         __syncwarp();
-        tmem_ld32(tmem_base + ((quad * 32) << 16) + acc * BN + c, r);
+        tmem_ld16(tmem_base + ((quad * 32) << 16) + acc * BN + c, r);
         tmem_ld_wait();
         const int col = n0 + c;
         float* srow = stage + lane_id() * kStagePitch;
 #pragma unroll
-        for (int j = 0; j < 32; j += 4) {
+        for (int j = 0; j < kChunk; j += 4) {
           float4 v;
           v.x = __uint_as_float(r[j]) + (bias ? __ldg(bias + col + j) : 0.0f);
           v.y = __uint_as_float(r[j + 1]) + (bias ? __ldg(bias + col + j + 1) : 0.0f);
@@ -201,29 +207,49 @@ __global__ void __launch_bounds__(kThreads, 1)
           *reinterpret_cast<float4*>(srow + j) = v;
         }
         __syncwarp();
+        if (MODE == kEpiResidualF32) {
+          float4 res[4], g[4];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const int lr = i * 4 + sub_row;
-          const int row = row_base + lr;
-          const float4 v = *reinterpret_cast<const float4*>(stage + lr * kStagePitch + sub_col);
-          if (row < M) {
-            if (MODE == kEpiStoreBf16 || MODE == kEpiGeluBf16) {
-              uint2 pk;
-              pk.x = pack_bf16(v.x, v.y);
-              pk.y = pack_bf16(v.z, v.w);
-              *reinterpret_cast<uint2*>(static_cast<__nv_bfloat16*>(c_ptr) + (size_t)row * N + col + sub_col) = pk;
-            } else if (MODE == kEpiStoreF32) {
-              *reinterpret_cast<float4*>(static_cast<float*>(c_ptr) + (size_t)row * N + col + sub_col) = v;
-            } else {  // kEpiResidualF32: C += gate * v
-              float4* dst = reinterpret_cast<float4*>(static_cast<float*>(c_ptr) + (size_t)row * N + col + sub_col);
-              float4 g = make_float4(1.f, 1.f, 1.f, 1.f);
-              if (gate) g = __ldg(reinterpret_cast<const float4*>(gate + (size_t)(row / rows_per_gate) * gate_stride + col + sub_col));
-              float4 o = *dst;
-              o.x += g.x * v.x;
-              o.y += g.y * v.y;
-              o.z += g.z * v.z;
-              o.w += g.w * v.w;
-              *dst = o;
+          for (int i = 0; i < 4; ++i) {
+            const int row = row_base + i * 8 + sub_row;
+            res[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+            g[i] = make_float4(1.f, 1.f, 1.f, 1.f);
+            if (row < M) {
+              res[i] = *reinterpret_cast<const float4*>(static_cast<float*>(c_ptr) + (size_t)row * N + col + sub_col);
+              if (gate)
+                g[i] = __ldg(reinterpret_cast<const float4*>(gate + (size_t)(row / rows_per_gate) * gate_stride +
+                                                             col + sub_col));
+            }
+          }
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const int lr = i * 8 + sub_row;
+            const int row = row_base + lr;
+            const float4 v = *reinterpret_cast<const float4*>(stage + lr * kStagePitch + sub_col);
+            if (row < M) {
+              float4 o = res[i];
+              o.x += g[i].x * v.x;
+              o.y += g[i].y * v.y;
+              o.z += g[i].z * v.z;
+              o.w += g[i].w * v.w;
+              *reinterpret_cast<float4*>(static_cast<float*>(c_ptr) + (size_t)row * N + col + sub_col) = o;
+            }
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const int lr = i * 8 + sub_row;
+            const int row = row_base + lr;
+            const float4 v = *reinterpret_cast<const float4*>(stage + lr * kStagePitch + sub_col);
+            if (row < M) {
+              if (MODE == kEpiStoreF32) {
+                *reinterpret_cast<float4*>(static_cast<float*>(c_ptr) + (size_t)row * N + col + sub_col) = v;
+              } else {
+                uint2 pk;
+                pk.x = pack_bf16(v.x, v.y);
+                pk.y = pack_bf16(v.z, v.w);
+                *reinterpret_cast<uint2*>(static_cast<__nv_bfloat16*>(c_ptr) + (size_t)row * N + col + sub_col) = pk;
+              }
             }
           }
         }

@@ -179,6 +179,8 @@ class _Ctx:
             raise err
 
     def read_kv(self, slot, layer, which):
+        if self.arena is None:
+            raise ContractViolation("KV of a closed session is no longer resident")
         arr = self.arena[layer, slot, which].float().cpu().numpy()
         return arr.reshape(self.T, self.cfg.heads, self.cfg.head_dim)
 
@@ -190,9 +192,14 @@ class _Ctx:
         return self.read_kv(slot, layer, which)
 
     def close(self):
+        """Destroy the C context and drop the device buffers (results that
+        still reference this context, e.g. a RunResult's pool handles, no
+        longer pin ~11-54 GB of KV arena)."""
         if self.handle:
             N.lib().bc_wan_destroy(self.handle)
             self.handle = None
+        self.arena = None
+        self.workspace = None
 
     def __del__(self):  # pragma: no cover
         try:
@@ -436,6 +443,12 @@ class WanSession:
     def emitted_device(self, block):
         return self.final[block]
 
+    def release_device(self):
+        self.torch.cuda.current_stream().synchronize()
+        self.ctx.close()
+        self.latents.clear()
+        self.final.clear()
+
     def fill_wall_times(self, events):
         if not events:
             return
@@ -448,4 +461,4 @@ class WanSession:
             ev.wall_clock = first.elapsed_time(t1) / 1e3
 
     def close(self):
-        pass
+        self.release_device()

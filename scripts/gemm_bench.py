@@ -21,3 +21,6 @@ def run(M, Nn, K, mode, bn=0, iters=20):
 for (M,Nn,K) in [(4680,4608,1536),(4680,1536,1536),(4680,8960,1536),(4680,1536,8960),(23400,4608,1536),(23400,8960,1536),(23400,1536,8960),(8192,8192,8192)]:
     for bn in (128, 256):
         run(M,Nn,K,0,bn)
+for (M,Nn,K) in [(23400,1536,1536),(23400,1536,8960),(4680,1536,1536)]:
+    for bn in (128, 256):
+        run(M,Nn,K,3,bn)
