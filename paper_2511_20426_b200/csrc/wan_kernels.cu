@@ -45,6 +45,23 @@ __device__ __forceinline__ void wait_peers_done(const PeerArgs& pa) {
   }
   __syncthreads();
 }
+// Sum over the WPR warps that cooperate on one row (fixed order).
+template <int WPR>
+__device__ __forceinline__ float row_reduce(float v, float* red, int slot, int wir) {
+  v = warp_sum(v);
+  if constexpr (WPR == 1) {
+    return v;
+  } else {
+    if ((threadIdx.x & 31) == 0) red[slot * WPR + wir] = v;
+    __syncthreads();
+    float t = 0.f;
+#pragma unroll
+    for (int w = 0; w < WPR; ++w) t += red[slot * WPR + w];
+    __syncthreads();
+    return t;
+  }
+}
+
 // after all CTAs' stores: the last CTA to finish runs `fn` (publication)
 template <class F>
 __device__ __forceinline__ void last_cta_publish(uint32_t* ctr, F&& fn) {
@@ -130,32 +147,36 @@ __global__ void timestep_sin_kernel(TimeArgs a, float* out, int freq_dim) {
 // ------------------------------------------------------------ LayerNorm rows
 // mode 0: LN(x) * (1 + mod[1]) + mod[0]   with mod = base[6][d] + e0[e][6][d] (chunks sel0/sel1)
 // mode 1: LN(x) * w + b                   (affine LN, cross-attn norm3)
-template <int VPL>  // float4 vectors per lane
+template <int VPL, int WPR>  // float4 vectors per lane, warps per row
 __global__ void ln_rows_kernel(const float* __restrict__ X, __nv_bfloat16* __restrict__ out, int rows,
                                int d, int rows_per_entry, LnArgs a) {
-  const int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (row >= rows) return;
-  const float4* x4 = reinterpret_cast<const float4*>(X + (size_t)row * d);
+  __shared__ float red[8];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int slot = warp / WPR, wir = warp % WPR;
+  const int row = blockIdx.x * (8 / WPR) + slot;
+  const int li = wir * 32 + lane;
+  const bool active = row < rows;
+  const float4* x4 = reinterpret_cast<const float4*>(X + (size_t)(active ? row : 0) * d);
   float4 v[VPL];
   float s = 0.0f;
 #pragma unroll
   for (int i = 0; i < VPL; ++i) {
-    const int idx = lane + 32 * i;
-    v[i] = (idx * 4 < d) ? x4[idx] : make_float4(0.f, 0.f, 0.f, 0.f);
+    const int idx = li + 32 * WPR * i;
+    v[i] = (active && idx * 4 < d) ? x4[idx] : make_float4(0.f, 0.f, 0.f, 0.f);
     s += v[i].x + v[i].y + v[i].z + v[i].w;
   }
-  const float mean = warp_sum(s) / d;
+  const float mean = row_reduce<WPR>(s, red, slot, wir) / d;
   float q = 0.0f;
 #pragma unroll
   for (int i = 0; i < VPL; ++i) {
-    const int idx = lane + 32 * i;
+    const int idx = li + 32 * WPR * i;
     if (idx * 4 < d) {
       const float a0 = v[i].x - mean, a1 = v[i].y - mean, a2 = v[i].z - mean, a3 = v[i].w - mean;
       q += a0 * a0 + a1 * a1 + a2 * a2 + a3 * a3;
     }
   }
-  const float rstd = rsqrtf(warp_sum(q) / d + kEps);
+  const float rstd = rsqrtf(row_reduce<WPR>(q, red, slot, wir) / d + kEps);
+  if (!active) return;
   const int e = row / rows_per_entry;
   const float* p_scale = a.base_scale;
   const float* p_shift = a.base_shift;
@@ -164,7 +185,7 @@ __global__ void ln_rows_kernel(const float* __restrict__ X, __nv_bfloat16* __res
   uint2* o2 = reinterpret_cast<uint2*>(out + (size_t)row * d);
 #pragma unroll
   for (int i = 0; i < VPL; ++i) {
-    const int idx = lane + 32 * i;
+    const int idx = li + 32 * WPR * i;
     if (idx * 4 >= d) continue;
     const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
     const float4 sc = p_scale ? reinterpret_cast<const float4*>(p_scale)[idx] : z4;
@@ -193,29 +214,48 @@ __global__ void ln_rows_kernel(const float* __restrict__ X, __nv_bfloat16* __res
 // row's entry (token t = row % T).  RMSNorm over the full d with weight,
 // eps 1e-6; RoPE on complex pairs (2i, 2i+1) of each 128-wide head, pair i
 // < 22 rotates with the global frame index, < 43 with the patch row, else
-// the patch column (Wan 44/42/42 split of head_dim 128).
-__device__ __forceinline__ float rope_angle(int i, int f, int h, int w) {
-  // inv_freq = 10000^(-2k/D_part), D_part = 44 / 42 / 42
-  if (i < 22) return (float)f * exp2f(-(2.0f * i / 44.0f) * 13.287712379549449f);
-  if (i < 43) return (float)h * exp2f(-(2.0f * (i - 22) / 42.0f) * 13.287712379549449f);
-  return (float)w * exp2f(-(2.0f * (i - 43) / 42.0f) * 13.287712379549449f);
+// the patch column (Wan 44/42/42 split of head_dim 128).  cos/sin come from
+// tables precomputed in double precision (rope_table_kernel).
+__global__ void rope_table_kernel(float2* tf, int max_frames, float2* th, int hp, float2* tw, int wp) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int nf = max_frames * 22, nh = hp * 21, nw = wp * 21;
+  double ang;
+  if (i < nf) {
+    ang = (double)(i / 22) * pow(10000.0, -2.0 * (i % 22) / 44.0);
+    tf[i] = make_float2((float)cos(ang), (float)sin(ang));
+  } else if (i < nf + nh) {
+    const int k = i - nf;
+    ang = (double)(k / 21) * pow(10000.0, -2.0 * (k % 21) / 42.0);
+    th[k] = make_float2((float)cos(ang), (float)sin(ang));
+  } else if (i < nf + nh + nw) {
+    const int k = i - nf - nh;
+    ang = (double)(k / 21) * pow(10000.0, -2.0 * (k % 21) / 42.0);
+    tw[k] = make_float2((float)cos(ang), (float)sin(ang));
+  }
 }
 
-template <int VPL>  // bf16x8 (16 B) vectors per lane for d
+template <int VPL, int WPR>  // bf16x8 (16 B) vectors per lane, warps per row
 __global__ void qk_norm_rope_kernel(const __nv_bfloat16* __restrict__ qkv, int rows, int d, int T,
                                     QkArgs a) {
-  const int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
+  __shared__ float red[8];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int slot = warp / WPR, wir = warp % WPR;
+  const int row = blockIdx.x * (8 / WPR) + slot;
+  const int li = wir * 32 + lane;
+  const bool active = row < rows;
   wait_peers_done(a.peer);
-  if (row < rows) {
-  const int e = row / T, t = row % T;
+  const int rr = active ? row : 0;
+  const int e = rr / T, t = rr % T;
   const int hw = a.hp * a.wp;
   const int fl = t / hw, rem = t % hw;
   const int f = a.frame0[e] + fl, ph = rem / a.wp, pw = rem % a.wp;
+  const float2* rf = a.rope_f + (size_t)f * 22;
+  const float2* rh = a.rope_h + (size_t)ph * 21;
+  const float2* rw = a.rope_w + (size_t)pw * 21;
   const size_t mat = (size_t)T * d;
   __nv_bfloat16* kdst = a.arena + ((size_t)a.mat_base + (size_t)a.slot[e] * 2) * mat + (size_t)t * d;
   __nv_bfloat16* vdst = kdst + mat;
-  const __nv_bfloat16* src = qkv + (size_t)row * 3 * d;
+  const __nv_bfloat16* src = qkv + (size_t)rr * 3 * d;
 #pragma unroll
   for (int which = 0; which < 2; ++which) {
     const uint4* s4 = reinterpret_cast<const uint4*>(src + which * d);
@@ -223,8 +263,8 @@ __global__ void qk_norm_rope_kernel(const __nv_bfloat16* __restrict__ qkv, int r
     float ss = 0.0f;
 #pragma unroll
     for (int i = 0; i < VPL; ++i) {
-      const int idx = lane + 32 * i;
-      if (idx * 8 < d) {
+      const int idx = li + 32 * WPR * i;
+      if (active && idx * 8 < d) {
         uint4 u = s4[idx];
         const __nv_bfloat16* h = reinterpret_cast<const __nv_bfloat16*>(&u);
 #pragma unroll
@@ -234,12 +274,13 @@ __global__ void qk_norm_rope_kernel(const __nv_bfloat16* __restrict__ qkv, int r
         }
       }
     }
-    const float inv = rsqrtf(warp_sum(ss) / d + kEps);
+    const float inv = rsqrtf(row_reduce<WPR>(ss, red, slot, wir) / d + kEps);
+    if (!active) continue;
     const float* wgt = which == 0 ? a.norm_q : a.norm_k;
     __nv_bfloat16* dst = which == 0 ? a.qout + (size_t)row * d : kdst;
 #pragma unroll
     for (int i = 0; i < VPL; ++i) {
-      const int idx = lane + 32 * i;
+      const int idx = li + 32 * WPR * i;
       if (idx * 8 >= d) continue;
       const int c0 = idx * 8;                 // element index in [0, d)
       const int pair0 = (c0 & 127) >> 1;      // pair index inside the head
@@ -249,10 +290,10 @@ __global__ void qk_norm_rope_kernel(const __nv_bfloat16* __restrict__ qkv, int r
       for (int j = 0; j < 8; j += 2) {
         const float x0 = vals[i][j] * inv * wgt[c0 + j];
         const float x1 = vals[i][j + 1] * inv * wgt[c0 + j + 1];
-        float sn, cs;
-        sincosf(rope_angle(pair0 + j / 2, f, ph, pw), &sn, &cs);
-        o[j] = __float2bfloat16(x0 * cs - x1 * sn);
-        o[j + 1] = __float2bfloat16(x0 * sn + x1 * cs);
+        const int pi = pair0 + j / 2;
+        const float2 cs = pi < 22 ? rf[pi] : (pi < 43 ? rh[pi - 22] : rw[pi - 43]);
+        o[j] = __float2bfloat16(x0 * cs.x - x1 * cs.y);
+        o[j + 1] = __float2bfloat16(x0 * cs.y + x1 * cs.x);
       }
       reinterpret_cast<uint4*>(dst)[idx] = u;
       if (which == 1) {  // fresh K -> every peer's replica (NVLink P2P store)
@@ -261,13 +302,14 @@ __global__ void qk_norm_rope_kernel(const __nv_bfloat16* __restrict__ qkv, int r
       }
     }
   }
-  // v: plain copy into the slot (and the peers' replicas)
-  const uint4* v4 = reinterpret_cast<const uint4*>(src + 2 * d);
-  for (int idx = lane; idx * 8 < d; idx += 32) {
-    const uint4 u = v4[idx];
-    reinterpret_cast<uint4*>(vdst)[idx] = u;
-    for (int p = 0; p < a.peer.n_peers; ++p) reinterpret_cast<uint4*>(a.peer.arena[p] + (vdst - a.arena))[idx] = u;
-  }
+  if (active) {
+    // v: plain copy into the slot (and the peers' replicas)
+    const uint4* v4 = reinterpret_cast<const uint4*>(src + 2 * d);
+    for (int idx = li; idx * 8 < d; idx += 32 * WPR) {
+      const uint4 u = v4[idx];
+      reinterpret_cast<uint4*>(vdst)[idx] = u;
+      for (int p = 0; p < a.peer.n_peers; ++p) reinterpret_cast<uint4*>(a.peer.arena[p] + (vdst - a.arena))[idx] = u;
+    }
   }
   if (a.peer.n_peers > 0) {
     last_cta_publish(a.peer.ctr, [&] {
@@ -278,20 +320,23 @@ __global__ void qk_norm_rope_kernel(const __nv_bfloat16* __restrict__ qkv, int r
   }
 }
 
-// in-place RMSNorm * weight over rows of width d (bf16), row stride ld
-template <int VPL>
+// RMSNorm * weight over rows of width d (bf16), row stride ld
+template <int VPL, int WPR>
 __global__ void rms_rows_kernel(__nv_bfloat16* x, int rows, int d, int ld, const float* w,
                                 __nv_bfloat16* out, int ld_out) {
-  const int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (row >= rows) return;
-  const uint4* s4 = reinterpret_cast<const uint4*>(x + (size_t)row * ld);
+  __shared__ float red[8];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int slot = warp / WPR, wir = warp % WPR;
+  const int row = blockIdx.x * (8 / WPR) + slot;
+  const int li = wir * 32 + lane;
+  const bool active = row < rows;
+  const uint4* s4 = reinterpret_cast<const uint4*>(x + (size_t)(active ? row : 0) * ld);
   float vals[VPL][8];
   float ss = 0.0f;
 #pragma unroll
   for (int i = 0; i < VPL; ++i) {
-    const int idx = lane + 32 * i;
-    if (idx * 8 < d) {
+    const int idx = li + 32 * WPR * i;
+    if (active && idx * 8 < d) {
       uint4 u = s4[idx];
       const __nv_bfloat16* h = reinterpret_cast<const __nv_bfloat16*>(&u);
 #pragma unroll
@@ -301,11 +346,12 @@ __global__ void rms_rows_kernel(__nv_bfloat16* x, int rows, int d, int ld, const
       }
     }
   }
-  const float inv = rsqrtf(warp_sum(ss) / d + kEps);
+  const float inv = rsqrtf(row_reduce<WPR>(ss, red, slot, wir) / d + kEps);
+  if (!active) return;
   uint4* d4 = reinterpret_cast<uint4*>(out + (size_t)row * ld_out);
 #pragma unroll
   for (int i = 0; i < VPL; ++i) {
-    const int idx = lane + 32 * i;
+    const int idx = li + 32 * WPR * i;
     if (idx * 8 >= d) continue;
     uint4 u;
     __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(&u);
@@ -423,37 +469,45 @@ int launch_timestep_sin(const TimeArgs& a, int n, float* out, int freq_dim, cuda
   return BC_OK;
 }
 
+// rows of <= 12 float4 per lane run warp-per-row; wider rows (14B: d=5120)
+// spread over 4 warps so registers stay ~80/thread and occupancy high.
 int launch_ln_rows(const float* X, __nv_bfloat16* out, int rows, int d, int rows_per_entry, const LnArgs& a,
                    cudaStream_t st) {
-  const int threads = 256, rows_per_cta = threads / 32;
-  const int grid = (rows + rows_per_cta - 1) / rows_per_cta;
-  const int vpl = (d / 4 + 31) / 32;
-  if (vpl <= 12) ln_rows_kernel<12><<<grid, threads, 0, st>>>(X, out, rows, d, rows_per_entry, a);
-  else if (vpl <= 40) ln_rows_kernel<40><<<grid, threads, 0, st>>>(X, out, rows, d, rows_per_entry, a);
-  else return bc_fail(BC_ERR_CONTRACT, "ln_rows: d=%d too wide", d);
+  const int v4 = d / 4;
+  if (v4 <= 32 * 12) {
+    ln_rows_kernel<12, 1><<<(rows + 7) / 8, 256, 0, st>>>(X, out, rows, d, rows_per_entry, a);
+  } else if (v4 <= 4 * 32 * 12) {
+    ln_rows_kernel<12, 4><<<(rows + 1) / 2, 256, 0, st>>>(X, out, rows, d, rows_per_entry, a);
+  } else {
+    return bc_fail(BC_ERR_CONTRACT, "ln_rows: d=%d too wide", d);
+  }
   BC_LAUNCHED();
   return BC_OK;
 }
 
 int launch_qk_norm_rope(const __nv_bfloat16* qkv, int rows, int d, int T, const QkArgs& a, cudaStream_t st) {
-  const int threads = 256, rows_per_cta = threads / 32;
-  const int grid = (rows + rows_per_cta - 1) / rows_per_cta;
-  const int vpl = (d / 8 + 31) / 32;
-  if (vpl <= 6) qk_norm_rope_kernel<6><<<grid, threads, 0, st>>>(qkv, rows, d, T, a);
-  else if (vpl <= 20) qk_norm_rope_kernel<20><<<grid, threads, 0, st>>>(qkv, rows, d, T, a);
-  else return bc_fail(BC_ERR_CONTRACT, "qk_norm_rope: d=%d too wide", d);
+  const int v8 = d / 8;
+  if (v8 <= 32 * 6) {
+    qk_norm_rope_kernel<6, 1><<<(rows + 7) / 8, 256, 0, st>>>(qkv, rows, d, T, a);
+  } else if (v8 <= 4 * 32 * 6) {
+    qk_norm_rope_kernel<6, 4><<<(rows + 1) / 2, 256, 0, st>>>(qkv, rows, d, T, a);
+  } else {
+    return bc_fail(BC_ERR_CONTRACT, "qk_norm_rope: d=%d too wide", d);
+  }
   BC_LAUNCHED();
   return BC_OK;
 }
 
 int launch_rms_rows(__nv_bfloat16* x, int rows, int d, int ld, const float* w, __nv_bfloat16* out, int ld_out,
                     cudaStream_t st) {
-  const int threads = 256, rows_per_cta = threads / 32;
-  const int grid = (rows + rows_per_cta - 1) / rows_per_cta;
-  const int vpl = (d / 8 + 31) / 32;
-  if (vpl <= 6) rms_rows_kernel<6><<<grid, threads, 0, st>>>(x, rows, d, ld, w, out, ld_out);
-  else if (vpl <= 20) rms_rows_kernel<20><<<grid, threads, 0, st>>>(x, rows, d, ld, w, out, ld_out);
-  else return bc_fail(BC_ERR_CONTRACT, "rms_rows: d=%d too wide", d);
+  const int v8 = d / 8;
+  if (v8 <= 32 * 6) {
+    rms_rows_kernel<6, 1><<<(rows + 7) / 8, 256, 0, st>>>(x, rows, d, ld, w, out, ld_out);
+  } else if (v8 <= 4 * 32 * 6) {
+    rms_rows_kernel<6, 4><<<(rows + 1) / 2, 256, 0, st>>>(x, rows, d, ld, w, out, ld_out);
+  } else {
+    return bc_fail(BC_ERR_CONTRACT, "rms_rows: d=%d too wide", d);
+  }
   BC_LAUNCHED();
   return BC_OK;
 }
@@ -475,6 +529,13 @@ int launch_head_update(const float* Y, int n, int T, int F, int H, int W, const 
                        cudaStream_t st) {
   const int n_el = F * 16 * H * W;
   head_update_kernel<<<dim3(grid_for(n_el, 256) / n + 1, n), 256, 0, st>>>(Y, T, F, H, W, u, status);
+  BC_LAUNCHED();
+  return BC_OK;
+}
+
+int launch_rope_tables(float2* tf, int max_frames, float2* th, int hp, float2* tw, int wp, cudaStream_t st) {
+  const int n = max_frames * 22 + (hp + wp) * 21;
+  rope_table_kernel<<<(n + 255) / 256, 256, 0, st>>>(tf, max_frames, th, hp, tw, wp);
   BC_LAUNCHED();
   return BC_OK;
 }

@@ -55,6 +55,9 @@ struct QkArgs {
   int hp, wp;
   const float* norm_q;
   const float* norm_k;
+  const float2* rope_f;  // [max_frames][22] cos/sin, time pairs
+  const float2* rope_h;  // [hp][21]
+  const float2* rope_w;  // [wp][21]
   PeerArgs peer;
 };
 
@@ -85,6 +88,8 @@ int launch_head_update(const float* Y, int n, int T, int F, int H, int W, const 
                        cudaStream_t st);
 int launch_mod_combine(const float* base, const float* e0, int L, int n, int d, float* out, cudaStream_t st);
 int launch_signal_done(const PeerArgs& p, cudaStream_t st);
+int launch_rope_tables(float2* tf, int max_frames, float2* th, int hp, float2* tw, int wp, cudaStream_t st);
+constexpr int kRopeMaxFrames = 4096;
 int launch_check_finite(const EntryPtrs& lat, int n, int n_el, int32_t* status, cudaStream_t st);
 
 }  // namespace bc

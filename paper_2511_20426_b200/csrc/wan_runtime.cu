@@ -39,7 +39,8 @@ struct bc_wan_ctx {
   float* Y;
   float *t_sin, *t_h, *t_e, *t_e0, *mod_all;
   __nv_bfloat16 *text_in, *text_h, *ctx, *text_tmp, *textkv;
-  bool text_ready;
+  float2 *rope_f, *rope_h, *rope_w;
+  bool text_ready, rope_ready;
   bc_wan_peers peers;
   struct StepState {
     bc_batch batch;
@@ -94,6 +95,9 @@ int64_t carve(bc_wan_ctx* c, const bc_wan_dims& dm, char* base) {
   t->ctx = cv.take<__nv_bfloat16>((int64_t)dm.text_len * d);
   t->text_tmp = cv.take<__nv_bfloat16>((int64_t)dm.text_len * 2 * d);
   t->textkv = cv.take<__nv_bfloat16>((int64_t)dm.layers * 2 * dm.text_len * d);
+  t->rope_f = cv.take<float2>((int64_t)bc::kRopeMaxFrames * 22);
+  t->rope_h = cv.take<float2>((int64_t)(dm.latent_h / 2) * 21);
+  t->rope_w = cv.take<float2>((int64_t)(dm.latent_w / 2) * 21);
   return cv.off + 256;
 }
 
@@ -229,6 +233,10 @@ extern "C" int bc_wan_set_text(bc_wan_ctx* c, const float* states, void* stream)
   const bc_wan_dims& dm = c->dims;
   const bc_wan_params& p = c->prm;
   const int d = c->d, Lt = dm.text_len;
+  if (!c->rope_ready) {
+    RC(bc::launch_rope_tables(c->rope_f, bc::kRopeMaxFrames, c->rope_h, dm.latent_h / 2, c->rope_w, dm.latent_w / 2, st));
+    c->rope_ready = true;
+  }
   RC(bc::launch_f32_to_bf16(states, c->text_in, (int64_t)Lt * dm.text_dim, st));
   RC(gemm(c->text_in, p.text_w1, c->text_h, Lt, d, dm.text_dim, bc::kEpiGeluBf16, p.text_b1, nullptr, 0, 1, st));
   RC(gemm(c->text_h, p.text_w2, c->ctx, Lt, d, d, bc::kEpiStoreBf16, p.text_b2, nullptr, 0, 1, st));
@@ -359,9 +367,14 @@ int stage_begin(bc_wan_ctx* c, const bc_batch* batch, const bc_wan_update* upd, 
   qa.arena = c->arena;
   qa.hp = H / 2;
   qa.wp = W / 2;
+  qa.rope_f = c->rope_f;
+  qa.rope_h = c->rope_h;
+  qa.rope_w = c->rope_w;
   for (int e = 0; e < n; ++e) {
     qa.slot[e] = batch->slot[e];
     qa.frame0[e] = batch->block_index[e] * F;
+    if ((batch->block_index[e] + 1) * F > bc::kRopeMaxFrames)
+      return bc_fail(BC_ERR_CONTRACT, "bc_wan_step: frame index beyond the RoPE table (%d)", bc::kRopeMaxFrames);
   }
   if (multi) qa.peer = peer_args(c, S.epoch);
   S.self_flops = 0.0;

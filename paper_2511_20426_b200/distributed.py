@@ -197,6 +197,10 @@ class DistWanSession:
                       config.latent_width)
         self.noise = noise_feed if noise_feed is not None else HostNoiseFeed(session_seed, config)
         self.latents, self.final, self.tags, self.host_out = {}, {}, {}, {}
+        # one pinned staging area for every emitted block (no per-emission
+        # cudaHostAlloc, which would serialise against the device)
+        self.host_buf = torch.empty((config.num_blocks,) + tuple(self.shape),
+                                    dtype=torch.float32).pin_memory()
         self.eps = [torch.empty(self.shape, dtype=torch.float32, device="cuda") for _ in range(width)]
         self.events = []
         self.set_conditioning(conditioning)
@@ -262,7 +266,7 @@ class DistWanSession:
             for k, i in enumerate(local):
                 e = plan.entries[i]
                 if posts[i][0] == POST_EMIT:
-                    host = torch.empty(self.shape, dtype=torch.float32).pin_memory()
+                    host = self.host_buf[e.block_index]
                     host.copy_(self.final[e.block_index], non_blocking=True)
                     self.host_out[e.block_index] = host
                 elif posts[i][0] == POST_CACHE:
@@ -343,6 +347,10 @@ class EmulatedRanks:
                       config.latent_width)
         self.noise = noise_feed if noise_feed is not None else HostNoiseFeed(session_seed, config)
         self.latents, self.final, self.tags, self.host_out = {}, {}, {}, {}
+        # one pinned staging area for every emitted block (no per-emission
+        # cudaHostAlloc, which would serialise against the device)
+        self.host_buf = torch.empty((config.num_blocks,) + tuple(self.shape),
+                                    dtype=torch.float32).pin_memory()
         self.eps = [torch.empty(self.shape, dtype=torch.float32, device="cuda")
                     for _ in range(width * world)]
         self.events = []
@@ -431,7 +439,7 @@ class EmulatedRanks:
         for e, (kind, _, _) in zip(plan.entries, posts):
             self.tags[e.block_index] = (e.noise_level, self.cond.id)
             if kind == POST_EMIT:
-                host = torch.empty(self.shape, dtype=torch.float32).pin_memory()
+                host = self.host_buf[e.block_index]
                 host.copy_(self.final[e.block_index], non_blocking=True)
                 self.host_out[e.block_index] = host
             elif kind == POST_CACHE:

@@ -367,6 +367,10 @@ class WanSession:
         self.noise = noise_feed if noise_feed is not None else HostNoiseFeed(session_seed, config)
         self.latents, self.final, self.tags = {}, {}, {}
         self.host_out = {}
+        # one pinned staging area for every emitted block (no per-emission
+        # cudaHostAlloc, which would serialise against the device)
+        self.host_buf = torch.empty((config.num_blocks,) + tuple(self.shape),
+                                    dtype=torch.float32).pin_memory()
         self.eps = [torch.empty(self.shape, dtype=torch.float32, device="cuda")
                     for _ in range(width)]
         self.events = []
@@ -420,7 +424,7 @@ class WanSession:
         for e, (kind, _, _) in zip(plan.entries, posts):
             self.tags[e.block_index] = (e.noise_level, self.cond.id)
             if kind == POST_EMIT:
-                host = torch.empty(self.shape, dtype=torch.float32).pin_memory()
+                host = self.host_buf[e.block_index]
                 host.copy_(self.final[e.block_index], non_blocking=True)
                 self.host_out[e.block_index] = host
                 self.d2h_bytes += host.numel() * 4
