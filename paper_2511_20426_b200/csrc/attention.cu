@@ -43,6 +43,10 @@ constexpr int kTile = 2 * kHalf;      // 32 KB
 constexpr int kRing = 3;              // K/V ring slots
 constexpr int kThreads = 384;
 constexpr float kRescaleThresh = 8.0f;  // log2 domain
+#ifndef BC_ATTN_PINGPONG
+#define BC_ATTN_PINGPONG 1
+#endif
+constexpr bool kPingPong = BC_ATTN_PINGPONG != 0;
 
 struct Smem {
   static constexpr int qa = 0;
@@ -84,7 +88,8 @@ struct SoftmaxBars {
 template <int kPolyEvery>
 __device__ __forceinline__ void softmax_tile(const AttnParams& prm, uint32_t tmem_s, uint32_t tmem_o,
                                              uint8_t* sp, SoftmaxBars b, int n_tiles, int tiles_per_slot,
-                                             uint32_t quad, int q_row0, int e, int head) {
+                                             uint32_t quad, int q_row0, int e, int head, int tile_x,
+                                             bool pingpong) {
   const uint32_t row = quad * 32 + lane_id();
   const uint32_t lane_base = (quad * 32) << 16;
   const float c = prm.scale * 1.4426950408889634f;
@@ -125,6 +130,14 @@ __device__ __forceinline__ void softmax_tile(const AttnParams& prm, uint32_t tme
     float tsum = 0.0f;
     const float neg_m = -m_used;
     uint32_t pk[64];
+    // MUFU ping-pong: the two softmax warpgroups take turns on the
+    // exponential phase (named barriers 1 = A->B, 2 = B->A), so one
+    // warpgroup's exp overlaps the tensor core's MMAs for the other tile
+    // instead of both exp phases colliding on the shared MUFU pipe.
+    if (pingpong) {
+      if (tile_x == 0 && j > 0) asm volatile("bar.sync 2, 256;" ::: "memory");
+      if (tile_x == 1) asm volatile("bar.sync 1, 256;" ::: "memory");
+    }
     if (valid == kKeys) {
       // full tile: every 4th pair of exponentials on the FMA pipe
 #pragma unroll
@@ -148,6 +161,10 @@ __device__ __forceinline__ void softmax_tile(const AttnParams& prm, uint32_t tme
         tsum += p0 + p1;
         pk[t] = pack_bf16(p0, p1);
       }
+    }
+    if (pingpong) {
+      if (tile_x == 0) asm volatile("bar.arrive 1, 256;" ::: "memory");
+      if (tile_x == 1 && j + 1 < n_tiles) asm volatile("bar.arrive 2, 256;" ::: "memory");
     }
     // PV(j-1) must be complete before O is rescaled or P is overwritten
     if (j > 0) {
@@ -366,7 +383,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (x == 0 || has_b) {
       SoftmaxBars b{&s_full[x], &s_empty[x], &p_full[x], &o_ready[x]};
       softmax_tile<kPolyEvery>(prm, tmem + x * 128, tmem + 256 + x * 128, smem + (x ? Smem::pb : Smem::pa), b, n_tiles,
-                   tiles_per_slot, warp & 3, q0 + x * kRows, e, head);
+                   tiles_per_slot, warp & 3, q0 + x * kRows, e, head, x, has_b && kPingPong);
     }
   }
   tc_fence_before();
