@@ -158,3 +158,51 @@ def test_wan_13b_dims_step(monkeypatch):
         visible_blocks(batch, [0], "bidirectional"), text_states(cond, cfg.text_len, cfg.text_dim))
     for o, (x0, _) in zip(outs, ref):
         assert rel(o.x0, x0.reshape(o.x0.shape)) < STEP_TOL
+
+
+def test_wan_14b_dims_step():
+    """Wan2.1-14B layer geometry (d=5120, 40 heads, ffn 13824; the row
+    kernels take their multi-warp path), 1 layer, 160x160 latent, width-2
+    cascade step over a 1-block pool, teacher-forced vs the oracle."""
+    import paper_2511_20426_b200 as bc
+    from oracle import wan as wo
+    from oracle.schedule import visible_blocks
+    from paper_2511_20426_b200.wan import WanWeights, text_states
+    cfg = bc.wan_config("14b", layers=1, latent_height=16, latent_width=16, text_len=128,
+                        total_frames=9)
+    w = WanWeights.random(cfg, 5)
+    cond = bc.embed_prompt("a red cube", cfg.cond_dim)
+    rng = np.random.default_rng(4)
+    pool = _pool(bc, cfg, w, [0], cond, rng)
+    batch, levels = [1, 2], [250.0, 750.0]
+    lat = {b: rng.standard_normal((cfg.block_size, cfg.latent_dim)).astype(np.float32) for b in batch}
+    mask = bc.build_mask(batch, [0], "causal", cfg.block_size)
+    outs = bc.forward(w, [bc.EntryInput(b, lat[b], lv, cond) for b, lv in zip(batch, levels)], pool, mask)
+    d = cfg.model_dim
+    pool_kv = {0: [(l.keys.reshape(-1, d), l.values.reshape(-1, d)) for l in pool[0]]}
+    ref = wo.WanOracle(w.host_params(), cfg).forward(
+        [(b, lat[b], lv) for b, lv in zip(batch, levels)], pool_kv,
+        visible_blocks(batch, [0], "causal"), text_states(cond, cfg.text_len, cfg.text_dim))
+    for o, (x0, _) in zip(outs, ref):
+        assert rel(o.x0, x0.reshape(o.x0.shape)) < STEP_TOL
+
+
+def test_wan_longlive_style_run(tiny, monkeypatch):
+    """Config-5 shape at tiny scale: long rollout (24 blocks), rolling
+    window without sink, cascade-mode prompt switches every 6 blocks, no
+    KV recache -- free-running vs the oracle engine."""
+    import paper_2511_20426_b200 as bc
+    from paper_2511_20426_b200 import engine
+    from oracle.loop import wan_oracle_runtime
+    cfg, w, params = tiny
+    cfg = bc.with_fields(cfg, total_frames=72, sink_blocks=0, window_blocks=5)
+    sw = [bc.SwitchSpec(f"scene {k}", "cascade", at_block=k) for k in (6, 12, 18)]
+    gpu = bc.run_cascade(cfg, "scene 0", weights=w, switches=sw)
+    assert [e.extra_passes for e in gpu.switch_events] == [0, 0, 0]
+    assert gpu.iterations == (cfg.num_blocks - 1) + cfg.passes
+    assert all(ev.pool_blocks <= 5 for ev in gpu.trace.events)
+    with monkeypatch.context() as m:
+        m.setattr(engine, "_runtime_for", wan_oracle_runtime(params))
+        cpu = bc.run_cascade(cfg, "scene 0", weights=w, switches=sw)
+    for b in range(cfg.num_blocks):
+        assert rel(gpu.outputs[b], cpu.outputs[b]) < RUN_TOL, b
