@@ -296,7 +296,7 @@ __global__ void qk_norm_rope_kernel(const __nv_bfloat16* __restrict__ qkv, int r
         o[j + 1] = __float2bfloat16(x0 * cs.y + x1 * cs.x);
       }
       reinterpret_cast<uint4*>(dst)[idx] = u;
-      if (which == 1) {  // fresh K -> every peer's replica (NVLink P2P store)
+      if (which == 1 && a.peer.push) {  // fresh K -> every peer's replica (NVLink P2P store)
         for (int p = 0; p < a.peer.n_peers; ++p)
           reinterpret_cast<uint4*>(a.peer.arena[p] + (dst - a.arena))[idx] = u;
       }
@@ -308,10 +308,11 @@ __global__ void qk_norm_rope_kernel(const __nv_bfloat16* __restrict__ qkv, int r
     for (int idx = li; idx * 8 < d; idx += 32 * WPR) {
       const uint4 u = v4[idx];
       reinterpret_cast<uint4*>(vdst)[idx] = u;
-      for (int p = 0; p < a.peer.n_peers; ++p) reinterpret_cast<uint4*>(a.peer.arena[p] + (vdst - a.arena))[idx] = u;
+      if (a.peer.push)
+        for (int p = 0; p < a.peer.n_peers; ++p) reinterpret_cast<uint4*>(a.peer.arena[p] + (vdst - a.arena))[idx] = u;
     }
   }
-  if (a.peer.n_peers > 0) {
+  if (a.peer.n_peers > 0 && a.peer.push) {
     last_cta_publish(a.peer.ctr, [&] {
       const int n = rows / T;
       for (int p = 0; p < a.peer.n_peers; ++p)

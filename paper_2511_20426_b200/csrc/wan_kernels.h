@@ -44,6 +44,7 @@ struct PeerArgs {
   uint32_t wait_done;                   // wait until every peer's done >= this (0 = no wait)
   int flag_base;                        // layer * n_slots
   uint32_t* ctr;                        // zeroed launch counter (last-CTA detection)
+  int push;                             // 1: q/k kernel stores K/V into peers + publishes
 };
 
 struct QkArgs {

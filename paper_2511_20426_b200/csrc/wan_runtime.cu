@@ -19,6 +19,10 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <stdlib.h>
+
 #include <cstring>
 #include <new>
 #include <vector>
@@ -42,6 +46,10 @@ struct bc_wan_ctx {
   float2 *rope_f, *rope_h, *rope_w;
   bool text_ready, rope_ready;
   bc_wan_peers peers;
+  // copy-engine push of fresh K/V to the peers' replicas (multi-GPU)
+  bool push_by_copy;
+  cudaStream_t side;
+  cudaEvent_t ev_qk, ev_side;
   struct StepState {
     bc_batch batch;
     bc_wan_update upd;
@@ -158,6 +166,18 @@ int timed(int cls, double flops, double bytes, cudaStream_t st, F&& f) {
   return rc;
 }
 
+PFN_cuStreamWriteValue32_v11070 write_value32() {
+  static PFN_cuStreamWriteValue32_v11070 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuStreamWriteValue32_v11070>(p);
+  }
+  return fn;
+}
+
 template <typename T>
 const T* at(const void* base, int64_t elems) {
   return static_cast<const T*>(base) + elems;
@@ -221,6 +241,12 @@ extern "C" int bc_wan_create(const bc_wan_dims* dims, const bc_wan_params* param
 }
 
 extern "C" int bc_wan_destroy(bc_wan_ctx* ctx) {
+  if (ctx && ctx->side) {
+    cudaStreamSynchronize(ctx->side);
+    cudaStreamDestroy(ctx->side);
+    cudaEventDestroy(ctx->ev_qk);
+    cudaEventDestroy(ctx->ev_side);
+  }
   delete ctx;
   return BC_OK;
 }
@@ -402,7 +428,33 @@ int stage_layer_a(bc_wan_ctx* c, int l, cudaStream_t st) {
   // the first K/V write of an iteration waits until every peer finished
   // reading the previous iteration's KV (slot reuse / in-place rewrite)
   qa.peer.wait_done = (l == 0 && S.epoch > 1) ? S.epoch - 1 : 0u;
+  qa.peer.push = (c->peers.n_peers > 0 && !c->push_by_copy) ? 1 : 0;
   RC(timed(kBandwidth, 0.0, 12.0 * R * d, st, [&] { return bc::launch_qk_norm_rope(c->qkv, R, d, T, qa, st); }));
+  if (c->peers.n_peers > 0 && c->push_by_copy && S.epoch > 0) {
+    // copy engines move each local entry's fresh K/V (layer l, one
+    // contiguous [2][T][d] slot matrix) into every peer replica, then a
+    // stream memory op publishes the (layer, slot) epoch -- no SM is needed,
+    // so a peer's spinning attention can never starve the transfer.
+    auto wv = write_value32();
+    if (!wv) return bc_fail(BC_ERR_CUDA, "cuStreamWriteValue32 unavailable");
+    BC_CUDA(cudaEventRecord(c->ev_qk, st));
+    BC_CUDA(cudaStreamWaitEvent(c->side, c->ev_qk, 0));
+    const size_t mat_bytes = (size_t)T * d * sizeof(__nv_bfloat16);
+    for (int e = 0; e < n; ++e) {
+      const size_t off = ((size_t)qa.mat_base + (size_t)S.batch.slot[e] * 2) * mat_bytes;
+      for (int pp = 0; pp < c->peers.n_peers; ++pp)
+        BC_CUDA(cudaMemcpyAsync(static_cast<char*>(c->peers.peer_arena[pp]) + off,
+                                reinterpret_cast<const char*>(c->arena) + off, 2 * mat_bytes,
+                                cudaMemcpyDeviceToDevice, c->side));
+    }
+    for (int pp = 0; pp < c->peers.n_peers; ++pp)
+      for (int e = 0; e < n; ++e) {
+        CUresult rr = wv((CUstream)c->side,
+                         (CUdeviceptr)(c->peers.peer_flags[pp] + (size_t)l * dm.n_slots + S.batch.slot[e]), S.epoch,
+                         0);
+        if (rr != CUDA_SUCCESS) return bc_fail(BC_ERR_CUDA, "cuStreamWriteValue32 failed (%d)", (int)rr);
+      }
+  }
   return BC_OK;
 }
 
@@ -455,7 +507,13 @@ int stage_end(bc_wan_ctx* c, cudaStream_t st) {
     u.post[e] = S.upd.post[e];
     u.block[e] = S.batch.block_index[e];
   }
-  if (c->peers.n_peers > 0 && S.epoch > 0) u.peer = peer_args(c, S.epoch);
+  if (c->peers.n_peers > 0 && S.epoch > 0) {
+    u.peer = peer_args(c, S.epoch);
+    if (c->push_by_copy) {  // this iteration's pushes are ordered before our done signal
+      BC_CUDA(cudaEventRecord(c->ev_side, c->side));
+      BC_CUDA(cudaStreamWaitEvent(st, c->ev_side, 0));
+    }
+  }
   RC(timed(kBandwidth, 0.0, (4.0 * 64 + 16.0 * 16) * R, st, [&] { return bc::launch_head_update(c->Y, n, T, F, dm.latent_h, dm.latent_w, u, S.status, st); }));
   return BC_OK;
 }
@@ -487,6 +545,13 @@ extern "C" int bc_wan_set_peers(bc_wan_ctx* c, const bc_wan_peers* peers) {
     if (!peers->peer_arena[p] || !peers->peer_flags[p] || !peers->peer_done[p])
       return bc_fail(BC_ERR_CONTRACT, "bc_wan_set_peers: null peer pointer");
   c->peers = *peers;
+  const char* how = getenv("BC_KV_PUSH");  // "kernel": P2P stores inside the q/k kernel
+  c->push_by_copy = !(how && std::strcmp(how, "kernel") == 0);
+  if (peers->n_peers > 0 && !c->side) {
+    BC_CUDA(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
+    BC_CUDA(cudaEventCreateWithFlags(&c->ev_qk, cudaEventDisableTiming));
+    BC_CUDA(cudaEventCreateWithFlags(&c->ev_side, cudaEventDisableTiming));
+  }
   return BC_OK;
 }
 

@@ -25,10 +25,14 @@ def _stack(run):
     return np.stack([run.outputs[k] for k in sorted(run.outputs)])
 
 
-@pytest.mark.parametrize("mode", ["bidirectional", "causal"])
-def test_emulated_ranks_bit_identical(tiny, monkeypatch, mode):
+@pytest.mark.parametrize("mode,push", [("bidirectional", "copy"), ("causal", "copy"),
+                                       ("bidirectional", "kernel")])
+def test_emulated_ranks_bit_identical(tiny, monkeypatch, mode, push):
+    """push = copy: copy engines + stream memory ops move the fresh K/V and
+    publish the flags; push = kernel: P2P stores from the q/k kernel."""
     import paper_2511_20426_b200 as bc
     from paper_2511_20426_b200 import distributed
+    monkeypatch.setenv("BC_KV_PUSH", push)
     cfg, w = tiny
     cfg = bc.with_fields(cfg, attention_mode=mode)
     base = bc.run_cascade(cfg, "a lighthouse in a storm", weights=w)
