@@ -1,0 +1,59 @@
+"""The real one-process-per-rank path (DistWanSession: CUDA-IPC-mapped peer
+KV replicas, copy-engine K/V pushes, stream-memop flags, done epochs, output
+gather) with two processes sharing cuda:0 over a gloo group.  The GPU
+time-slices the two contexts; outputs must equal the single-process run
+bit-for-bit (placement independence, reference test_acceptance.py:58-76)."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _rank(rank, world, port, q, mode):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import torch
+    import torch.distributed as dist
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_2511_20426_b200 as bc
+        from paper_2511_20426_b200.wan import WanWeights
+        cfg = bc.wan_config("tiny", total_frames=15, attention_mode=mode)
+        w = WanWeights.random(cfg, 7)
+        run = bc.run_cascade(cfg, "a lighthouse in a storm", weights=w)
+        if rank == 0:
+            q.put({b: run.outputs[b] for b in run.outputs})
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("mode", ["bidirectional", "causal"])
+def test_two_processes_one_gpu(mode):
+    import torch.multiprocessing as mp
+    import paper_2511_20426_b200 as bc
+    from paper_2511_20426_b200.wan import WanWeights
+    cfg = bc.wan_config("tiny", total_frames=15, attention_mode=mode)
+    base = bc.run_cascade(cfg, "a lighthouse in a storm", weights=WanWeights.random(cfg, 7))
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_rank, args=(r, 2, port, q, mode)) for r in range(2)]
+    for p in procs:
+        p.start()
+    got = q.get(timeout=600)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    assert sorted(got) == sorted(base.outputs)
+    for b in base.outputs:
+        assert np.array_equal(got[b], base.outputs[b]), b
