@@ -164,6 +164,21 @@ def cpu_sample_desc(cfg):
             f"fps = 12 frames / (sample x {cfg.layers * min(cfg.cascade_width, cfg.num_blocks)})")
 
 
+def metric_name(args):
+    return f"generated frames/sec (cascaded, Wan2.1-{args.preset.upper()}-shaped, 480x832)"
+
+
+def workload_config(args, cfg, parallelism):
+    return {"workload": f"wan2.1-{args.preset} cascade o=1, {cfg.num_blocks} blocks "
+                        f"({cfg.num_blocks * FRAMES_PER_BLOCK} frames), 480x832, 4-step, "
+                        f"3 latent frames/block, bidirectional, W=7 sink={args.sink}"
+                        + (f", cascade prompt switch every {args.switch_every} blocks"
+                           if args.switch_every else ""),
+            "model": f"wan2.1-{args.preset}-shaped", "global_batch": 1,
+            "seq_len": cfg.tokens_per_block, "parallelism": parallelism,
+            "l2": "working set (weights + KV arena) >> 126 MB L2; no flush"}
+
+
 def run_reference(args, cfg):
     world, rank, _ = dist_env()
     if rank != 0:
@@ -175,12 +190,11 @@ def run_reference(args, cfg):
     per = statistics.mean(times)
     fps = cpu_fps_from_sample(cfg, per)
     line = {
-        "impl": "reference", "metric": "generated frames/sec (cascaded, Wan2.1-1.3B-shaped, 480x832)",
+        "impl": "reference", "metric": metric_name(args),
         "value": fps, "unit": "frames/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": per * 1e3, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "f32", "data": "synthetic (random-init weights, N(0,1) activations)",
-        "config": {"workload": "wan2.1-1.3b cascade o=1, 13 blocks, 480x832, bidirectional, W=7 sink=1",
-                   "model": "wan2.1-1.3b-shaped", "parallelism": "cpu"},
+        "config": workload_config(args, cfg, "cpu"),
         "cpu_baseline": {"value": fps, "unit": "frames/s", "cores": cores, "kind": "port",
                          "sample": cpu_sample_desc(cfg)},
         "e2e": {"value": fps, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -302,20 +316,13 @@ def run_ours(args, cfg):
         cpu = {"value": cpu_fps_from_sample(cfg, samp), "unit": "frames/s", "cores": os.cpu_count(),
                "kind": "port", "sample": cpu_sample_desc(cfg), "sample_seconds": samp}
     line = {
-        "metric": f"generated frames/sec (cascaded, Wan2.1-{args.preset.upper()}-shaped, 480x832)",
+        "metric": metric_name(args),
         "value": value, "unit": "frames/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic (random-init Wan2.1-1.3B-shaped weights, counter-keyed N(0,1) noise, "
                 "hash-expanded 512x4096 text states)",
-        "config": {"workload": f"wan2.1-{args.preset} cascade o=1, {cfg.num_blocks} blocks "
-                               f"({cfg.num_blocks * FRAMES_PER_BLOCK} frames), 480x832, 4-step, "
-                               f"3 latent frames/block, bidirectional, W=7 sink={args.sink}"
-                               + (f", cascade prompt switch every {args.switch_every} blocks"
-                                  if args.switch_every else ""),
-                   "model": f"wan2.1-{args.preset}-shaped", "global_batch": 1,
-                   "seq_len": cfg.tokens_per_block, "parallelism": f"temporal{world}",
-                   "l2": "working set (2.6 GB weights + 11 GB KV arena) >> 126 MB L2; no flush"},
+        "config": workload_config(args, cfg, f"temporal{world}"),
         "streaming_fps": stream_fps,
         "sequential": {"e2e_fps": seq_e2e, "streaming_fps": seq_stream},
         "cascade_over_sequential_streaming": stream_fps / seq_stream if seq_stream else None,
