@@ -194,7 +194,7 @@ def run_reference(args, cfg):
         "value": fps, "unit": "frames/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": per * 1e3, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "f32", "data": "synthetic (random-init weights, N(0,1) activations)",
-        "config": workload_config(args, cfg, "cpu"),
+        "config": workload_config(args, cfg, f"temporal{world}"),
         "cpu_baseline": {"value": fps, "unit": "frames/s", "cores": cores, "kind": "port",
                          "sample": cpu_sample_desc(cfg)},
         "e2e": {"value": fps, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
