@@ -47,6 +47,10 @@ constexpr float kRescaleThresh = 8.0f;  // log2 domain
 #define BC_ATTN_PINGPONG 1
 #endif
 constexpr bool kPingPong = BC_ATTN_PINGPONG != 0;
+#ifndef BC_ATTN_ALU_PACK
+#define BC_ATTN_ALU_PACK 1
+#endif
+constexpr bool kAluPack = BC_ATTN_ALU_PACK != 0;
 
 struct Smem {
   static constexpr int qa = 0;
@@ -75,6 +79,16 @@ __device__ __forceinline__ float ex2_poly(float x) {
   const float p = fmaf(fmaf(fmaf(0.05508868380751114f, f, 0.24260405145947936f), f, 0.6932762416819607f), f,
                        0.9999289403695112f);
   return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
+}
+
+// fp32 pair -> bf16x2 with round-to-nearest-even on the integer ALU
+// (inputs are finite and >= 0), keeping F2FP off the MUFU/XU pipe that the
+// exponentials saturate.
+__device__ __forceinline__ uint32_t pack_bf16_alu(float a, float b) {
+  uint32_t ua = __float_as_uint(a), ub = __float_as_uint(b);
+  ua += 0x7FFFu + ((ua >> 16) & 1u);
+  ub += 0x7FFFu + ((ub >> 16) & 1u);
+  return __byte_perm(ua, ub, 0x7632);
 }
 
 struct SoftmaxBars {
@@ -151,7 +165,7 @@ __device__ __forceinline__ void softmax_tile(const AttnParams& prm, uint32_t tme
           p1 = ex2(fmaf(s[2 * t + 1], c, neg_m));
         }
         tsum += p0 + p1;
-        pk[t] = pack_bf16(p0, p1);
+        pk[t] = kAluPack ? pack_bf16_alu(p0, p1) : pack_bf16(p0, p1);
       }
     } else {
 #pragma unroll
@@ -159,7 +173,7 @@ __device__ __forceinline__ void softmax_tile(const AttnParams& prm, uint32_t tme
         const float p0 = ex2(fmaf(s[2 * t], c, neg_m));
         const float p1 = ex2(fmaf(s[2 * t + 1], c, neg_m));
         tsum += p0 + p1;
-        pk[t] = pack_bf16(p0, p1);
+        pk[t] = kAluPack ? pack_bf16_alu(p0, p1) : pack_bf16(p0, p1);
       }
     }
     if (pingpong) {
