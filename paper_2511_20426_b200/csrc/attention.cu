@@ -48,7 +48,7 @@ constexpr float kRescaleThresh = 8.0f;  // log2 domain
 #endif
 constexpr bool kPingPong = BC_ATTN_PINGPONG != 0;
 #ifndef BC_ATTN_ALU_PACK
-#define BC_ATTN_ALU_PACK 1
+#define BC_ATTN_ALU_PACK 0
 #endif
 constexpr bool kAluPack = BC_ATTN_ALU_PACK != 0;
 
