@@ -32,6 +32,16 @@
 #include "bc_common.h"
 #include "sm100.cuh"
 
+#ifdef BC_ATTN_TRACE
+unsigned long long* bc_attn_trace_ptr = nullptr;
+extern "C" int bc_attn_trace_read(unsigned long long* host) {
+  if (!bc_attn_trace_ptr) return 1;
+  cudaDeviceSynchronize();
+  cudaMemcpy(host, bc_attn_trace_ptr, 32 * 64 * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+  return 0;
+}
+#endif
+
 namespace bc {
 namespace {
 
@@ -91,6 +101,21 @@ __device__ __forceinline__ uint32_t pack_bf16_alu(float a, float b) {
   return __byte_perm(ua, ub, 0x7632);
 }
 
+// Diagnostic timeline (BC_ATTN_TRACE builds only): CTA (0,0,0) records
+// clock64() at protocol points into prm.trace[slot*64 + j].
+#ifdef BC_ATTN_TRACE
+#define ATRACE(slot, j)                                                                       \
+  do {                                                                                        \
+    if (prm.trace && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && lane_id() == 0 && \
+        (j) < 64)                                                                             \
+      prm.trace[(slot) * 64 + (j)] = clock64();                                               \
+  } while (0)
+#else
+#define ATRACE(slot, j) \
+  do {                  \
+  } while (0)
+#endif
+
 struct SoftmaxBars {
   uint64_t* s_full;
   uint64_t* s_empty;
@@ -112,6 +137,7 @@ __device__ __forceinline__ void softmax_tile(const AttnParams& prm, uint32_t tme
     const int t0 = (j % tiles_per_slot) * kKeys;
     const int valid = min(kKeys, prm.kv_tokens - t0);
     mbar_wait(b.s_full, j & 1);
+    if ((quad) == 0) ATRACE(0 + tile_x * 8, j);
     tc_fence_after();
     float s[128];
 #pragma unroll
@@ -152,6 +178,7 @@ __device__ __forceinline__ void softmax_tile(const AttnParams& prm, uint32_t tme
       if (tile_x == 0 && j > 0) asm volatile("bar.sync 2, 256;" ::: "memory");
       if (tile_x == 1) asm volatile("bar.sync 1, 256;" ::: "memory");
     }
+    if (quad == 0) ATRACE(1 + tile_x * 8, j);
     if (valid == kKeys) {
       // full tile: every 4th pair of exponentials on the FMA pipe
 #pragma unroll
@@ -177,6 +204,7 @@ __device__ __forceinline__ void softmax_tile(const AttnParams& prm, uint32_t tme
       }
     }
     if (pingpong) {
+      if (quad == 0) ATRACE(2 + tile_x * 8, j);
       if (tile_x == 0) asm volatile("bar.arrive 1, 256;" ::: "memory");
       if (tile_x == 1 && j + 1 < n_tiles) asm volatile("bar.arrive 2, 256;" ::: "memory");
     }
@@ -209,6 +237,7 @@ __device__ __forceinline__ void softmax_tile(const AttnParams& prm, uint32_t tme
     fence_async_shared();
     tc_fence_before();
     mbar_arrive(b.p_full);
+    if (quad == 0) ATRACE(3 + tile_x * 8, j);
   }
   // epilogue: O / l -> bf16
   if (n_tiles > 0) {
@@ -380,14 +409,18 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int x = 0; x < n_q; ++x) {
         if (next) {
           mbar_wait(&s_empty[x], j & 1);  // softmax x has read S_x(j)
+          ATRACE(16 + x * 4, j);
           if (x == 0) ring_wait(2 * (j + 1));
           tc_fence_after();
           issue_qk(x, j + 1);
+          ATRACE(17 + x * 4, j);
         }
         mbar_wait(&p_full[x], j & 1);
+        ATRACE(18 + x * 4, j);
         if (x == 0) ring_wait(2 * j + 1);
         tc_fence_after();
         issue_pv(x, j);
+        ATRACE(19 + x * 4, j);
       }
       if (next) release(2 * (j + 1));
       release(2 * j + 1);
@@ -471,6 +504,15 @@ int attention_run(const AttnArgs& a, cudaStream_t st) {
   }
   p.flags = a.flags;
   p.flag_base = a.flag_base;
+  p.trace = nullptr;
+#ifdef BC_ATTN_TRACE
+  {
+    static unsigned long long* buf = nullptr;
+    if (!buf) cudaMalloc(&buf, 32 * 64 * sizeof(unsigned long long));
+    p.trace = buf;
+    bc_attn_trace_ptr = buf;
+  }
+#endif
   static int poly = -1;
   if (poly < 0) {
     const char* env = getenv("BC_ATTN_POLY");  // tuning knob: 0 = all MUFU

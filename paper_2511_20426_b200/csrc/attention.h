@@ -17,6 +17,7 @@ struct AttnParams {
   int v_offset;    // matrices from a slot's K to its V
   float scale;     // softmax scale (1/sqrt(head_dim))
   void* out;       // bf16 [n_entries*q_tokens][heads*128]
+  unsigned long long* trace;  // diagnostic timeline (BC_ATTN_TRACE builds)
   int n_vis[BC_MAX_ENTRIES];
   int vis_slot[BC_MAX_ENTRIES][BC_MAX_VIS];
   // multi-GPU: before the first tile of visible slot v, wait until

@@ -1,0 +1,41 @@
+#!/bin/bash
+# Build a tracing variant of the library (BC_ATTN_TRACE) into /tmp and dump
+# the per-phase timeline of CTA (0,0,0) of a steady-state attention launch.
+set -e
+cd "$(dirname "$0")/../paper_2511_20426_b200/csrc"
+OUT=/tmp/bc_trace; mkdir -p $OUT
+NV="nvcc -O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a -Xcompiler -fPIC --expt-relaxed-constexpr"
+for f in *.cu; do $NV -DBC_ATTN_TRACE -c $f -o $OUT/${f%.cu}.o; done
+for f in *.cpp; do g++ -O3 -std=c++17 -fPIC -c $f -o $OUT/${f%.cpp}.o; done
+NPR=$(python -c "import numpy,os;print(os.path.join(os.path.dirname(numpy.__file__),'random','lib'))")
+nvcc -gencode arch=compute_100a,code=sm_100a -shared -o $OUT/libbcb200.so $OUT/*.o -L$NPR -lnpyrandom -lm -lpthread
+cd ../..
+python - <<'PY'
+import ctypes, sys, numpy as np, os
+sys.path.insert(0, os.getcwd())
+from paper_2511_20426_b200 import _native as N
+N.LIB_PATH = "/tmp/bc_trace/libbcb200.so"
+import torch
+T, heads, n_ent, n_vis = 4680, 12, 5, 13
+arena = torch.randn(13, 2, T, heads * 128, device="cuda").bfloat16()
+q = torch.randn(n_ent * T, heads * 128, device="cuda").bfloat16()
+out = torch.empty_like(q)
+b = N.make_batch(3, list(range(n_ent)), [0.0] * n_ent, [0] * n_ent, [list(range(n_vis))] * n_ent)
+mat = T * heads * 128
+for _ in range(3):
+    N.check(N.lib().bc_attention_paged(N.ptr(q), N.ptr(arena), N.ptr(arena) + mat * 2, 2 * mat, T, b, T,
+                                       heads, N.ptr(out), N.stream_ptr()), "attn")
+buf = (ctypes.c_ulonglong * (32 * 64))()
+lib = ctypes.CDLL(N.LIB_PATH)
+lib.bc_attn_trace_read(buf)
+t = np.array(buf, dtype=np.int64).reshape(32, 64)
+t0 = t[t > 0].min()
+names = {0: "A s_full", 1: "A token", 2: "A exp done", 3: "A p_full", 8: "B s_full", 9: "B token", 10: "B exp done",
+         11: "B p_full", 16: "M s_emptyA", 17: "M QK_A", 18: "M p_fullA", 19: "M PV_A", 20: "M s_emptyB",
+         21: "M QK_B", 22: "M p_fullB", 23: "M PV_B"}
+for j in range(20, 28):
+    row = {names[k]: int(t[k, j] - t0) for k in names if t[k, j] > 0}
+    print(j, sorted(row.items(), key=lambda kv: kv[1]))
+per = [(t[1, j + 1] - t[1, j]) for j in range(20, 40)]
+print("A token period (cycles):", per)
+PY
