@@ -116,6 +116,26 @@ __device__ __forceinline__ uint32_t pack_bf16_alu(float a, float b) {
   } while (0)
 #endif
 
+// Ring positions: K_0 -> 0, K_m -> 2m-1 (m >= 1); V_m -> 2m+2, except the
+// last V_{n-1} -> 2n-1.  (Emission order K0 K1 V0 K2 V1 ... K_{n-1} V_{n-2} V_{n-1}.)
+__device__ __forceinline__ int kpos(int m) { return m == 0 ? 0 : 2 * m - 1; }
+__device__ __forceinline__ int vpos(int m, int n) { return m == n - 1 ? 2 * n - 1 : 2 * m + 2; }
+__device__ __forceinline__ void ring_item(int i, int n, int& j, int& is_v) {
+  if (i == 0) {
+    j = 0;
+    is_v = 0;
+  } else if (i == 2 * n - 1) {
+    j = n - 1;
+    is_v = 1;
+  } else if (i & 1) {  // odd positions are K_{(i+1)/2}
+    j = (i + 1) >> 1;
+    is_v = 0;
+  } else {             // even positions >= 2 are V_{(i-2)/2}
+    j = (i - 2) >> 1;
+    is_v = 1;
+  }
+}
+
 struct SoftmaxBars {
   uint64_t* s_full;
   uint64_t* s_empty;
@@ -327,9 +347,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         tma_load_3d(smem + Smem::qb, &map_q, q_full, 0, head, qrow + kRows);
         tma_load_3d(smem + Smem::qb + kHalf, &map_q, q_full, 64, head, qrow + kRows);
       }
-      // ring order: K0 V0 K1 V1 ...
+      // ring order K0 K1 V0 K2 V1 K3 V2 ... (K runs one tile ahead of V, see
+      // ring_pos): K_{j+1} is consumed in the same period as V_j, so with
+      // this order every load has about one period of prefetch slack in a
+      // 3-slot ring.
       for (int i = 0; i < 2 * n_tiles; ++i) {
-        const int j = i >> 1, is_v = i & 1;
+        int j, is_v;
+        ring_item(i, n_tiles, j, is_v);
         const int slot = i % kRing;
         const uint32_t ph = (i / kRing) & 1;
         const int kv_slot = prm.vis_slot[e][j / tiles_per_slot];
@@ -364,7 +388,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     auto ring_slot = [&](int i) { return smem_u32(smem + Smem::ring + (i % kRing) * kTile); };
     auto issue_qk = [&](int x, int j) {  // S_x = Q_x K_j^T ; K_j is ring item 2j
       if (elect_one()) {
-        const uint32_t sk = ring_slot(2 * j);
+        const uint32_t sk = ring_slot(kpos(j));
 #pragma unroll
         for (int k = 0; k < kHd / 16; ++k) {
           const uint32_t off = (k >> 2) * kHalf + (k & 3) * 32;
@@ -377,7 +401,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     };
     auto issue_pv = [&](int x, int j) {  // O_x += P_x V_j ; V_j is ring item 2j+1
       if (elect_one()) {
-        const uint32_t sv = ring_slot(2 * j + 1);
+        const uint32_t sv = ring_slot(vpos(j, n_tiles));
 #pragma unroll
         for (int k = 0; k < kKeys / 16; ++k) {
           const uint32_t aoff = (k >> 2) * kHalf + (k & 3) * 32;
@@ -410,20 +434,20 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (next) {
           mbar_wait(&s_empty[x], j & 1);  // softmax x has read S_x(j)
           ATRACE(16 + x * 4, j);
-          if (x == 0) ring_wait(2 * (j + 1));
+          if (x == 0) ring_wait(kpos(j + 1));
           tc_fence_after();
           issue_qk(x, j + 1);
           ATRACE(17 + x * 4, j);
         }
         mbar_wait(&p_full[x], j & 1);
         ATRACE(18 + x * 4, j);
-        if (x == 0) ring_wait(2 * j + 1);
+        if (x == 0) ring_wait(vpos(j, n_tiles));
         tc_fence_after();
         issue_pv(x, j);
         ATRACE(19 + x * 4, j);
       }
-      if (next) release(2 * (j + 1));
-      release(2 * j + 1);
+      if (next) release(kpos(j + 1));
+      release(vpos(j, n_tiles));
     }
   } else if (warp >= 4) {
     const int x = (warp >= 8) ? 1 : 0;
