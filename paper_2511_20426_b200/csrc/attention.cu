@@ -54,7 +54,7 @@ constexpr int kRing = 3;              // K/V ring slots
 constexpr int kThreads = 384;
 constexpr float kRescaleThresh = 8.0f;  // log2 domain
 #ifndef BC_ATTN_PINGPONG
-#define BC_ATTN_PINGPONG 1
+#define BC_ATTN_PINGPONG 0
 #endif
 constexpr bool kPingPong = BC_ATTN_PINGPONG != 0;
 #ifndef BC_ATTN_ALU_PACK
