@@ -1,0 +1,30 @@
+"""Small launches of every device kernel family for compute-sanitizer."""
+import os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+import torch
+import paper_2511_20426_b200 as bc
+from paper_2511_20426_b200 import _native as N
+from paper_2511_20426_b200.wan import WanWeights
+
+# GEMM, all epilogues, ragged M
+A = torch.randn(300, 256, device="cuda").bfloat16(); B = torch.randn(256, 256, device="cuda").bfloat16()
+for mode, dt in ((0, torch.bfloat16), (1, torch.bfloat16), (2, torch.float32), (3, torch.float32)):
+    C = torch.zeros(300, 256, device="cuda", dtype=dt)
+    g = torch.ones(4, 256, device="cuda")
+    N.check(N.lib().bc_gemm_bf16(N.ptr(A), N.ptr(B), N.ptr(C), 300, 256, 256, mode, 0,
+                                 N.ptr(g) if mode == 3 else 0, 256, 100, N.stream_ptr()), "gemm")
+# attention, ragged q/kv
+T, H = 200, 2
+arena = torch.randn(4, 2, T, H * 128, device="cuda").bfloat16()
+q = torch.randn(2 * T, H * 128, device="cuda").bfloat16(); out = torch.empty_like(q)
+b = N.make_batch(3, [0, 1], [0.0, 0.0], [0, 1], [[0, 1], [0, 1, 2, 3]])
+mat = T * H * 128
+N.check(N.lib().bc_attention_paged(N.ptr(q), N.ptr(arena), N.ptr(arena) + mat * 2, 2 * mat, T, b, T, H,
+                                   N.ptr(out), N.stream_ptr()), "attn")
+# tiny Wan cascade (all kernels incl. head update) + toy
+cfg = bc.wan_config("tiny", total_frames=9)
+bc.run_cascade(cfg, "p", weights=WanWeights.random(cfg, 1))
+bc.run_cascade(bc.CascadeConfig(total_frames=9).validate(), "p")
+torch.cuda.synchronize()
+print("sanitize workload done")
