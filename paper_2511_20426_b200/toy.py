@@ -100,7 +100,7 @@ class ToyRuntime:
         host = [not hasattr(e.latents, "is_cuda") for e in batch]
         lat = [torch.from_numpy(np.ascontiguousarray(e.latents, dtype=np.float64)).cuda()
                if h else e.latents.to(torch.float64).contiguous() for e, h in zip(batch, host)]
-        conds = [torch.from_numpy(np.ascontiguousarray(e.conditioning.embedding)).cuda()
+        conds = [torch.from_numpy(np.array(e.conditioning.embedding, dtype=np.float64)).cuda()
                  for e in batch]
         x0s = [torch.empty((S, self.D), dtype=torch.float64, device="cuda") for _ in batch]
         ws = torch.empty(2 * len(batch) * S * self.D, dtype=torch.float64, device="cuda")
@@ -164,7 +164,7 @@ class ToySession:
 
     def set_conditioning(self, cond):
         self.cond = cond
-        self.cond_dev = self.torch.from_numpy(np.ascontiguousarray(cond.embedding)).cuda()
+        self.cond_dev = self.torch.from_numpy(np.array(cond.embedding, dtype=np.float64)).cuda()
 
     def step(self, plan, mask, pool, vis_lists, posts):
         from .engine import POST_CACHE, POST_EMIT, POST_RENOISE
