@@ -17,6 +17,7 @@
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "bc_common.h"
 #include "gemm.h"
@@ -34,15 +35,63 @@ constexpr int kChunk = 16;        // columns per TMEM load / staging round
 constexpr int kStagePitch = 20;   // floats per staged row (16 + 4 pad, 16 B aligned)
 constexpr int kEpiStageBytes = kEpiWarps * 32 * kStagePitch * 4;
 
-template <int BN>
+// CG = 1: one CTA per tile (M=128 MMA).  CG = 2: a CTA pair (cluster of 2
+// on one TPC) shares a 256 x BN tile -- tcgen05.mma.cta_group::2 with M=256,
+// each CTA holding 128 rows of A and BN/2 rows of B in its own smem and its
+// own 128 x BN accumulator in TMEM; the leader CTA issues the MMAs, both
+// CTAs' TMA loads complete on the leader's mbarrier, commits multicast to
+// both CTAs.  Halves the B traffic per CTA and the smem operand bandwidth.
+template <int BN, int CG>
 struct GemmCfg {
-  static constexpr int kStages = BN >= 256 ? 4 : (BN >= 128 ? 6 : 8);
   static constexpr int kABytes = BM * BK * 2;
-  static constexpr int kBBytes = BN * BK * 2;
+  static constexpr int kBBytes = (BN / CG) * BK * 2;
   static constexpr int kStageBytes = kABytes + kBBytes;
+  static constexpr int kStages = (192 * 1024) / kStageBytes > 8 ? 8 : (192 * 1024) / kStageBytes;
   static constexpr int kTmemCols = 2 * BN >= 32 ? 2 * BN : 32;
   static constexpr size_t kSmem = 1024 /*align slack*/ + (size_t)kStages * kStageBytes + 256 + kEpiStageBytes;
 };
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// shared::cluster address of the same variable in CTA `rank` of the cluster
+__device__ __forceinline__ uint32_t map_rank(const void* p, uint32_t rank) {
+  uint32_t out;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(out) : "r"(smem_u32(p)), "r"(rank));
+  return out;
+}
+__device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+__device__ __forceinline__ void tma_load_2d_pair(void* dst, const CUtensorMap* map, uint32_t leader_bar, int32_t c0,
+                                                 int32_t c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(leader_bar), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ void mma_bf16_ss_pair(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                                                 uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void mma_commit_pair(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"((uint16_t)0x3)
+      : "memory");
+}
 
 // Grouped rasterisation: tiles run in bands of kGroupM M-tiles with N
 // fastest inside a band, so the ~148 concurrent tiles cover a compact
@@ -64,13 +113,14 @@ __device__ __forceinline__ float gelu_tanh(float x) {
   return 0.5f * x * (1.0f + tanhf(k0 * (x + k1 * x * x * x)));
 }
 
-template <int BN, int MODE>
+template <int BN, int MODE, int CG>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                 void* __restrict__ c_ptr, int M, int N, int K, const float* __restrict__ bias,
                 const float* __restrict__ gate, int gate_stride, int rows_per_gate) {
-  using Cfg = GemmCfg<BN>;
+  using Cfg = GemmCfg<BN, CG>;
   constexpr int S = Cfg::kStages;
+  constexpr int TM = BM * CG;  // rows per (cluster) tile
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sa = smem;
@@ -83,7 +133,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const uint32_t warp = warp_id();
-  const int num_m = (M + BM - 1) / BM;
+  const uint32_t rank = CG == 2 ? cluster_rank() : 0u;
+  const bool leader = rank == 0;
+  const int unit = CG == 2 ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;  // cluster index
+  const int n_units = CG == 2 ? (int)(gridDim.x >> 1) : (int)gridDim.x;
+  const int num_m = (M + TM - 1) / TM;
   const int num_n = N / BN;
   const int num_tiles = num_m * num_n;
   const int num_kb = K / BK;
@@ -92,18 +146,27 @@ __global__ void __launch_bounds__(kThreads, 1)
     tma_prefetch(&map_a);
     tma_prefetch(&map_b);
     for (int i = 0; i < S; ++i) {
-      mbar_init(&full[i], 1);
+      mbar_init(&full[i], CG);  // CG producer arrivals (+ tx bytes of both CTAs)
       mbar_init(&empty[i], 1);
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
-      mbar_init(&tempty[i], 32 * kEpiWarps);
+      mbar_init(&tempty[i], CG == 2 ? CG * kEpiWarps : 32 * kEpiWarps);
     }
     fence_barrier_init();
   }
-  if (warp == 1) tmem_alloc<Cfg::kTmemCols>(tmem_slot);
+  if (warp == 1) {
+    if (CG == 2) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                   "n"(Cfg::kTmemCols)
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+    } else {
+      tmem_alloc<Cfg::kTmemCols>(tmem_slot);
+    }
+  }
   tc_fence_before();
-  __syncthreads();
+  if (CG == 2) cluster_sync_all(); else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
@@ -111,15 +174,23 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane_id() == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+      for (int tile = unit; tile < num_tiles; tile += n_units) {
         int mb, nb;
         tile_coords(tile, num_m, num_n, mb, nb);
-        const int m0 = mb * BM, n0 = nb * BN;
+        const int m0 = mb * TM + (int)rank * BM, n0 = nb * BN + (int)rank * (BN / CG);
         for (int kb = 0; kb < num_kb; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
-          mbar_arrive_expect_tx(&full[stage], Cfg::kStageBytes);
-          tma_load_2d(sa + stage * Cfg::kABytes, &map_a, &full[stage], kb * BK, m0);
-          tma_load_2d(sb + stage * Cfg::kBBytes, &map_b, &full[stage], kb * BK, n0);
+          if (CG == 2) {
+            const uint32_t lb = map_rank(&full[stage], 0);
+            if (leader) mbar_arrive_expect_tx(&full[stage], CG * Cfg::kStageBytes);
+            else mbar_arrive_remote(lb);
+            tma_load_2d_pair(sa + stage * Cfg::kABytes, &map_a, lb, kb * BK, m0);
+            tma_load_2d_pair(sb + stage * Cfg::kBBytes, &map_b, lb, kb * BK, n0);
+          } else {
+            mbar_arrive_expect_tx(&full[stage], Cfg::kStageBytes);
+            tma_load_2d(sa + stage * Cfg::kABytes, &map_a, &full[stage], kb * BK, m0);
+            tma_load_2d(sb + stage * Cfg::kBBytes, &map_b, &full[stage], kb * BK, n0);
+          }
           if (++stage == S) {
             stage = 0;
             phase ^= 1;
@@ -128,11 +199,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp == 1) {
-    constexpr uint32_t idesc = idesc_bf16(BM, BN);
+    if (CG == 2 && !leader) goto teardown;  // the leader issues the pair's MMAs
+    constexpr uint32_t idesc = idesc_bf16(TM, BN);
     int stage = 0;
     uint32_t phase = 0;
     int it = 0;
-    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
+    for (int tile = unit; tile < num_tiles; tile += n_units, ++it) {
       const int acc = it & 1;
       const uint32_t acc_phase = (it >> 1) & 1;
       mbar_wait(&tempty[acc], acc_phase ^ 1);
@@ -148,10 +220,16 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int k = 0; k < BK / 16; ++k) {
             const uint64_t ad = desc_sw128(a0 + k * 32, 16, 1024);
             const uint64_t bd = desc_sw128(b0 + k * 32, 16, 1024);
-            mma_bf16_ss(d_tmem, ad, bd, idesc, (kb | k) != 0);
+            if (CG == 2) mma_bf16_ss_pair(d_tmem, ad, bd, idesc, (kb | k) != 0);
+            else mma_bf16_ss(d_tmem, ad, bd, idesc, (kb | k) != 0);
           }
-          mma_commit(&empty[stage]);
-          if (kb == num_kb - 1) mma_commit(&tfull[acc]);
+          if (CG == 2) {
+            mma_commit_pair(&empty[stage]);
+            if (kb == num_kb - 1) mma_commit_pair(&tfull[acc]);
+          } else {
+            mma_commit(&empty[stage]);
+            if (kb == num_kb - 1) mma_commit(&tfull[acc]);
+          }
         }
         __syncwarp();
         if (++stage == S) {
@@ -174,12 +252,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int sub_row = lane_id() >> 2;        // 0..7
     const int sub_col = (lane_id() & 3) * 4;   // 0..12
     int it = 0;
-    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
+    for (int tile = unit; tile < num_tiles; tile += n_units, ++it) {
       const int acc = it & 1;
       const uint32_t acc_phase = (it >> 1) & 1;
       int mb, nb;
       tile_coords(tile, num_m, num_n, mb, nb);
-      const int m0 = mb * BM, n0 = nb * BN;
+      const int m0 = mb * TM + (int)rank * BM, n0 = nb * BN;
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const int row_base = m0 + (int)quad * 32;
@@ -255,11 +333,24 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
       tc_fence_before();
-      mbar_arrive(&tempty[acc]);
+      if (CG == 2) {
+        __syncwarp();
+        if (lane_id() == 0) mbar_arrive_remote(map_rank(&tempty[acc], 0));  // leader's barrier
+      } else {
+        mbar_arrive(&tempty[acc]);
+      }
     }
   }
-  __syncthreads();
-  if (warp == 1) tmem_dealloc<Cfg::kTmemCols>(tmem_base);
+teardown:
+  tc_fence_before();
+  if (CG == 2) cluster_sync_all(); else __syncthreads();
+  if (warp == 1) {
+    if (CG == 2)
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "n"(Cfg::kTmemCols)
+                   : "memory");
+    else
+      tmem_dealloc<Cfg::kTmemCols>(tmem_base);
+  }
 }
 
 // ---------------------------------------------------------------- host side
@@ -286,33 +377,46 @@ int sm_count() {
   return n;
 }
 
-template <int BN, int MODE>
+template <int BN, int MODE, int CG>
 int launch(const CUtensorMap& ma, const CUtensorMap& mb, void* C, int M, int N, int K,
            const float* bias, const float* gate, int gate_stride, int rows_per_gate,
            cudaStream_t st) {
-  using Cfg = GemmCfg<BN>;
+  using Cfg = GemmCfg<BN, CG>;
   static bool attr = false;
   if (!attr) {
-    BC_CUDA(cudaFuncSetAttribute(gemm_kernel<BN, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    BC_CUDA(cudaFuncSetAttribute(gemm_kernel<BN, MODE, CG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)Cfg::kSmem));
     attr = true;
   }
-  const int tiles = ((M + BM - 1) / BM) * (N / BN);
-  const int grid = tiles < sm_count() ? tiles : sm_count();
-  gemm_kernel<BN, MODE><<<grid, kThreads, Cfg::kSmem, st>>>(ma, mb, C, M, N, K, bias, gate,
-                                                             gate_stride, rows_per_gate);
+  const int tiles = ((M + BM * CG - 1) / (BM * CG)) * (N / BN);
+  const int units = sm_count() / CG;
+  const int grid = (tiles < units ? tiles : units) * CG;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = Cfg::kSmem;
+  cfg.stream = st;
+  cudaLaunchAttribute attrs[1];
+  attrs[0].id = cudaLaunchAttributeClusterDimension;
+  attrs[0].val.clusterDim.x = CG;
+  attrs[0].val.clusterDim.y = 1;
+  attrs[0].val.clusterDim.z = 1;
+  cfg.attrs = attrs;
+  cfg.numAttrs = 1;
+  BC_CUDA(cudaLaunchKernelEx(&cfg, gemm_kernel<BN, MODE, CG>, ma, mb, C, M, N, K, bias, gate, gate_stride,
+                             rows_per_gate));
   BC_LAUNCHED();
   return BC_OK;
 }
 
-template <int BN>
+template <int BN, int CG>
 int dispatch_mode(int mode, const CUtensorMap& ma, const CUtensorMap& mb, void* C, int M, int N,
                   int K, const float* bias, const float* gate, int gs, int rpg, cudaStream_t st) {
   switch (mode) {
-    case kEpiStoreBf16: return launch<BN, kEpiStoreBf16>(ma, mb, C, M, N, K, bias, gate, gs, rpg, st);
-    case kEpiGeluBf16: return launch<BN, kEpiGeluBf16>(ma, mb, C, M, N, K, bias, gate, gs, rpg, st);
-    case kEpiStoreF32: return launch<BN, kEpiStoreF32>(ma, mb, C, M, N, K, bias, gate, gs, rpg, st);
-    case kEpiResidualF32: return launch<BN, kEpiResidualF32>(ma, mb, C, M, N, K, bias, gate, gs, rpg, st);
+    case kEpiStoreBf16: return launch<BN, kEpiStoreBf16, CG>(ma, mb, C, M, N, K, bias, gate, gs, rpg, st);
+    case kEpiGeluBf16: return launch<BN, kEpiGeluBf16, CG>(ma, mb, C, M, N, K, bias, gate, gs, rpg, st);
+    case kEpiStoreF32: return launch<BN, kEpiStoreF32, CG>(ma, mb, C, M, N, K, bias, gate, gs, rpg, st);
+    case kEpiResidualF32: return launch<BN, kEpiResidualF32, CG>(ma, mb, C, M, N, K, bias, gate, gs, rpg, st);
   }
   return bc_fail(BC_ERR_CONTRACT, "gemm: unknown epilogue mode %d", mode);
 }
@@ -350,15 +454,27 @@ int gemm_run(const GemmArgs& g, cudaStream_t st) {
   if (g.K % BK || g.N % 64 || g.M < 1)
     return bc_fail(BC_ERR_CONTRACT, "gemm: need K %% 64 == 0, N %% 64 == 0 (M=%d N=%d K=%d)", g.M, g.N, g.K);
   const int bn = g.bn ? g.bn : gemm_plan_bn(g.M, g.N);
+  // CTA pairs for wide tiles when they still fill the machine (tuning knob
+  // BC_GEMM_PAIR=0/1 overrides)
+  static int pair_env = -2;
+  if (pair_env == -2) {
+    const char* e = getenv("BC_GEMM_PAIR");
+    pair_env = e ? atoi(e) : -1;
+  }
+  const int pair_tiles = ((g.M + 2 * BM - 1) / (2 * BM)) * (g.N / (bn ? bn : 1));
+  const bool pair = bn == 256 && g.cg != 1 && (g.cg == 2 || (pair_env >= 0 ? pair_env == 1 : pair_tiles >= sm_count() / 2));
+  const int cg = pair ? 2 : 1;
   CUtensorMap ma, mb;
   int rc = make_tmap_2d(&ma, g.A, g.K, g.M, (uint64_t)g.K * 2, BK, BM);
   if (rc) return rc;
-  rc = make_tmap_2d(&mb, g.B, g.K, g.N, (uint64_t)g.K * 2, BK, bn);
+  rc = make_tmap_2d(&mb, g.B, g.K, g.N, (uint64_t)g.K * 2, BK, bn / cg);
   if (rc) return rc;
+  if (cg == 2)
+    return dispatch_mode<256, 2>(g.mode, ma, mb, g.C, g.M, g.N, g.K, g.bias, g.gate, g.gate_stride, g.rows_per_gate, st);
   switch (bn) {
-    case 256: return dispatch_mode<256>(g.mode, ma, mb, g.C, g.M, g.N, g.K, g.bias, g.gate, g.gate_stride, g.rows_per_gate, st);
-    case 128: return dispatch_mode<128>(g.mode, ma, mb, g.C, g.M, g.N, g.K, g.bias, g.gate, g.gate_stride, g.rows_per_gate, st);
-    case 64: return dispatch_mode<64>(g.mode, ma, mb, g.C, g.M, g.N, g.K, g.bias, g.gate, g.gate_stride, g.rows_per_gate, st);
+    case 256: return dispatch_mode<256, 1>(g.mode, ma, mb, g.C, g.M, g.N, g.K, g.bias, g.gate, g.gate_stride, g.rows_per_gate, st);
+    case 128: return dispatch_mode<128, 1>(g.mode, ma, mb, g.C, g.M, g.N, g.K, g.bias, g.gate, g.gate_stride, g.rows_per_gate, st);
+    case 64: return dispatch_mode<64, 1>(g.mode, ma, mb, g.C, g.M, g.N, g.K, g.bias, g.gate, g.gate_stride, g.rows_per_gate, st);
   }
   return bc_fail(BC_ERR_CONTRACT, "gemm: bad tile width %d", bn);
 }
@@ -369,7 +485,9 @@ extern "C" int bc_gemm_bf16(const void* A, const void* B, void* C, int32_t M, in
                             int32_t mode, const float* bias, const float* gate, int32_t gate_stride,
                             int32_t rows_per_gate, void* stream) {
   // mode bits 0-7: epilogue; bits 8-15: forced tile width (0 = auto)
+  // mode bits 16-17: 1 = single-CTA tiles only, 2 = CTA pairs when possible
   bc::GemmArgs g{A, B, C, M, N, K, mode & 0xff, bias, gate, gate_stride,
-                 rows_per_gate > 0 ? rows_per_gate : 1, (mode >> 8) & 0xff ? ((mode >> 8) & 0xff) * 64 : 0};
+                 rows_per_gate > 0 ? rows_per_gate : 1, (mode >> 8) & 0xff ? ((mode >> 8) & 0xff) * 64 : 0,
+                 (mode >> 16) & 3};
   return bc::gemm_run(g, (cudaStream_t)stream);
 }

@@ -24,6 +24,7 @@ struct GemmArgs {
   int gate_stride;
   int rows_per_gate;
   int bn;  // 0 = auto
+  int cg;  // 0 = auto, 1 = single CTA, 2 = CTA pair
 };
 
 int gemm_run(const GemmArgs& g, cudaStream_t st);

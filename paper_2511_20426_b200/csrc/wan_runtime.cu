@@ -129,7 +129,7 @@ int check_dims(const bc_wan_dims& dm) {
 
 int gemm(const void* A, const void* B, void* C, int M, int N, int K, int mode, const float* bias,
          const float* gate, int gate_stride, int rows_per_gate, cudaStream_t st) {
-  bc::GemmArgs g{A, B, C, M, N, K, mode, bias, gate, gate_stride, rows_per_gate, 0};
+  bc::GemmArgs g{A, B, C, M, N, K, mode, bias, gate, gate_stride, rows_per_gate, 0, 0};
   return bc::gemm_run(g, st);
 }
 

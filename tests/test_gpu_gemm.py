@@ -10,10 +10,11 @@ pytestmark = pytest.mark.gpu
 from paper_2511_20426_b200 import _native as N
 
 
-def gemm(A, B, C, mode, bias=None, gate=None, gate_stride=0, rows_per_gate=1, bn=0):
+def gemm(A, B, C, mode, bias=None, gate=None, gate_stride=0, rows_per_gate=1, bn=0, cg=0):
     M, K = A.shape
     Nn = B.shape[0]
-    N.check(N.lib().bc_gemm_bf16(N.ptr(A), N.ptr(B), N.ptr(C), M, Nn, K, mode | ((bn // 64) << 8),
+    N.check(N.lib().bc_gemm_bf16(N.ptr(A), N.ptr(B), N.ptr(C), M, Nn, K,
+                                 mode | ((bn // 64) << 8) | (cg << 16),
                                  N.ptr(bias), N.ptr(gate), gate_stride, rows_per_gate,
                                  N.stream_ptr()), "gemm")
 
@@ -27,8 +28,9 @@ SHAPES = [(128, 256, 64), (300, 128, 128), (4680, 1536, 1536), (1000, 768, 256),
 
 
 @pytest.mark.parametrize("M,Nn,K", SHAPES)
-@pytest.mark.parametrize("bn", [0, 64, 128, 256])
-def test_gemm_modes(M, Nn, K, bn):
+@pytest.mark.parametrize("bn,cg", [(0, 0), (64, 1), (128, 1), (256, 1), (256, 2)])
+def test_gemm_modes(M, Nn, K, bn, cg):
+    """cg = 2: tcgen05.mma.cta_group::2 CTA pairs (256 x 256 tiles)."""
     if bn and Nn % bn:
         pytest.skip("tile width does not divide N")
     g = torch.Generator(device="cuda").manual_seed(M * 7 + Nn + K)
@@ -37,19 +39,19 @@ def test_gemm_modes(M, Nn, K, bn):
     bias = torch.randn(Nn, device="cuda", generator=g)
     ref = A.float() @ B.float().T + bias
     C = torch.empty(M, Nn, device="cuda", dtype=torch.float32)
-    gemm(A, B, C, 2, bias, bn=bn)
+    gemm(A, B, C, 2, bias, bn=bn, cg=cg)
     assert rel(C, ref) < 1e-5
     Cb = torch.empty(M, Nn, device="cuda", dtype=torch.bfloat16)
-    gemm(A, B, Cb, 0, bias, bn=bn)
+    gemm(A, B, Cb, 0, bias, bn=bn, cg=cg)
     assert rel(Cb, ref) < 4e-3
-    gemm(A, B, Cb, 1, bias, bn=bn)
+    gemm(A, B, Cb, 1, bias, bn=bn, cg=cg)
     assert rel(Cb, torch.nn.functional.gelu(ref, approximate="tanh")) < 4e-3
     rows_per_gate = 97
     groups = (M + rows_per_gate - 1) // rows_per_gate
     gate = torch.randn(groups, Nn, device="cuda", generator=g)
     X = torch.randn(M, Nn, device="cuda", generator=g)
     want = X + gate.repeat_interleave(rows_per_gate, 0)[:M] * ref
-    gemm(A, B, X, 3, bias, gate, Nn, rows_per_gate, bn=bn)
+    gemm(A, B, X, 3, bias, gate, Nn, rows_per_gate, bn=bn, cg=cg)
     assert rel(X, want) < 1e-5
 
 
