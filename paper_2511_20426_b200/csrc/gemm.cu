@@ -98,6 +98,21 @@ __device__ __forceinline__ void mma_commit_pair(uint64_t* bar) {
 // (M x N) rectangle and both operand panels stay L2-resident (with plain
 // M-fastest order a K=8960 GEMM re-reads A once per N column).
 constexpr int kGroupM = 16;
+
+#ifdef BC_GEMM_TRACE
+// debug timeline (scripts/gemm_trace.cu): [cta 0..3][event][kb] globaltimer
+__device__ unsigned long long g_gemm_trace[4][3][256];
+__device__ __forceinline__ void gemm_trace(int ev, int kb) {
+  if (blockIdx.x < 4 && kb < 256) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_gemm_trace[blockIdx.x][ev][kb] = t;
+  }
+}
+#define GEMM_TRACE(ev, kb) gemm_trace(ev, kb)
+#else
+#define GEMM_TRACE(ev, kb)
+#endif
 __device__ __forceinline__ void tile_coords(int tile, int num_m, int num_n, int& m_blk, int& n_blk) {
   const int per_group = kGroupM * num_n;
   const int g = tile / per_group;
@@ -146,7 +161,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     tma_prefetch(&map_a);
     tma_prefetch(&map_b);
     for (int i = 0; i < S; ++i) {
-      mbar_init(&full[i], CG);  // CG producer arrivals (+ tx bytes of both CTAs)
+      mbar_init(&full[i], 1);  // the leader producer's arrival (+ tx bytes of both CTAs)
       mbar_init(&empty[i], 1);
     }
     for (int i = 0; i < 2; ++i) {
@@ -180,10 +195,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int m0 = mb * TM + (int)rank * BM, n0 = nb * BN + (int)rank * (BN / CG);
         for (int kb = 0; kb < num_kb; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
+          if (tile == unit) GEMM_TRACE(0, kb);
           if (CG == 2) {
+            // only the leader arrives (expecting both CTAs' bytes); the
+            // peer's loads just complete their tx on the leader's barrier.
+            // A remote arrive per stage costs ~0.5 us of issue latency.
             const uint32_t lb = map_rank(&full[stage], 0);
             if (leader) mbar_arrive_expect_tx(&full[stage], CG * Cfg::kStageBytes);
-            else mbar_arrive_remote(lb);
             tma_load_2d_pair(sa + stage * Cfg::kABytes, &map_a, lb, kb * BK, m0);
             tma_load_2d_pair(sb + stage * Cfg::kBBytes, &map_b, lb, kb * BK, n0);
           } else {
@@ -213,6 +231,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int kb = 0; kb < num_kb; ++kb) {
         mbar_wait(&full[stage], phase);
         tc_fence_after();
+        if (it < 2 && lane_id() == 0) GEMM_TRACE(1, kb + it * num_kb);
         if (elect_one()) {
           const uint32_t a0 = smem_u32(sa + stage * Cfg::kABytes);
           const uint32_t b0 = smem_u32(sb + stage * Cfg::kBBytes);
@@ -260,6 +279,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int m0 = mb * TM + (int)rank * BM, n0 = nb * BN;
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
+      if (ew == 0 && lane_id() == 0) GEMM_TRACE(2, it);
       const int row_base = m0 + (int)quad * 32;
 #pragma unroll 1
       for (int c = c_begin; c < c_begin + BN / 2; c += kChunk) {
@@ -389,10 +409,7 @@ int launch(const CUtensorMap& ma, const CUtensorMap& mb, void* C, int M, int N, 
     attr = true;
   }
   const int tiles = ((M + BM * CG - 1) / (BM * CG)) * (N / BN);
-  const int units = sm_count() / CG;
-  const int grid = (tiles < units ? tiles : units) * CG;
   cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = Cfg::kSmem;
   cfg.stream = st;
@@ -403,6 +420,24 @@ int launch(const CUtensorMap& ma, const CUtensorMap& mb, void* C, int M, int N, 
   attrs[0].val.clusterDim.z = 1;
   cfg.attrs = attrs;
   cfg.numAttrs = 1;
+  // A persistent grid must be fully co-resident: the tiles are pre-assigned
+  // per unit, so a unit that only starts when another finishes doubles the
+  // kernel time.  Pairs need both CTAs on one TPC, and not every TPC of the
+  // part is whole, so ask the occupancy calculator how many clusters fit.
+  static int units = 0;
+  if (!units) {
+    units = sm_count() / CG;
+    if (CG > 1) {
+      cfg.gridDim = dim3(units * CG);
+      int n = 0;
+      if (cudaOccupancyMaxActiveClusters(&n, gemm_kernel<BN, MODE, CG>, &cfg) == cudaSuccess && n > 0 &&
+          n < units)
+        units = n;
+      (void)cudaGetLastError();
+    }
+  }
+  const int grid = (tiles < units ? tiles : units) * CG;
+  cfg.gridDim = dim3(grid);
   BC_CUDA(cudaLaunchKernelEx(&cfg, gemm_kernel<BN, MODE, CG>, ma, mb, C, M, N, K, bias, gate, gate_stride,
                              rows_per_gate));
   BC_LAUNCHED();
