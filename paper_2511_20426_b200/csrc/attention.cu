@@ -53,6 +53,9 @@ constexpr int kTile = 2 * kHalf;      // 32 KB
 constexpr int kRing = 3;              // K/V ring slots
 constexpr int kThreads = 384;
 constexpr float kRescaleThresh = 8.0f;  // log2 domain
+constexpr int kRegsCtl = 56;        // 128 x 56 + 256 x 224 = 64 K registers
+constexpr int kRegsSoftmax = 224;
+constexpr int kDefaultPoly = 0;
 #ifndef BC_ATTN_PINGPONG
 #define BC_ATTN_PINGPONG 0
 #endif
@@ -78,9 +81,40 @@ __device__ __forceinline__ float ex2(float x) {
   return y;
 }
 
+// 3-input max (FMNMX3, sm_100+): halves the ALU ops of the row max
+__device__ __forceinline__ float fmax3(float a, float b, float c) {
+  float d;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+  return d;
+}
+
+// packed fp32x2 (FFMA2 / FADD2, sm_100+): half the FMA-pipe instructions
+__device__ __forceinline__ uint64_t f2(float lo, float hi) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ void f2_split(uint64_t v, float& lo, float& hi) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+}
+__device__ __forceinline__ uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ void sts128(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
+}
+
 // 2^x on the FMA pipe (Cody-Waite split + degree-3 minimax on [-0.5, 0.5],
 // max rel. error 7.7e-5 << bf16's 3.9e-3) to offload part of the MUFU work:
-// the softmax is MUFU-bound at 16 ex2/clk/SM otherwise.
+// the softmax is MUFU-bound at 16 ex2/clk/SM otherwise (measured 15.5-16 on
+// B200, scripts/mufu_probe.cu).
 __device__ __forceinline__ float ex2_poly(float x) {
   x = fmaxf(x, -126.0f);
   const float t = x + 12582912.0f;  // 1.5 * 2^23: round-to-nearest integer in the low mantissa bits
@@ -89,6 +123,25 @@ __device__ __forceinline__ float ex2_poly(float x) {
   const float p = fmaf(fmaf(fmaf(0.05508868380751114f, f, 0.24260405145947936f), f, 0.6932762416819607f), f,
                        0.9999289403695112f);
   return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
+}
+
+// the same on a pair with packed FFMA2/FADD2: ~6 FMA-pipe instructions
+// per PAIR, so a fraction of the pairs can move off the MUFU for free
+__device__ __forceinline__ void ex2_poly2(float x0, float x1, float& y0, float& y1) {
+  constexpr float kMagic = 12582912.0f;  // 1.5 * 2^23
+  const uint64_t x = f2(fmaxf(x0, -126.0f), fmaxf(x1, -126.0f));
+  const uint64_t t = fadd2(x, f2(kMagic, kMagic));
+  const uint64_t n = fadd2(t, f2(-kMagic, -kMagic));
+  const uint64_t fr = ffma2(n, f2(-1.0f, -1.0f), x);
+  uint64_t p = ffma2(f2(0.05508868380751114f, 0.05508868380751114f), fr,
+                     f2(0.24260405145947936f, 0.24260405145947936f));
+  p = ffma2(p, fr, f2(0.6932762416819607f, 0.6932762416819607f));
+  p = ffma2(p, fr, f2(0.9999289403695112f, 0.9999289403695112f));
+  float p0, p1, t0, t1;
+  f2_split(p, p0, p1);
+  f2_split(t, t0, t1);
+  y0 = __int_as_float(__float_as_int(p0) + (__float_as_int(t0) << 23));
+  y1 = __int_as_float(__float_as_int(p1) + (__float_as_int(t1) << 23));
 }
 
 // fp32 pair -> bf16x2 with round-to-nearest-even on the integer ALU
@@ -144,7 +197,7 @@ struct SoftmaxBars {
 };
 
 // One softmax warpgroup: 128 threads, thread <-> query row of its tile.
-template <int kPolyEvery>
+template <int kPoly>
 __device__ __forceinline__ void softmax_tile(const AttnParams& prm, uint32_t tmem_s, uint32_t tmem_o,
                                              uint8_t* sp, SoftmaxBars b, int n_tiles, int tiles_per_slot,
                                              uint32_t quad, int q_row0, int e, int head, int tile_x,
@@ -152,9 +205,10 @@ __device__ __forceinline__ void softmax_tile(const AttnParams& prm, uint32_t tme
   const uint32_t row = quad * 32 + lane_id();
   const uint32_t lane_base = (quad * 32) << 16;
   const float c = prm.scale * 1.4426950408889634f;
+  const uint32_t sp_u32 = smem_u32(sp);
   float m_used = -INFINITY, l_sum = 0.0f;
-  for (int j = 0; j < n_tiles; ++j) {
-    const int t0 = (j % tiles_per_slot) * kKeys;
+  int t0 = 0;  // first key of tile j within its visible block
+  for (int j = 0; j < n_tiles; ++j, t0 = (t0 + kKeys < prm.kv_tokens) ? t0 + kKeys : 0) {
     const int valid = min(kKeys, prm.kv_tokens - t0);
     mbar_wait(b.s_full, j & 1);
     if ((quad) == 0) ATRACE(0 + tile_x * 8, j);
@@ -170,14 +224,33 @@ __device__ __forceinline__ void softmax_tile(const AttnParams& prm, uint32_t tme
     }
     tc_fence_before();
     mbar_arrive(b.s_empty);  // S buffer may now be overwritten by the next QK^T
+    if (quad == 0) ATRACE(4 + tile_x * 8, j);
+#ifdef BC_ATTN_NOSOFTMAX  // timing experiment only: MMA/TMA skeleton
+    if (j > 0) mbar_wait(b.o_ready, (j - 1) & 1);
+    if (s[5] == 1234.5f) l_sum += 1.0f;
+    fence_async_shared();
+    tc_fence_before();
+    mbar_arrive(b.p_full);
+    continue;
+#endif
     if (valid < kKeys) {     // ragged last tile of a slot (warp-uniform)
 #pragma unroll
       for (int i = 0; i < 128; ++i)
         if (i >= valid) s[i] = -INFINITY;
     }
-    float mx = s[0];
+    // row max as 8 independent FMNMX3 chains (a single fmaxf chain is a
+    // 128-deep dependency: ~500 cycles of latency on the softmax critical path)
+    float m8[8];
 #pragma unroll
-    for (int i = 1; i < 128; ++i) mx = fmaxf(mx, s[i]);
+    for (int k = 0; k < 8; ++k) m8[k] = fmax3(s[k], s[8 + k], s[16 + k]);
+#pragma unroll
+    for (int i = 24; i < 120; i += 16) {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) m8[k] = fmax3(m8[k], s[i + k], s[i + 8 + k]);
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) m8[k] = fmaxf(m8[k], s[120 + k]);
+    const float mx = fmax3(fmax3(m8[0], m8[1], m8[2]), fmax3(m8[3], m8[4], m8[5]), fmaxf(m8[6], m8[7]));
     const float mt = mx * c;
     float alpha = 1.0f;
     const bool bump = (j == 0) || (mt > m_used + kRescaleThresh);
@@ -187,8 +260,8 @@ __device__ __forceinline__ void softmax_tile(const AttnParams& prm, uint32_t tme
       m_used = m_new;
     }
     // P = 2^(s*c - m) -> packed bf16 in registers (s dies as P is formed)
-    float tsum = 0.0f;
-    const float neg_m = -m_used;
+    uint64_t sum2[2] = {0ull, 0ull};  // (+0.0f, +0.0f) pairs
+    const uint64_t c2 = f2(c, c), nm2 = f2(-m_used, -m_used);
     uint32_t pk[64];
     // MUFU ping-pong: the two softmax warpgroups take turns on the
     // exponential phase (named barriers 1 = A->B, 2 = B->A), so one
@@ -203,28 +276,31 @@ __device__ __forceinline__ void softmax_tile(const AttnParams& prm, uint32_t tme
       // full tile: every 4th pair of exponentials on the FMA pipe
 #pragma unroll
       for (int t = 0; t < 64; ++t) {
-        float p0, p1;
-        if (kPolyEvery > 0 && (t % kPolyEvery) == kPolyEvery - 1) {
-          p0 = ex2_poly(fmaf(s[2 * t], c, neg_m));
-          p1 = ex2_poly(fmaf(s[2 * t + 1], c, neg_m));
+        float x0, x1, p0, p1;
+        f2_split(ffma2(f2(s[2 * t], s[2 * t + 1]), c2, nm2), x0, x1);
+        if (((t * kPoly) & 7) < kPoly) {  // kPoly of every 8 pairs, spread out
+          ex2_poly2(x0, x1, p0, p1);
         } else {
-          p0 = ex2(fmaf(s[2 * t], c, neg_m));
-          p1 = ex2(fmaf(s[2 * t + 1], c, neg_m));
+          p0 = ex2(x0);
+          p1 = ex2(x1);
         }
-        tsum += p0 + p1;
+        const uint64_t pp = f2(p0, p1);
+        sum2[t & 1] = fadd2(sum2[t & 1], pp);
         pk[t] = kAluPack ? pack_bf16_alu(p0, p1) : pack_bf16(p0, p1);
       }
     } else {
 #pragma unroll
       for (int t = 0; t < 64; ++t) {
-        const float p0 = ex2(fmaf(s[2 * t], c, neg_m));
-        const float p1 = ex2(fmaf(s[2 * t + 1], c, neg_m));
-        tsum += p0 + p1;
+        float x0, x1;
+        f2_split(ffma2(f2(s[2 * t], s[2 * t + 1]), c2, nm2), x0, x1);
+        const float p0 = ex2(x0);
+        const float p1 = ex2(x1);
+        sum2[t & 1] = fadd2(sum2[t & 1], f2(p0, p1));
         pk[t] = kAluPack ? pack_bf16_alu(p0, p1) : pack_bf16(p0, p1);
       }
     }
+    if (quad == 0) ATRACE(2 + tile_x * 8, j);
     if (pingpong) {
-      if (quad == 0) ATRACE(2 + tile_x * 8, j);
       if (tile_x == 0) asm volatile("bar.arrive 1, 256;" ::: "memory");
       if (tile_x == 1 && j + 1 < n_tiles) asm volatile("bar.arrive 2, 256;" ::: "memory");
     }
@@ -232,6 +308,7 @@ __device__ __forceinline__ void softmax_tile(const AttnParams& prm, uint32_t tme
     if (j > 0) {
       mbar_wait(b.o_ready, (j - 1) & 1);
       tc_fence_after();
+      if (quad == 0) ATRACE(5 + tile_x * 8, j);
       if (__any_sync(0xffffffffu, bump)) {
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
@@ -247,13 +324,20 @@ __device__ __forceinline__ void softmax_tile(const AttnParams& prm, uint32_t tme
     }
     // P -> smem in the UMMA K-major SW128 layout: half h holds keys
     // [64h, 64h+64); 16-byte chunk q of row r sits at chunk (q ^ (r & 7)).
+#ifndef BC_ATTN_NOPSTORE  // timing experiment only: skip the P stores
 #pragma unroll
     for (int q = 0; q < 16; ++q) {
+#else
+    for (int q = 0; q < 16; ++q) if (pk[4 * q] == 0x12345678u) {
+#endif
       const int half = q >> 3, ch = q & 7;
-      *reinterpret_cast<uint4*>(sp + half * kHalf + row * 128 + ((ch ^ (row & 7)) << 4)) =
-          make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
+      sts128(sp_u32 + half * kHalf + row * 128 + ((ch ^ (row & 7)) << 4), pk[4 * q], pk[4 * q + 1], pk[4 * q + 2],
+             pk[4 * q + 3]);
     }
-    l_sum = l_sum * alpha + tsum;
+    float sa, sb, sc, sd;
+    f2_split(sum2[0], sa, sb);
+    f2_split(sum2[1], sc, sd);
+    l_sum = l_sum * alpha + ((sa + sc) + (sb + sd));
     fence_async_shared();
     tc_fence_before();
     mbar_arrive(b.p_full);
@@ -289,7 +373,7 @@ __device__ __forceinline__ void softmax_tile(const AttnParams& prm, uint32_t tme
   }
 }
 
-template <int kPolyEvery>
+template <int kPoly>
 __global__ void __launch_bounds__(kThreads, 1)
     attn_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_kv,
                 AttnParams prm) {
@@ -337,6 +421,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
+  // register split (setmaxnreg, per warpgroup, inside each role's branch so
+  // the allocator sees disjoint regions): the TMA/MMA warpgroup needs few
+  // registers, the softmax warpgroups hold a 128-float score row + 64 packed
+  // P words per thread
+  if (warp < 4) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegsCtl));
   if (warp == 0) {
     if (lane_id() == 0) {
       const int qrow = e * prm.q_tokens + q0;
@@ -435,25 +524,31 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbar_wait(&s_empty[x], j & 1);  // softmax x has read S_x(j)
           ATRACE(16 + x * 4, j);
           if (x == 0) ring_wait(kpos(j + 1));
+          if (x == 0) ATRACE(24, j);
           tc_fence_after();
           issue_qk(x, j + 1);
           ATRACE(17 + x * 4, j);
+          // K_{j+1} is free once the last tile's QK^T on it completes:
+          // release it now (not after PV_B(j)) so the TMA refills its ring
+          // slot (with V_{j+1}) one MMA group earlier
+          if (x == n_q - 1) release(kpos(j + 1));
         }
         mbar_wait(&p_full[x], j & 1);
         ATRACE(18 + x * 4, j);
         if (x == 0) ring_wait(vpos(j, n_tiles));
+        if (x == 0) ATRACE(25, j);
         tc_fence_after();
         issue_pv(x, j);
         ATRACE(19 + x * 4, j);
       }
-      if (next) release(kpos(j + 1));
       release(vpos(j, n_tiles));
     }
   } else if (warp >= 4) {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegsSoftmax));
     const int x = (warp >= 8) ? 1 : 0;
     if (x == 0 || has_b) {
       SoftmaxBars b{&s_full[x], &s_empty[x], &p_full[x], &o_ready[x]};
-      softmax_tile<kPolyEvery>(prm, tmem + x * 128, tmem + 256 + x * 128, smem + (x ? Smem::pb : Smem::pa), b, n_tiles,
+      softmax_tile<kPoly>(prm, tmem + x * 128, tmem + 256 + x * 128, smem + (x ? Smem::pb : Smem::pa), b, n_tiles,
                    tiles_per_slot, warp & 3, q0 + x * kRows, e, head, x, has_b && kPingPong);
     }
   }
@@ -539,18 +634,23 @@ int attention_run(const AttnArgs& a, cudaStream_t st) {
 #endif
   static int poly = -1;
   if (poly < 0) {
-    const char* env = getenv("BC_ATTN_POLY");  // tuning knob: 0 = all MUFU
-    poly = env ? atoi(env) : 0;
+    // tuning knob: pairs of exponentials (of every 8) evaluated by the FMA-pipe
+    // polynomial instead of MUFU.EX2
+    const char* env = getenv("BC_ATTN_POLY");
+    poly = env ? atoi(env) : kDefaultPoly;
+    if (poly != 0 && poly != 2 && poly != 3 && poly != 4) poly = kDefaultPoly;
     BC_CUDA(cudaFuncSetAttribute(attn_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, Smem::total + 1024));
-    BC_CUDA(cudaFuncSetAttribute(attn_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, Smem::total + 1024));
-    BC_CUDA(cudaFuncSetAttribute(attn_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, Smem::total + 1024));
+    BC_CUDA(cudaFuncSetAttribute(attn_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, Smem::total + 1024));
     BC_CUDA(cudaFuncSetAttribute(attn_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, Smem::total + 1024));
+    BC_CUDA(cudaFuncSetAttribute(attn_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, Smem::total + 1024));
   }
   dim3 grid((a.q_tokens + 2 * kRows - 1) / (2 * kRows), a.n_entries, a.heads);
-  if (poly == 0) attn_kernel<0><<<grid, kThreads, Smem::total + 1024, st>>>(mq, mkv, p);
-  else if (poly == 3) attn_kernel<3><<<grid, kThreads, Smem::total + 1024, st>>>(mq, mkv, p);
-  else if (poly == 8) attn_kernel<8><<<grid, kThreads, Smem::total + 1024, st>>>(mq, mkv, p);
-  else attn_kernel<4><<<grid, kThreads, Smem::total + 1024, st>>>(mq, mkv, p);
+  switch (poly) {
+    case 2: attn_kernel<2><<<grid, kThreads, Smem::total + 1024, st>>>(mq, mkv, p); break;
+    case 3: attn_kernel<3><<<grid, kThreads, Smem::total + 1024, st>>>(mq, mkv, p); break;
+    case 4: attn_kernel<4><<<grid, kThreads, Smem::total + 1024, st>>>(mq, mkv, p); break;
+    default: attn_kernel<0><<<grid, kThreads, Smem::total + 1024, st>>>(mq, mkv, p);
+  }
   BC_LAUNCHED();
   return BC_OK;
 }

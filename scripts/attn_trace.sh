@@ -5,7 +5,7 @@ set -e
 cd "$(dirname "$0")/../paper_2511_20426_b200/csrc"
 OUT=/tmp/bc_trace; mkdir -p $OUT
 NV="nvcc -O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a -Xcompiler -fPIC --expt-relaxed-constexpr"
-for f in *.cu; do $NV -DBC_ATTN_TRACE -c $f -o $OUT/${f%.cu}.o; done
+for f in *.cu; do $NV -DBC_ATTN_TRACE ${EXTRA:-} -c $f -o $OUT/${f%.cu}.o; done
 for f in *.cpp; do g++ -O3 -std=c++17 -fPIC -c $f -o $OUT/${f%.cpp}.o; done
 NPR=$(python -c "import numpy,os;print(os.path.join(os.path.dirname(numpy.__file__),'random','lib'))")
 nvcc -gencode arch=compute_100a,code=sm_100a -shared -o $OUT/libbcb200.so $OUT/*.o -L$NPR -lnpyrandom -lm -lpthread
@@ -30,9 +30,9 @@ lib = ctypes.CDLL(N.LIB_PATH)
 lib.bc_attn_trace_read(buf)
 t = np.array(buf, dtype=np.int64).reshape(32, 64)
 t0 = t[t > 0].min()
-names = {0: "A s_full", 1: "A token", 2: "A exp done", 3: "A p_full", 8: "B s_full", 9: "B token", 10: "B exp done",
-         11: "B p_full", 16: "M s_emptyA", 17: "M QK_A", 18: "M p_fullA", 19: "M PV_A", 20: "M s_emptyB",
-         21: "M QK_B", 22: "M p_fullB", 23: "M PV_B"}
+names = {0: "A s_full", 4: "A s_read", 1: "A max", 2: "A exp", 5: "A o_rdy", 3: "A p_full",
+         8: "B s_full", 12: "B s_read", 9: "B max", 10: "B exp", 13: "B o_rdy", 11: "B p_full", 16: "M s_emptyA", 17: "M QK_A", 18: "M p_fullA", 19: "M PV_A", 20: "M s_emptyB",
+         21: "M QK_B", 22: "M p_fullB", 23: "M PV_B", 24: "M K_rdy", 25: "M V_rdy"}
 for j in range(20, 28):
     row = {names[k]: int(t[k, j] - t0) for k in names if t[k, j] > 0}
     print(j, sorted(row.items(), key=lambda kv: kv[1]))
