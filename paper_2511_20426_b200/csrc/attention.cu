@@ -53,8 +53,14 @@ constexpr int kTile = 2 * kHalf;      // 32 KB
 constexpr int kRing = 3;              // K/V ring slots
 constexpr int kThreads = 384;
 constexpr float kRescaleThresh = 8.0f;  // log2 domain
-constexpr int kRegsCtl = 56;        // 128 x 56 + 256 x 224 = 64 K registers
+// setmaxnreg only moves registers inside the CTA's launch allocation
+// (384 x 168): the softmax warps' increase must be covered by what the
+// control warpgroup releases (128 x (168 - 56) = 256 x (224 - 168)), or the
+// increasing warps block forever
+constexpr int kRegsLaunch = 168;
+constexpr int kRegsCtl = 56;
 constexpr int kRegsSoftmax = 224;
+static_assert(128 * (kRegsLaunch - kRegsCtl) >= 256 * (kRegsSoftmax - kRegsLaunch), "register split");
 constexpr int kDefaultPoly = 0;
 #ifndef BC_ATTN_PINGPONG
 #define BC_ATTN_PINGPONG 0
@@ -643,6 +649,10 @@ int attention_run(const AttnArgs& a, cudaStream_t st) {
     BC_CUDA(cudaFuncSetAttribute(attn_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, Smem::total + 1024));
     BC_CUDA(cudaFuncSetAttribute(attn_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, Smem::total + 1024));
     BC_CUDA(cudaFuncSetAttribute(attn_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, Smem::total + 1024));
+    cudaFuncAttributes fa;
+    BC_CUDA(cudaFuncGetAttributes(&fa, attn_kernel<0>));
+    if (fa.numRegs != kRegsLaunch)  // the setmaxnreg split assumes this allocation (else: deadlock)
+      return bc_fail(BC_ERR_CUDA, "attention kernel built with %d registers, expected %d", fa.numRegs, kRegsLaunch);
   }
   dim3 grid((a.q_tokens + 2 * kRows - 1) / (2 * kRows), a.n_entries, a.heads);
   switch (poly) {

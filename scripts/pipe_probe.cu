@@ -22,6 +22,9 @@ __global__ void k(float* out, int iters, long long* cyc) {
       if (OP == 3) asm volatile("max.f32 %0, %0, %1, %2;" : "+f"(v[i]) : "f"(v[i + 8]), "f"(v[(i + 1) & 15]));  // FMNMX3
       if (OP == 4) { __nv_bfloat162 p = __floats2bfloat162_rn(v[i], v[i + 8]); u[i] += *reinterpret_cast<uint32_t*>(&p); v[i] += 1e-7f; }  // F2FP (+FADD)
       if (OP == 5) { float y; asm volatile("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(v[i])); v[i] = y * 0.5f; }  // MUFU (+FMUL)
+      if (OP == 7) { uint32_t y; asm volatile("ex2.approx.f16x2 %0, %1;" : "=r"(y) : "r"(u[i])); u[i] = y ^ 0x00010001u; }  // MUFU f16x2
+      if (OP == 8) { uint32_t y; asm volatile("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(y) : "f"(v[i]), "f"(v[i + 8])); u[i] += y; v[i] += 1e-7f; }  // F2FP f16
+      if (OP == 9) { asm volatile("add.rn.f16x2 %0, %0, %1;" : "+r"(u[i]) : "r"(u[(i + 1) & 7])); }  // HADD2
       if (OP == 6) { v[i] = fmaf(v[i], 0.999f, -0.001f); v[i + 8] = fmaf(v[i + 8], 0.999f, -0.001f); }  // FFMA imm
     }
   }
@@ -52,5 +55,8 @@ int main() {
   run<3>("FMNMX3", 8, out, cyc);
   run<4>("F2FP+FADD", 8, out, cyc);
   run<5>("MUFU+FMUL", 8, out, cyc);
+  run<7>("MUFU.f16x2", 8, out, cyc);
+  run<8>("F2FP.f16+FADD", 8, out, cyc);
+  run<9>("HADD2", 8, out, cyc);
   return 0;
 }
