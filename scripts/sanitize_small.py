@@ -14,6 +14,13 @@ for mode, dt in ((0, torch.bfloat16), (1, torch.bfloat16), (2, torch.float32), (
     g = torch.ones(4, 256, device="cuda")
     N.check(N.lib().bc_gemm_bf16(N.ptr(A), N.ptr(B), N.ptr(C), 300, 256, 256, mode, 0,
                                  N.ptr(g) if mode == 3 else 0, 256, 100, N.stream_ptr()), "gemm")
+# CTA-pair GEMM (cta_group::2, 256-row tiles), ragged M, all epilogues
+A2 = torch.randn(600, 256, device="cuda").bfloat16(); B2 = torch.randn(512, 256, device="cuda").bfloat16()
+for mode, dt in ((0, torch.bfloat16), (1, torch.bfloat16), (2, torch.float32), (3, torch.float32)):
+    C = torch.zeros(600, 512, device="cuda", dtype=dt)
+    g = torch.ones(6, 512, device="cuda")
+    N.check(N.lib().bc_gemm_bf16(N.ptr(A2), N.ptr(B2), N.ptr(C), 600, 512, 256, mode | (4 << 8) | (2 << 16), 0,
+                                 N.ptr(g) if mode == 3 else 0, 512, 100, N.stream_ptr()), "gemm pair")
 # attention, ragged q/kv
 T, H = 200, 2
 arena = torch.randn(4, 2, T, H * 128, device="cuda").bfloat16()
