@@ -220,13 +220,15 @@ __device__ __forceinline__ void softmax_tile(const AttnParams& prm, uint32_t tme
     if ((quad) == 0) ATRACE(0 + tile_x * 8, j);
     tc_fence_after();
     float s[128];
+    {  // all four 32-column loads in flight, one wait
+      uint32_t r[4][32];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      uint32_t r[32];
-      tmem_ld32(tmem_s + lane_base + k * 32, r);
+      for (int k = 0; k < 4; ++k) tmem_ld32(tmem_s + lane_base + k * 32, r[k]);
       tmem_ld_wait();
 #pragma unroll
-      for (int i = 0; i < 32; ++i) s[k * 32 + i] = __uint_as_float(r[i]);
+      for (int k = 0; k < 4; ++k)
+#pragma unroll
+        for (int i = 0; i < 32; ++i) s[k * 32 + i] = __uint_as_float(r[k][i]);
     }
     tc_fence_before();
     mbar_arrive(b.s_empty);  // S buffer may now be overwritten by the next QK^T
