@@ -324,8 +324,8 @@ def run_ours(args, cfg):
         "value": value, "unit": "frames/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
-        "data": "synthetic (random-init Wan2.1-1.3B-shaped weights, counter-keyed N(0,1) noise, "
-                "hash-expanded 512x4096 text states)",
+        "data": f"synthetic (random-init Wan2.1-{args.preset.upper()}-shaped weights, counter-keyed N(0,1) "
+                "noise, hash-expanded 512x4096 text states)",
         "config": workload_config(args, cfg, f"temporal{world}"),
         "streaming_fps": stream_fps,
         "sequential": {"e2e_fps": seq_e2e, "streaming_fps": seq_stream},
