@@ -62,14 +62,6 @@ constexpr int kRegsCtl = 56;
 constexpr int kRegsSoftmax = 224;
 static_assert(128 * (kRegsLaunch - kRegsCtl) >= 256 * (kRegsSoftmax - kRegsLaunch), "register split");
 constexpr int kDefaultPoly = 0;
-#ifndef BC_ATTN_PINGPONG
-#define BC_ATTN_PINGPONG 0
-#endif
-constexpr bool kPingPong = BC_ATTN_PINGPONG != 0;
-#ifndef BC_ATTN_ALU_PACK
-#define BC_ATTN_ALU_PACK 0
-#endif
-constexpr bool kAluPack = BC_ATTN_ALU_PACK != 0;
 
 struct Smem {
   static constexpr int qa = 0;
@@ -117,22 +109,11 @@ __device__ __forceinline__ void sts128(uint32_t addr, uint32_t a, uint32_t b, ui
   asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
 }
 
-// 2^x on the FMA pipe (Cody-Waite split + degree-3 minimax on [-0.5, 0.5],
-// max rel. error 7.7e-5 << bf16's 3.9e-3) to offload part of the MUFU work:
-// the softmax is MUFU-bound at 16 ex2/clk/SM otherwise (measured 15.5-16 on
-// B200, scripts/mufu_probe.cu).
-__device__ __forceinline__ float ex2_poly(float x) {
-  x = fmaxf(x, -126.0f);
-  const float t = x + 12582912.0f;  // 1.5 * 2^23: round-to-nearest integer in the low mantissa bits
-  const float n = t - 12582912.0f;
-  const float f = x - n;
-  const float p = fmaf(fmaf(fmaf(0.05508868380751114f, f, 0.24260405145947936f), f, 0.6932762416819607f), f,
-                       0.9999289403695112f);
-  return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
-}
-
-// the same on a pair with packed FFMA2/FADD2: ~6 FMA-pipe instructions
-// per PAIR, so a fraction of the pairs can move off the MUFU for free
+// 2^x for a pair on the FMA pipe (Cody-Waite split + degree-3 minimax on
+// [-0.5, 0.5], max rel. error 7.7e-5 << bf16's 3.9e-3; packed FFMA2/FADD2,
+// ~6 FMA-pipe instructions per pair) to offload part of the MUFU work, which
+// is 16 ex2/clk/SM (measured, scripts/mufu_probe.cu).  Off by default
+// (BC_ATTN_POLY): measured no faster, see profiles/README.md.
 __device__ __forceinline__ void ex2_poly2(float x0, float x1, float& y0, float& y1) {
   constexpr float kMagic = 12582912.0f;  // 1.5 * 2^23
   const uint64_t x = f2(fmaxf(x0, -126.0f), fmaxf(x1, -126.0f));
@@ -148,16 +129,6 @@ __device__ __forceinline__ void ex2_poly2(float x0, float x1, float& y0, float& 
   f2_split(t, t0, t1);
   y0 = __int_as_float(__float_as_int(p0) + (__float_as_int(t0) << 23));
   y1 = __int_as_float(__float_as_int(p1) + (__float_as_int(t1) << 23));
-}
-
-// fp32 pair -> bf16x2 with round-to-nearest-even on the integer ALU
-// (inputs are finite and >= 0), keeping F2FP off the MUFU/XU pipe that the
-// exponentials saturate.
-__device__ __forceinline__ uint32_t pack_bf16_alu(float a, float b) {
-  uint32_t ua = __float_as_uint(a), ub = __float_as_uint(b);
-  ua += 0x7FFFu + ((ua >> 16) & 1u);
-  ub += 0x7FFFu + ((ub >> 16) & 1u);
-  return __byte_perm(ua, ub, 0x7632);
 }
 
 // Diagnostic timeline (BC_ATTN_TRACE builds only): CTA (0,0,0) records
@@ -206,8 +177,7 @@ struct SoftmaxBars {
 template <int kPoly>
 __device__ __forceinline__ void softmax_tile(const AttnParams& prm, uint32_t tmem_s, uint32_t tmem_o,
                                              uint8_t* sp, SoftmaxBars b, int n_tiles, int tiles_per_slot,
-                                             uint32_t quad, int q_row0, int e, int head, int tile_x,
-                                             bool pingpong) {
+                                             uint32_t quad, int q_row0, int e, int head, int tile_x) {
   const uint32_t row = quad * 32 + lane_id();
   const uint32_t lane_base = (quad * 32) << 16;
   const float c = prm.scale * 1.4426950408889634f;
@@ -271,17 +241,8 @@ __device__ __forceinline__ void softmax_tile(const AttnParams& prm, uint32_t tme
     uint64_t sum2[2] = {0ull, 0ull};  // (+0.0f, +0.0f) pairs
     const uint64_t c2 = f2(c, c), nm2 = f2(-m_used, -m_used);
     uint32_t pk[64];
-    // MUFU ping-pong: the two softmax warpgroups take turns on the
-    // exponential phase (named barriers 1 = A->B, 2 = B->A), so one
-    // warpgroup's exp overlaps the tensor core's MMAs for the other tile
-    // instead of both exp phases colliding on the shared MUFU pipe.
-    if (pingpong) {
-      if (tile_x == 0 && j > 0) asm volatile("bar.sync 2, 256;" ::: "memory");
-      if (tile_x == 1) asm volatile("bar.sync 1, 256;" ::: "memory");
-    }
     if (quad == 0) ATRACE(1 + tile_x * 8, j);
     if (valid == kKeys) {
-      // full tile: every 4th pair of exponentials on the FMA pipe
 #pragma unroll
       for (int t = 0; t < 64; ++t) {
         float x0, x1, p0, p1;
@@ -294,7 +255,7 @@ __device__ __forceinline__ void softmax_tile(const AttnParams& prm, uint32_t tme
         }
         const uint64_t pp = f2(p0, p1);
         sum2[t & 1] = fadd2(sum2[t & 1], pp);
-        pk[t] = kAluPack ? pack_bf16_alu(p0, p1) : pack_bf16(p0, p1);
+        pk[t] = pack_bf16(p0, p1);
       }
     } else {
 #pragma unroll
@@ -304,14 +265,10 @@ __device__ __forceinline__ void softmax_tile(const AttnParams& prm, uint32_t tme
         const float p0 = ex2(x0);
         const float p1 = ex2(x1);
         sum2[t & 1] = fadd2(sum2[t & 1], f2(p0, p1));
-        pk[t] = kAluPack ? pack_bf16_alu(p0, p1) : pack_bf16(p0, p1);
+        pk[t] = pack_bf16(p0, p1);
       }
     }
     if (quad == 0) ATRACE(2 + tile_x * 8, j);
-    if (pingpong) {
-      if (tile_x == 0) asm volatile("bar.arrive 1, 256;" ::: "memory");
-      if (tile_x == 1 && j + 1 < n_tiles) asm volatile("bar.arrive 2, 256;" ::: "memory");
-    }
     // PV(j-1) must be complete before O is rescaled or P is overwritten
     if (j > 0) {
       mbar_wait(b.o_ready, (j - 1) & 1);
@@ -332,12 +289,8 @@ __device__ __forceinline__ void softmax_tile(const AttnParams& prm, uint32_t tme
     }
     // P -> smem in the UMMA K-major SW128 layout: half h holds keys
     // [64h, 64h+64); 16-byte chunk q of row r sits at chunk (q ^ (r & 7)).
-#ifndef BC_ATTN_NOPSTORE  // timing experiment only: skip the P stores
 #pragma unroll
     for (int q = 0; q < 16; ++q) {
-#else
-    for (int q = 0; q < 16; ++q) if (pk[4 * q] == 0x12345678u) {
-#endif
       const int half = q >> 3, ch = q & 7;
       sts128(sp_u32 + half * kHalf + row * 128 + ((ch ^ (row & 7)) << 4), pk[4 * q], pk[4 * q + 1], pk[4 * q + 2],
              pk[4 * q + 3]);
@@ -557,7 +510,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (x == 0 || has_b) {
       SoftmaxBars b{&s_full[x], &s_empty[x], &p_full[x], &o_ready[x]};
       softmax_tile<kPoly>(prm, tmem + x * 128, tmem + 256 + x * 128, smem + (x ? Smem::pb : Smem::pa), b, n_tiles,
-                   tiles_per_slot, warp & 3, q0 + x * kRows, e, head, x, has_b && kPingPong);
+                   tiles_per_slot, warp & 3, q0 + x * kRows, e, head, x);
     }
   }
   tc_fence_before();

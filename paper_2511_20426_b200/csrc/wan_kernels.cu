@@ -235,7 +235,7 @@ __global__ void rope_table_kernel(float2* tf, int max_frames, float2* th, int hp
 }
 
 template <int VPL, int WPR>  // bf16x8 (16 B) vectors per lane, warps per row
-__global__ void qk_norm_rope_kernel(const __nv_bfloat16* __restrict__ qkv, int rows, int d, int T,
+__global__ void __launch_bounds__(256) qk_norm_rope_kernel(const __nv_bfloat16* __restrict__ qkv, int rows, int d, int T,
                                     QkArgs a) {
   __shared__ float red[8];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -256,60 +256,69 @@ __global__ void qk_norm_rope_kernel(const __nv_bfloat16* __restrict__ qkv, int r
   __nv_bfloat16* kdst = a.arena + ((size_t)a.mat_base + (size_t)a.slot[e] * 2) * mat + (size_t)t * d;
   __nv_bfloat16* vdst = kdst + mat;
   const __nv_bfloat16* src = qkv + (size_t)rr * 3 * d;
+  // all of the row's q, k and v loads are issued before the first reduction
+  // (3x the bytes in flight per warp of the q-then-k-then-v order)
+  uint4 raw[3][VPL];
 #pragma unroll
-  for (int which = 0; which < 2; ++which) {
+  for (int which = 0; which < 3; ++which) {
     const uint4* s4 = reinterpret_cast<const uint4*>(src + which * d);
-    float vals[VPL][8];
-    float ss = 0.0f;
 #pragma unroll
     for (int i = 0; i < VPL; ++i) {
       const int idx = li + 32 * WPR * i;
-      if (active && idx * 8 < d) {
-        uint4 u = s4[idx];
-        const __nv_bfloat16* h = reinterpret_cast<const __nv_bfloat16*>(&u);
+      raw[which][i] = (active && idx * 8 < d) ? s4[idx] : make_uint4(0u, 0u, 0u, 0u);
+    }
+  }
+  float inv[2];
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          vals[i][j] = bf(h[j]);
-          ss += vals[i][j] * vals[i][j];
+  for (int which = 0; which < 2; ++which) {
+    float ss = 0.0f;
+#pragma unroll
+    for (int i = 0; i < VPL; ++i) {
+      const __nv_bfloat16* h = reinterpret_cast<const __nv_bfloat16*>(&raw[which][i]);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) ss += bf(h[j]) * bf(h[j]);
+    }
+    inv[which] = rsqrtf(row_reduce<WPR>(ss, red, slot, wir) / d + kEps);
+  }
+  if (active) {
+#pragma unroll
+    for (int which = 0; which < 2; ++which) {
+      const float* wgt = which == 0 ? a.norm_q : a.norm_k;
+      __nv_bfloat16* dst = which == 0 ? a.qout + (size_t)row * d : kdst;
+#pragma unroll
+      for (int i = 0; i < VPL; ++i) {
+        const int idx = li + 32 * WPR * i;
+        if (idx * 8 >= d) continue;
+        const int c0 = idx * 8;                 // element index in [0, d)
+        const int pair0 = (c0 & 127) >> 1;      // pair index inside the head
+        const __nv_bfloat16* h = reinterpret_cast<const __nv_bfloat16*>(&raw[which][i]);
+        uint4 u;
+        __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(&u);
+#pragma unroll
+        for (int j = 0; j < 8; j += 2) {
+          const float x0 = bf(h[j]) * inv[which] * wgt[c0 + j];
+          const float x1 = bf(h[j + 1]) * inv[which] * wgt[c0 + j + 1];
+          const int pi = pair0 + j / 2;
+          const float2 cs = pi < 22 ? rf[pi] : (pi < 43 ? rh[pi - 22] : rw[pi - 43]);
+          o[j] = __float2bfloat16(x0 * cs.x - x1 * cs.y);
+          o[j + 1] = __float2bfloat16(x0 * cs.y + x1 * cs.x);
+        }
+        reinterpret_cast<uint4*>(dst)[idx] = u;
+        if (which == 1 && a.peer.push) {  // fresh K -> every peer's replica (NVLink P2P store)
+          for (int p = 0; p < a.peer.n_peers; ++p)
+            reinterpret_cast<uint4*>(a.peer.arena[p] + (dst - a.arena))[idx] = u;
         }
       }
     }
-    const float inv = rsqrtf(row_reduce<WPR>(ss, red, slot, wir) / d + kEps);
-    if (!active) continue;
-    const float* wgt = which == 0 ? a.norm_q : a.norm_k;
-    __nv_bfloat16* dst = which == 0 ? a.qout + (size_t)row * d : kdst;
+    // v: plain copy into the slot (and the peers' replicas)
 #pragma unroll
     for (int i = 0; i < VPL; ++i) {
       const int idx = li + 32 * WPR * i;
       if (idx * 8 >= d) continue;
-      const int c0 = idx * 8;                 // element index in [0, d)
-      const int pair0 = (c0 & 127) >> 1;      // pair index inside the head
-      uint4 u;
-      __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(&u);
-#pragma unroll
-      for (int j = 0; j < 8; j += 2) {
-        const float x0 = vals[i][j] * inv * wgt[c0 + j];
-        const float x1 = vals[i][j + 1] * inv * wgt[c0 + j + 1];
-        const int pi = pair0 + j / 2;
-        const float2 cs = pi < 22 ? rf[pi] : (pi < 43 ? rh[pi - 22] : rw[pi - 43]);
-        o[j] = __float2bfloat16(x0 * cs.x - x1 * cs.y);
-        o[j + 1] = __float2bfloat16(x0 * cs.y + x1 * cs.x);
-      }
-      reinterpret_cast<uint4*>(dst)[idx] = u;
-      if (which == 1 && a.peer.push) {  // fresh K -> every peer's replica (NVLink P2P store)
-        for (int p = 0; p < a.peer.n_peers; ++p)
-          reinterpret_cast<uint4*>(a.peer.arena[p] + (dst - a.arena))[idx] = u;
-      }
-    }
-  }
-  if (active) {
-    // v: plain copy into the slot (and the peers' replicas)
-    const uint4* v4 = reinterpret_cast<const uint4*>(src + 2 * d);
-    for (int idx = li; idx * 8 < d; idx += 32 * WPR) {
-      const uint4 u = v4[idx];
-      reinterpret_cast<uint4*>(vdst)[idx] = u;
+      reinterpret_cast<uint4*>(vdst)[idx] = raw[2][i];
       if (a.peer.push)
-        for (int p = 0; p < a.peer.n_peers; ++p) reinterpret_cast<uint4*>(a.peer.arena[p] + (vdst - a.arena))[idx] = u;
+        for (int p = 0; p < a.peer.n_peers; ++p)
+          reinterpret_cast<uint4*>(a.peer.arena[p] + (vdst - a.arena))[idx] = raw[2][i];
     }
   }
   if (a.peer.n_peers > 0 && a.peer.push) {
@@ -488,10 +497,12 @@ int launch_ln_rows(const float* X, __nv_bfloat16* out, int rows, int d, int rows
 
 int launch_qk_norm_rope(const __nv_bfloat16* qkv, int rows, int d, int T, const QkArgs& a, cudaStream_t st) {
   const int v8 = d / 8;
-  if (v8 <= 32 * 6) {
-    qk_norm_rope_kernel<6, 1><<<(rows + 7) / 8, 256, 0, st>>>(qkv, rows, d, T, a);
-  } else if (v8 <= 4 * 32 * 6) {
-    qk_norm_rope_kernel<6, 4><<<(rows + 1) / 2, 256, 0, st>>>(qkv, rows, d, T, a);
+  // 3 vectors per lane per matrix (q, k, v all in flight: 36 registers of
+  // payload) keeps ~80 registers and 3 CTAs per SM
+  if (v8 <= 2 * 32 * 3) {
+    qk_norm_rope_kernel<3, 2><<<(rows + 3) / 4, 256, 0, st>>>(qkv, rows, d, T, a);
+  } else if (v8 <= 8 * 32 * 3) {
+    qk_norm_rope_kernel<3, 8><<<rows, 256, 0, st>>>(qkv, rows, d, T, a);
   } else {
     return bc_fail(BC_ERR_CONTRACT, "qk_norm_rope: d=%d too wide", d);
   }
