@@ -222,7 +222,11 @@ int bc_memset_async(void* ptr, int value, int64_t bytes, void* stream);
 /* C[M,N] (+)= epilogue(A[M,K] . B[N,K]^T + bias); bf16 in, fp32 accumulate.
  * mode 0: C bf16 = acc+bias;  1: C bf16 = gelu_tanh(acc+bias);
  * 2: C fp32 = acc+bias;       3: C fp32 += gate[row/rows_per_gate] * (acc+bias)
- * K % 64 == 0, N % 64 == 0; lda = ldb = K, ldc = N. */
+ * K % 64 == 0, N % 64 == 0; lda = ldb = K, ldc = N.
+ * Tuning bits above the epilogue (0 = automatic): bits 8-15 force the tile
+ * width in units of 64 columns; bits 16-17 = 1 single-CTA tiles, 2 CTA-pair
+ * tiles (tcgen05 cta_group::2, 256 rows; needs the width 256).  Results are
+ * identical for every choice (fixed K order, no split-K). */
 int bc_gemm_bf16(const void* A, const void* B, void* C, int32_t M, int32_t N, int32_t K,
                  int32_t mode, const float* bias, const float* gate, int32_t gate_stride,
                  int32_t rows_per_gate, void* stream);

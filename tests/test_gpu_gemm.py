@@ -61,3 +61,21 @@ def test_gemm_rejects_bad_shapes():
     C = torch.zeros(128, 128, device="cuda")
     with pytest.raises(Exception):
         gemm(A, B, C, 2)
+
+
+@pytest.mark.parametrize("M,Nn,K", [(4680, 1536, 1536), (600, 512, 8960), (9360, 4608, 1536)])
+def test_gemm_tilings_bitwise_equal(M, Nn, K):
+    """Every tiling (64/128/256 columns, single CTA or CTA pair) runs the K
+    loop in the same order, so the fp32 outputs are bit-identical -- the
+    runtime's automatic tile choice can never change a result."""
+    g = torch.Generator(device="cuda").manual_seed(M + Nn + K)
+    A = torch.randn(M, K, device="cuda", generator=g).bfloat16()
+    B = (torch.randn(Nn, K, device="cuda", generator=g) / K ** 0.5).bfloat16()
+    bias = torch.randn(Nn, device="cuda", generator=g)
+    outs = []
+    for bn, cg in ((64, 1), (128, 1), (256, 1), (256, 2), (0, 0)):
+        C = torch.empty(M, Nn, device="cuda")
+        gemm(A, B, C, 2, bias=bias, bn=bn, cg=cg)
+        outs.append(C)
+    for C in outs[1:]:
+        assert torch.equal(C, outs[0])
