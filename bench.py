@@ -290,6 +290,27 @@ def run_ours(args, cfg):
         seq_e2e = end_to_end_fps(seq.trace)
         seq_stream = streaming_fps(seq.trace, clock="wall")
 
+    # ---- prompt switch at block 8: cascade mode (product: text K/V swap only)
+    # vs the KV-recache baseline (paper: ~200 ms stall) ----
+    switch = None
+    if world == 1 and not args.no_switch and cfg.num_blocks > 9:
+        switch = {"at_block": 8}
+        for mode in ("cascade", "recache"):
+            sw = [bc.SwitchSpec(f"{PROMPT}, new scene", mode, at_block=8)]
+            r = bc.run_cascade(cfg, PROMPT, session_seed=SESSION_SEED, weights=weights,
+                               noise_feed=feed, switches=sw)
+            evs = r.trace.events
+            k = next(i for i, e in enumerate(evs) if e.switch is not None)
+            prev = evs[k - 1].wall_clock if k else 0.0
+            stall_ms = (evs[k].wall_clock - prev - evs[k].wall_seconds) * 1e3
+            nxt = next(e for e in evs[k:] if e.emitted_block is not None)
+            switch[mode] = {"extra_passes": r.switch_events[0].extra_passes,
+                            "stall_ms": round(stall_ms, 3),
+                            "pool_blocks": evs[k].pool_blocks,
+                            "fps_next_block": round(nxt.emitted_video_frames /
+                                                    (nxt.wall_clock - prev), 2),
+                            "e2e_fps": end_to_end_fps(r.trace)}
+
     S = cfg.block_size
     lat_bytes = S * cfg.latent_dim * 4
     h2d = len(run_noise_keys(cfg)) * lat_bytes + cfg.text_len * cfg.text_dim * 4
@@ -330,6 +351,7 @@ def run_ours(args, cfg):
         "streaming_fps": stream_fps,
         "sequential": {"e2e_fps": seq_e2e, "streaming_fps": seq_stream},
         "cascade_over_sequential_streaming": stream_fps / seq_stream if seq_stream else None,
+        "prompt_switch": switch,
         "roofline": {"bound": "tensor", "kernel": dom, "achieved": achieved, "peak": peak,
                      "unit": "TFLOP/s", "frac": achieved / peak if achieved else None,
                      "traffic": traffic, "peak_kind": f"{peak_kind} bf16 sustained",
@@ -358,6 +380,8 @@ def main():
     ap.add_argument("--switch-every", type=int, default=0,
                     help="cascade-mode prompt switch every N blocks (LongLive-style config 5)")
     ap.add_argument("--no-seq", action="store_true", help="skip the sequential rollout")
+    ap.add_argument("--no-switch", action="store_true",
+                    help="skip the cascade-vs-recache prompt-switch measurement")
     args = ap.parse_args()
     from paper_2511_20426_b200 import wan_config
     cfg = wan_config(args.preset, total_frames=3 * args.blocks, offset=1,

@@ -70,6 +70,19 @@ class ToyOracleSession:
             else:
                 self.latents.pop(b, None)
 
+    def recache_block(self, block, mask, vis_list):
+        pool_kv = {b: self.kv[b] for b in mask.pool_blocks}
+        (_, kv), = toy_oracle.forward(self.W, [(block, self.final[block], 0.0, self.cond.embedding)],
+                                      pool_kv, {block: vis_list})
+        self.kv[block] = kv
+        self.tags[block] = (0.0, self.cond.id)
+
+    def begin_stall(self):
+        pass
+
+    def end_stall(self, iteration):
+        pass
+
     def kv_handle(self, block):
         level, cid = self.tags[block]
         return tuple(_KV(block, l, k, v, level, cid) for l, (k, v) in enumerate(self.kv[block]))
@@ -144,6 +157,19 @@ class WanOracleSession:
                 self.latents[b] = x0
             else:
                 self.latents.pop(b, None)
+
+    def recache_block(self, block, mask, vis_list):
+        pool_kv = {b: self.kv[b] for b in mask.pool_blocks}
+        (_, kv), = self.o.forward([(block, self.final[block], 0.0)], pool_kv, {block: vis_list},
+                                  None, text_kv=self.text_kv)
+        self.kv[block] = kv
+        self.tags[block] = (0.0, self.cond.id)
+
+    def begin_stall(self):
+        pass
+
+    def end_stall(self, iteration):
+        pass
 
     def kv_handle(self, block):
         level, cid = self.tags[block]

@@ -206,6 +206,14 @@ __device__ __forceinline__ void softmax_tile(const AttnParams& prm, uint32_t tme
 #ifdef BC_ATTN_NOSOFTMAX  // timing experiment only: MMA/TMA skeleton
     if (j > 0) mbar_wait(b.o_ready, (j - 1) & 1);
     if (s[5] == 1234.5f) l_sum += 1.0f;
+#ifdef BC_ATTN_SKEL_STS  // + the P stores: does the smem write traffic cost tensor time?
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+      const int half = q >> 3, ch = q & 7;
+      sts128(sp_u32 + half * kHalf + row * 128 + ((ch ^ (row & 7)) << 4), __float_as_uint(s[8 * q]),
+             __float_as_uint(s[8 * q + 1]), __float_as_uint(s[8 * q + 2]), __float_as_uint(s[8 * q + 3]));
+    }
+#endif
     fence_async_shared();
     tc_fence_before();
     mbar_arrive(b.p_full);

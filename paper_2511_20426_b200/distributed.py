@@ -27,7 +27,7 @@ import os
 import numpy as np
 
 from . import _native as N
-from .errors import ContractViolation
+from .errors import ContractViolation, InvalidInputError
 
 # Tests flip this to run `workers > 1` sessions as emulated ranks on one GPU.
 EMULATE = os.environ.get("BC_EMULATE_RANKS", "0") == "1"
@@ -211,6 +211,16 @@ class DistWanSession:
         ev.record()
         self.events.append(ev)
 
+    def recache_block(self, block, mask, vis_list):
+        raise InvalidInputError("the KV-recache comparison baseline runs on one GPU only "
+                                "(the product switch is mode='cascade')")
+
+    def begin_stall(self):
+        pass
+
+    def end_stall(self, iteration):
+        pass
+
     def set_conditioning(self, cond):
         self.cond = cond
         self.state.ctx.set_text(cond)
@@ -358,6 +368,16 @@ class EmulatedRanks:
         ev = torch.cuda.Event(enable_timing=True)
         ev.record()
         self.events.append(ev)
+
+    def recache_block(self, block, mask, vis_list):
+        raise InvalidInputError("the KV-recache comparison baseline runs on one GPU only "
+                                "(the product switch is mode='cascade')")
+
+    def begin_stall(self):
+        pass
+
+    def end_stall(self, iteration):
+        pass
 
     def set_conditioning(self, cond):
         self.cond = cond

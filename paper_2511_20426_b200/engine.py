@@ -110,6 +110,25 @@ def _collect_outputs(dev, blocks) -> dict:
     return {b: dev.emitted_host(b) for b in blocks}
 
 
+def _recache(dev, pool, targets, S, iteration):
+    """KV recache (reference ``kvpool.recache``, kvpool.py:109-140): every
+    target pool block, in ascending order, reruns one causal level-0 forward
+    from its emitted x0 under the new conditioning, attending to its
+    already-recached pool predecessors; its KV is rewritten in place.  Only
+    the recache comparison baseline and ``refresh_sink_on_switch`` get here.
+    Returns the rebuilt pool and the visible frames of each pass."""
+    frames = []
+    dev.begin_stall()
+    for b in targets:
+        preds = [x for x in pool.block_indices if x < b]
+        mask = build_mask([b], preds, "causal", S)
+        dev.recache_block(b, mask, visible_block_lists(mask)[0])
+        pool = pool.insert(b, dev.kv_handle(b))
+        frames.append(mask.visible_frames(b))
+    dev.end_stall(iteration)
+    return pool, frames
+
+
 def run_cascade(config: CascadeConfig, prompt: str,
                 session_seed: int = DEFAULT_SESSION_SEED,
                 weight_seed: int = DEFAULT_WEIGHT_SEED,
@@ -121,10 +140,6 @@ def run_cascade(config: CascadeConfig, prompt: str,
     if config.decode_overlap and config.workers < 2:
         raise InvalidInputError("decode overlap needs at least 2 workers",
                                 fields=["decode_overlap", "workers"])
-    if config.refresh_sink_on_switch:
-        raise InvalidInputError(
-            "refresh_sink_on_switch re-runs a KV recache pass; the B200 build has "
-            "no KV-recache path", fields=["refresh_sink_on_switch"])
     sched = config.schedule()
     if weights is None:
         weights = _default_weights(config, weight_seed)
@@ -153,19 +168,26 @@ def run_cascade(config: CascadeConfig, prompt: str,
                 if live is not None:
                     spec = SwitchSpec(prompt=live.prompt, mode=live.mode,
                                       at_iteration=state.iteration)
+            stall = 0.0
             if spec is not None:
-                if spec.mode != "cascade":
-                    err = InvalidInputError(
-                        "recache switches are not on the B200 path (no KV-recache); "
-                        "use mode='cascade'")
-                    if live is not None:
-                        live.reject(err)
-                    raise err
                 cond = embed_prompt(spec.prompt, config.cond_dim)
                 dev.set_conditioning(cond)
+                extra = 0
+                if spec.mode == "recache":
+                    targets = pool.block_indices
+                elif config.refresh_sink_on_switch and pool.sink_indices:
+                    targets = pool.sink_indices[:1]
+                else:
+                    targets = ()
+                if targets:
+                    # comparison baseline only: the product
+                    # switch is mode="cascade", which touches no KV
+                    pool, frames = _recache(dev, pool, targets, S, state.iteration)
+                    extra = len(frames)
+                    stall = sum(cost.pass_cost(v) for v in frames)
                 ev = SwitchEvent(iteration=state.iteration, boundary_block=state.lead,
-                                 mode=spec.mode, extra_passes=0, conditioning_id=cond.id,
-                                 prompt=spec.prompt, stall_modeled=0.0)
+                                 mode=spec.mode, extra_passes=extra, conditioning_id=cond.id,
+                                 prompt=spec.prompt, stall_modeled=stall)
                 switch_events.append(ev)
                 record = ev.to_dict()
                 if live is not None:
@@ -219,11 +241,11 @@ def run_cascade(config: CascadeConfig, prompt: str,
                     decode_done_at = dec_done
                 else:
                     dec_charge = cost.decode_cost()
-            modeled += max(busy) + comm + dec_charge
+            modeled += stall + max(busy) + comm + dec_charge
 
             event = TraceEvent(
                 iteration=plan.iteration, entries=entry_rows, wall_seconds=0.0,
-                modeled_exec=max(busy), modeled_comm=comm, modeled_stall=0.0,
+                modeled_exec=max(busy), modeled_comm=comm, modeled_stall=stall,
                 modeled_decode=dec_charge, modeled_clock=modeled, wall_clock=0.0,
                 pool_blocks=len(pre_pool.block_indices), pool_frames=pre_pool.frame_count(),
                 pool_state=pre_pool.state_dump(), emitted_block=emitted_block,

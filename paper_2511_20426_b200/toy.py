@@ -150,6 +150,7 @@ class ToySession:
         self.x0 = [torch.empty((self.S, self.D), dtype=torch.float64, device="cuda")
                    for _ in range(N.MAX_ENTRIES)]
         self.events = []
+        self.stalls = {}
         self.set_conditioning(conditioning)
         self._mark()
 
@@ -197,6 +198,25 @@ class ToySession:
                 raise ContractViolation(f"unknown post op {kind}")
         self._mark()
 
+    def recache_block(self, block, mask, vis_list):
+        """One causal level-0 forward of an emitted block from its x0 under
+        the current conditioning; rewrites its KV slot (recache baseline,
+        reference kvpool.py:109-140)."""
+        vis = [self.slots.slot_of(v) for v in vis_list]
+        slot = self.slots.slot_of(block)
+        bt = N.make_batch(self.S, [block], [0.0], [slot], [vis])
+        self.rt.launch(bt, [self.final[block]], [self.cond_dev], self.arena, self.x0[:1], self.ws)
+        self.tags[block] = (0.0, self.cond.id)
+
+    def begin_stall(self):
+        self._stall0 = self.torch.cuda.Event(enable_timing=True)
+        self._stall0.record()
+
+    def end_stall(self, iteration):
+        ev = self.torch.cuda.Event(enable_timing=True)
+        ev.record()
+        self.stalls[iteration] = (self._stall0, ev)
+
     def kv_handle(self, block):
         level, cid = self.tags[block]
         return SlotKV(self.arena, self.slots.slot_of(block), block, level, cid, self.S)
@@ -220,6 +240,9 @@ class ToySession:
             t0, t1 = self.events[i], self.events[i + 1]
             ev.wall_seconds = t0.elapsed_time(t1) / 1e3
             ev.wall_clock = first.elapsed_time(t1) / 1e3
+            if i in self.stalls:  # the stall counts on the clock, not in the iteration
+                s0, s1 = self.stalls[i]
+                ev.wall_seconds -= s0.elapsed_time(s1) / 1e3
 
     def close(self):
         pass

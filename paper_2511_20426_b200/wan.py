@@ -374,6 +374,7 @@ class WanSession:
         self.eps = [torch.empty(self.shape, dtype=torch.float32, device="cuda")
                     for _ in range(width)]
         self.events = []
+        self.stalls = {}
         self.d2h_bytes = 0
         self.set_conditioning(conditioning)
         self._mark()
@@ -432,6 +433,29 @@ class WanSession:
                 self.latents.pop(e.block_index, None)
         self._mark()
 
+    def recache_block(self, block, mask, vis_list):
+        """One causal level-0 forward of an emitted block from its x0 under
+        the current conditioning, rewriting its KV slot in place (recache
+        baseline, reference kvpool.py:109-140; not the product switch)."""
+        vis = [self.slots.slot_of(v) for v in vis_list]
+        bt = N.make_batch(self.cfg.block_size, [block], [0.0], [self.slots.slot_of(block)], [vis])
+        upd = _make_update([POST_CACHE], [self.final[block]], [None], [None], [None])
+        self.ctx.step(bt, upd)
+        self.tags[block] = (0.0, self.cond.id)
+
+    def begin_stall(self):
+        self._stall0 = self.torch.cuda.Event(enable_timing=True)
+        self._stall0.record()
+
+    def end_stall(self, iteration):
+        ev = self.torch.cuda.Event(enable_timing=True)
+        ev.record()
+        self.stalls[iteration] = (self._stall0, ev)
+
+    def stall_seconds(self):
+        self.torch.cuda.current_stream().synchronize()
+        return {i: a.elapsed_time(b) / 1e3 for i, (a, b) in self.stalls.items()}
+
     def kv_handle(self, block):
         level, cid = self.tags[block]
         return SlotKV(self.ctx, self.slots.slot_of(block), block, level, cid, self.cfg.block_size)
@@ -463,6 +487,9 @@ class WanSession:
             t0, t1 = self.events[ev.iteration], self.events[ev.iteration + 1]
             ev.wall_seconds = t0.elapsed_time(t1) / 1e3
             ev.wall_clock = first.elapsed_time(t1) / 1e3
+            if ev.iteration in self.stalls:  # on the clock, not in the iteration
+                s0, s1 = self.stalls[ev.iteration]
+                ev.wall_seconds -= s0.elapsed_time(s1) / 1e3
 
     def close(self):
         self.release_device()

@@ -83,6 +83,14 @@ def main():
     arrays["default_cascade_o2"] = run_outputs(bc.with_fields(dflt, offset=2), "a red cube")
     sw = [bc.SwitchSpec("a calm meadow after the storm", "cascade", at_block=8)]
     arrays["default_cascade_switch8"] = run_outputs(dflt, "a lighthouse in a storm", switches=sw)
+    # KV-recache comparison baseline and the sink refresh (both rebuild pool KV)
+    rc = [bc.SwitchSpec("a calm meadow after the storm", "recache", at_block=8)]
+    arrays["default_cascade_recache8"] = run_outputs(dflt, "a lighthouse in a storm", switches=rc)
+    rc5 = [bc.SwitchSpec("a calm meadow", "recache", at_block=5)]
+    arrays["default_causal_recache5"] = run_outputs(bc.with_fields(dflt, attention_mode="causal"),
+                                                    "a red cube", switches=rc5)
+    arrays["default_refresh_sink8"] = run_outputs(bc.with_fields(dflt, refresh_sink_on_switch=True),
+                                                  "a lighthouse in a storm", switches=sw)
     # ---- operator cases: forward with pool + batch ----
     w_small = bc.init_model(11, 2, 2, 16, 16)
     w_tiny = bc.init_model(7, 4, 2, 256, 256)

@@ -77,6 +77,53 @@ def test_toy_runs_match_reference(golden, tiny_config, default_config):
                 golden["default_cascade_switch8"]) < REL
 
 
+def test_toy_recache_baseline_matches_reference(golden, default_config):
+    """KV-recache comparison baseline on the device (fp64) vs the
+    reference's own outputs, plus the sink refresh."""
+    import paper_2511_20426_b200 as bc
+    d = default_config
+    rc = [bc.SwitchSpec("a calm meadow after the storm", "recache", at_block=8)]
+    run = bc.run_cascade(d, "a lighthouse in a storm", switches=rc)
+    assert _rel(_stack(run), golden["default_cascade_recache8"]) < REL
+    assert run.switch_events[0].extra_passes == 7
+    hit = next(e for e in run.trace.events if e.switch is not None)
+    assert hit.wall_clock > 0 and 0 < hit.wall_seconds < hit.wall_clock
+    rc5 = [bc.SwitchSpec("a calm meadow", "recache", at_block=5)]
+    assert _rel(_stack(bc.run_cascade(bc.with_fields(d, attention_mode="causal"), "a red cube",
+                                      switches=rc5)), golden["default_causal_recache5"]) < REL
+    sw = [bc.SwitchSpec("a calm meadow after the storm", "cascade", at_block=8)]
+    assert _rel(_stack(bc.run_cascade(bc.with_fields(d, refresh_sink_on_switch=True),
+                                      "a lighthouse in a storm", switches=sw)),
+                golden["default_refresh_sink8"]) < REL
+
+
+def test_toy_recache_fixture_stream(default_config):
+    """The reference's golden event stream (recache_session.jsonl) from the
+    device engine: every non-pixel field identical, float32 pixels of all 13
+    blocks within 1e-6 relative (fp64 device vs fp64 BLAS order)."""
+    import base64
+    import json
+    import os
+    import paper_2511_20426_b200 as bc
+    from paper_2511_20426_b200.stream import events_from_trace
+    cfg = bc.with_fields(default_config, workers=5)
+    run = bc.run_cascade(cfg, "a lighthouse in a storm",
+                         switches=[bc.SwitchSpec("a calm meadow after the storm", "recache",
+                                                 at_block=8)])
+    with open(os.path.join(os.path.dirname(__file__), "golden", "recache_session.jsonl")) as fh:
+        want = [json.loads(l) for l in fh if l.strip()]
+    got = [json.loads(l) for l in events_from_trace(run.trace, cfg, run.outputs)]
+    assert len(got) == len(want)
+
+    def px(doc):
+        return np.frombuffer(base64.b64decode(doc.pop("pixels")["data"]), dtype="<f4")
+    for g, w in zip(got, want):
+        if w["type"] == "block":
+            a, b = px(g), px(w)
+            assert _rel(a, b) < 1e-6
+        assert g == w
+
+
 def test_p1_equivalence_exact(default_config):
     """offset = passes reproduces the sequential rollout bit-for-bit
     (test_acceptance.py:27-40) -- on the device too."""

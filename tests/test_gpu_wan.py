@@ -130,8 +130,30 @@ def test_wan_prompt_switch_cascade_mode(tiny):
     assert not np.array_equal(sw.outputs[5], plain.outputs[5])
     for b in range(cfg.num_blocks):
         assert np.array_equal(same.outputs[b], plain.outputs[b])
-    with pytest.raises(bc.InvalidInputError):
-        bc.run_cascade(cfg, "p", weights=w, switches=[bc.SwitchSpec("x", "recache", at_block=2)])
+
+
+def test_wan_recache_baseline_vs_oracle(tiny, monkeypatch):
+    """The KV-recache comparison baseline (every pool block re-run causal at
+    level 0 under the new prompt) on the device vs the oracle engine; the
+    stall is on the trace's clock but not in the iteration's wall_seconds."""
+    import paper_2511_20426_b200 as bc
+    from paper_2511_20426_b200 import engine
+    from oracle.loop import wan_oracle_runtime
+    cfg, w, params = tiny
+    cfg = bc.with_fields(cfg, total_frames=21)
+    sw = [bc.SwitchSpec("second scene", "recache", at_block=5)]
+    gpu = bc.run_cascade(cfg, "first scene", weights=w, switches=sw)
+    hit = next(e for e in gpu.trace.events if e.switch is not None)
+    assert gpu.switch_events[0].extra_passes == hit.pool_blocks > 0
+    assert all(r["noise_tag"] == 0.0 for r in hit.pool_state)
+    with monkeypatch.context() as m:
+        m.setattr(engine, "_runtime_for", wan_oracle_runtime(params))
+        cpu = bc.run_cascade(cfg, "first scene", weights=w, switches=sw)
+    for b in range(cfg.num_blocks):
+        assert rel(gpu.outputs[b], cpu.outputs[b]) < RUN_TOL, b
+    plain = bc.run_cascade(cfg, "first scene", weights=w,
+                           switches=[bc.SwitchSpec("second scene", "cascade", at_block=5)])
+    assert not np.array_equal(plain.outputs[6], gpu.outputs[6])
 
 
 def test_wan_13b_dims_step(monkeypatch):

@@ -159,11 +159,19 @@ def test_switch_spec_and_queue():
         r.wait(0.1)
 
 
-def test_engine_rejects_recache_paths(oracle_engine, default_config):
-    with pytest.raises(bc.InvalidInputError):
-        bc.run_cascade(default_config, "p", switches=[bc.SwitchSpec("q", "recache", at_block=2)])
-    with pytest.raises(bc.InvalidInputError):
-        bc.run_cascade(bc.with_fields(default_config, refresh_sink_on_switch=True), "p")
+def test_engine_recache_accounting(oracle_engine, default_config):
+    """A recache switch pays one pass per pool block (stall on the modeled
+    clock, pool re-tagged level 0 / new prompt); a cascade switch pays none."""
+    cfg = bc.with_fields(default_config, total_frames=24)
+    run = bc.run_cascade(cfg, "p", switches=[bc.SwitchSpec("q", "recache", at_block=6)])
+    ev = run.switch_events[0]
+    hit = next(e for e in run.trace.events if e.switch is not None)
+    assert ev.extra_passes == hit.pool_blocks and hit.modeled_stall == ev.stall_modeled > 0
+    assert all(row["noise_tag"] == 0.0 and row["conditioning_id"] == ev.conditioning_id
+               for row in hit.pool_state)
+    plain = bc.run_cascade(cfg, "p", switches=[bc.SwitchSpec("q", "cascade", at_block=6)])
+    assert plain.switch_events[0].extra_passes == 0
+    assert run.trace.events[-1].modeled_clock == plain.trace.events[-1].modeled_clock + ev.stall_modeled
 
 
 def test_engine_properties_on_oracle(oracle_engine, default_config):

@@ -158,6 +158,26 @@ def test_engine_runs_match_reference(oracle_engine, golden, tiny_config, default
                           golden["default_cascade_switch8"])
 
 
+def test_recache_baseline_runs_match_reference(oracle_engine, golden, default_config):
+    """KV-recache comparison baseline (reference kvpool.recache,
+    engine._apply_switch) and the sink refresh, through the product engine."""
+    from paper_2511_20426_b200 import SwitchSpec, run_cascade, with_fields
+    d = default_config
+    rc = [SwitchSpec("a calm meadow after the storm", "recache", at_block=8)]
+    run = run_cascade(d, "a lighthouse in a storm", switches=rc)
+    assert np.array_equal(_stack(run), golden["default_cascade_recache8"])
+    ev = run.switch_events[0]
+    assert (ev.extra_passes, ev.stall_modeled) == (7, 7.0)
+    rc5 = [SwitchSpec("a calm meadow", "recache", at_block=5)]
+    assert np.array_equal(_stack(run_cascade(with_fields(d, attention_mode="causal"), "a red cube",
+                                             switches=rc5)), golden["default_causal_recache5"])
+    sw = [SwitchSpec("a calm meadow after the storm", "cascade", at_block=8)]
+    ref = run_cascade(with_fields(d, refresh_sink_on_switch=True), "a lighthouse in a storm",
+                      switches=sw)
+    assert np.array_equal(_stack(ref), golden["default_refresh_sink8"])
+    assert ref.switch_events[0].extra_passes == 1
+
+
 def test_engine_trace_matches_reference(oracle_engine, golden_sched, tiny_config):
     from paper_2511_20426_b200 import run_cascade
     run = run_cascade(tiny_config, "a red cube")
@@ -167,29 +187,20 @@ def test_engine_trace_matches_reference(oracle_engine, golden_sched, tiny_config
     assert got == golden_sched["tiny_trace"]
 
 
-def test_recache_fixture_prefix(oracle_engine, default_config):
-    """The reference's own golden stream (frontend fixture): before the
-    recache switch at block 8 the schedule, pool and decoded pixels of
-    blocks 0..7 are fixed by the cascade; our host engine reproduces them."""
-    from paper_2511_20426_b200 import run_cascade, with_fields
-    from paper_2511_20426_b200.executor import decode_block, make_decode_map
+def test_recache_fixture_full_stream(oracle_engine, default_config):
+    """The reference's own golden stream (frontend fixture
+    recache_session.jsonl: 13 blocks, G=5, a recache switch at block 8),
+    reproduced byte for byte -- every switch/metrics/block/done line incl.
+    the float32-decoded pixels -- by the product engine + event projection
+    driven by the oracle forward."""
+    from paper_2511_20426_b200 import SwitchSpec, run_cascade, with_fields
+    from paper_2511_20426_b200.stream import events_from_trace
     cfg = with_fields(default_config, workers=5)
-    run = run_cascade(cfg, "a lighthouse in a storm")
-    lines = [json.loads(l) for l in open(os.path.join(os.path.dirname(__file__), "golden",
-                                                       "recache_session.jsonl"))]
-    switch_it = next(l["iteration"] for l in lines if l["type"] == "switch")
-    metrics = {l["iteration"]: l for l in lines if l["type"] == "metrics"}
-    for ev in run.trace.events:
-        if ev.iteration >= switch_it:
-            break
-        m = metrics[ev.iteration]
-        assert m["entries"] == ev.entries
-        assert (m["pool_blocks"], m["pool_frames"], m["phase_width"]) == \
-               (ev.pool_blocks, ev.pool_frames, len(ev.entries))
-        assert (m["modeled_exec"], m["modeled_clock"]) == (ev.modeled_exec, ev.modeled_clock)
-    dmap = make_decode_map(cfg.pixel_dim, cfg.latent_dim, cfg.video_frames_per_latent, seed=7)
-    blocks = {l["index"]: l for l in lines if l["type"] == "block"}
-    for b in range(8):
-        pix = decode_block(run.outputs[b], dmap, cfg.video_frames_per_latent)
-        enc = base64.b64encode(np.ascontiguousarray(pix, dtype="<f4").tobytes()).decode()
-        assert blocks[b]["pixels"]["data"] == enc
+    run = run_cascade(cfg, "a lighthouse in a storm",
+                      switches=[SwitchSpec("a calm meadow after the storm", "recache", at_block=8)])
+    with open(os.path.join(os.path.dirname(__file__), "golden", "recache_session.jsonl")) as fh:
+        want = [l.rstrip("\n") for l in fh if l.strip()]
+    got = events_from_trace(run.trace, cfg, run.outputs)
+    assert len(got) == len(want) == 32
+    for g, w in zip(got, want):
+        assert g == w
