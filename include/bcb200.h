@@ -180,30 +180,45 @@ int bc_wan_step(bc_wan_ctx* ctx, const bc_batch* batch, const bc_wan_update* upd
                 int32_t* status, void* stream);
 
 /* ---- multi-GPU temporal parallelism (one process per GPU, NVLink P2P) ----
- * Every rank holds a full KV-arena replica.  The q/k kernel writes each
- * fresh K/V row into the local slot AND into every peer's replica (P2P
- * stores), then publishes epoch into peers' flags[layer][slot]; attention
- * waits (per visible slot) for flags >= need before its first tile of that
- * slot; the head kernel publishes iteration-done epochs, which the next
- * iteration's first K/V write waits for (no reader of a slot is overtaken).
+ * Every rank holds a full KV-arena replica.  Fresh K/V rows computed by a
+ * rank are copied into every peer's replica (copy engines, or P2P stores
+ * from the q/k kernel with BC_KV_PUSH=kernel) and the rank publishes
+ * epoch into peers' flags[layer][slot][my_rank]; attention waits (per
+ * visible slot) until the flag of every producer rank in pmask is >= need
+ * before its first tile of that slot; the head kernel publishes
+ * iteration-done epochs, which the next iteration's first K/V write waits
+ * for (no reader of a slot is overtaken).
+ * Two partitions of an iteration (the caller chooses per step):
+ *  - blocks: a rank runs whole entries (row1 = 0; batch = its own entries);
+ *  - rows:   every rank gets the whole batch and runs the global rows
+ *            [row0, row1) of the n*T concatenated rows; Y rows are exchanged
+ *            (my_y / peer_y, yready flags) and every rank updates every
+ *            entry's latents (replicated, so latents never move).
  * Pointers are device (IPC-mapped) addresses. */
 #define BC_MAX_PEERS 8
 typedef struct {
   int32_t n_peers, my_rank, n_ranks;             /* n_ranks = n_peers + 1      */
   void* peer_arena[BC_MAX_PEERS];
-  uint32_t* peer_flags[BC_MAX_PEERS];            /* peers' [L][n_slots]        */
+  uint32_t* peer_flags[BC_MAX_PEERS];            /* peers' [L][n_slots][n_ranks] */
   uint32_t* peer_done[BC_MAX_PEERS];             /* peers' [n_ranks]           */
   uint32_t* my_flags;                            /* ours, written by peers     */
   uint32_t* my_done;
   uint32_t* counters;                            /* >= 1 zeroed u32 (scratch)  */
+  /* row-sharded steps only (else NULL): Y [max_entries*T][64] fp32 */
+  float* my_y;
+  void* peer_y[BC_MAX_PEERS];
+  uint32_t* my_yready;                           /* ours [n_ranks], written by peers */
+  uint32_t* peer_yready[BC_MAX_PEERS];
 } bc_wan_peers;
 int bc_wan_set_peers(bc_wan_ctx* ctx, const bc_wan_peers* peers);
 
 typedef struct {
-  uint32_t epoch;                                 /* iteration epoch, >= 1     */
+  uint32_t epoch;                                 /* iteration epoch, 1 .. 2^24-1 */
   uint32_t need[BC_MAX_ENTRIES][BC_MAX_VIS];      /* wait epoch per visible slot (0 = none) */
-  int32_t stage;                                  /* -1 whole step; 0 begin; 1 layer part A; 2 part B; 3 end */
+  uint8_t pmask[BC_MAX_ENTRIES][BC_MAX_VIS];      /* producer ranks to wait for (bit r) */
+  int32_t stage;  /* -1 whole step; 0 begin; 1 layer part A; 2 part B; 3 head (+Y push); 4 update */
   int32_t layer;
+  int32_t row0, row1;                             /* rows partition: global row slice; row1 = 0: blocks */
 } bc_wan_dist;
 int bc_wan_step_dist(bc_wan_ctx* ctx, const bc_batch* batch, const bc_wan_update* upd,
                      const bc_wan_dist* dist, int32_t* status, void* stream);

@@ -78,12 +78,15 @@ class WanPeers(C.Structure):
     _fields_ = [("n_peers", C.c_int32), ("my_rank", C.c_int32), ("n_ranks", C.c_int32),
                 ("peer_arena", C.c_void_p * MAX_PEERS), ("peer_flags", C.c_void_p * MAX_PEERS),
                 ("peer_done", C.c_void_p * MAX_PEERS), ("my_flags", C.c_void_p),
-                ("my_done", C.c_void_p), ("counters", C.c_void_p)]
+                ("my_done", C.c_void_p), ("counters", C.c_void_p),
+                ("my_y", C.c_void_p), ("peer_y", C.c_void_p * MAX_PEERS),
+                ("my_yready", C.c_void_p), ("peer_yready", C.c_void_p * MAX_PEERS)]
 
 
 class WanDist(C.Structure):
     _fields_ = [("epoch", C.c_uint32), ("need", (C.c_uint32 * MAX_VIS) * MAX_ENTRIES),
-                ("stage", C.c_int32), ("layer", C.c_int32)]
+                ("pmask", (C.c_uint8 * MAX_VIS) * MAX_ENTRIES),
+                ("stage", C.c_int32), ("layer", C.c_int32), ("row0", C.c_int32), ("row1", C.c_int32)]
 
 
 _SIGS = {

@@ -177,7 +177,7 @@ struct SoftmaxBars {
 template <int kPoly>
 __device__ __forceinline__ void softmax_tile(const AttnParams& prm, uint32_t tmem_s, uint32_t tmem_o,
                                              uint8_t* sp, SoftmaxBars b, int n_tiles, int tiles_per_slot,
-                                             uint32_t quad, int q_row0, int e, int head, int tile_x) {
+                                             uint32_t quad, int q_tok0, int e, int head, int tile_x) {
   const uint32_t row = quad * 32 + lane_id();
   const uint32_t lane_base = (quad * 32) << 16;
   const float c = prm.scale * 1.4426950408889634f;
@@ -317,11 +317,11 @@ __device__ __forceinline__ void softmax_tile(const AttnParams& prm, uint32_t tme
     mbar_wait(b.o_ready, (n_tiles - 1) & 1);
     tc_fence_after();
   }
-  const int qrow = q_row0 + (int)row;
-  const bool live = qrow < prm.q_tokens;
+  const int qtok = q_tok0 + (int)row;
+  const bool live = qtok < prm.q_hi[e];
   const float inv = (l_sum > 0.0f) ? 1.0f / l_sum : 0.0f;
   __nv_bfloat16* out = static_cast<__nv_bfloat16*>(prm.out) +
-                       ((size_t)(e * prm.q_tokens + qrow) * prm.heads + head) * kHd;
+                       ((size_t)(prm.q_row[e] + qtok - prm.q_lo[e]) * prm.heads + head) * kHd;
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
     uint32_t r[32];
@@ -361,8 +361,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   // grid: x = query-tile pair, y = entry, z = head (concurrent CTAs share a
   // head's K/V in L2)
   const int pair = blockIdx.x, e = blockIdx.y, head = blockIdx.z;
-  const int q0 = pair * 2 * kRows;
-  const bool has_b = q0 + kRows < prm.q_tokens;
+  const int q0 = prm.q_lo[e] + pair * 2 * kRows;  // first query token of tile A
+  if (q0 >= prm.q_hi[e]) return;                  // this entry has fewer tiles here
+  const bool has_b = q0 + kRows < prm.q_hi[e];
   const int n_vis = prm.n_vis[e];
   const int tiles_per_slot = (prm.kv_tokens + kKeys - 1) / kKeys;
   const int n_tiles = n_vis * tiles_per_slot;
@@ -397,7 +398,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp < 4) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegsCtl));
   if (warp == 0) {
     if (lane_id() == 0) {
-      const int qrow = e * prm.q_tokens + q0;
+      const int qrow = prm.q_row[e] + (q0 - prm.q_lo[e]);
       mbar_arrive_expect_tx(q_full, has_b ? 2 * kTile : kTile);
       tma_load_3d(smem + Smem::qa, &map_q, q_full, 0, head, qrow);
       tma_load_3d(smem + Smem::qa + kHalf, &map_q, q_full, 64, head, qrow);
@@ -419,13 +420,17 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int mat = prm.mat_base + kv_slot * prm.mat_stride + (is_v ? prm.v_offset : 0);
         if (!is_v && prm.flags && (j % tiles_per_slot) == 0) {
           const uint32_t need = prm.need[e][j / tiles_per_slot];
-          if (need) {  // K/V of this block is pushed by a peer GPU: wait for it
-            const uint32_t* f = prm.flags + prm.flag_base + kv_slot;
-            uint32_t v;
-            for (;;) {
-              asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
-              if (v >= need) break;
-              __nanosleep(256);
+          if (need) {  // K/V rows of this block come from peer GPUs: wait for each producer
+            const uint32_t ep = need >> 8;
+            const uint32_t* f = prm.flags + (size_t)(prm.flag_base + kv_slot) * prm.n_ranks;
+            for (uint32_t m = need & 0xffu; m; m &= m - 1) {
+              const uint32_t* fr = f + (__ffs(m) - 1);
+              uint32_t v;
+              for (;;) {
+                asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(fr) : "memory");
+                if (v >= ep) break;
+                __nanosleep(256);
+              }
             }
             asm volatile("fence.proxy.async.global;" ::: "memory");
           }
@@ -560,7 +565,8 @@ int attention_run(const AttnArgs& a, cudaStream_t st) {
   const uint64_t row_bytes = (uint64_t)a.heads * kHd * 2;
   CUtensorMap mq, mkv;
   {
-    cuuint64_t dims[3] = {kHd, (cuuint64_t)a.heads, (cuuint64_t)a.n_entries * a.q_tokens};
+    cuuint64_t dims[3] = {kHd, (cuuint64_t)a.heads,
+                          (cuuint64_t)(a.ranged ? a.q_rows : a.n_entries * a.q_tokens)};
     cuuint64_t strides[2] = {kHd * 2, row_bytes};
     cuuint32_t box[3] = {64, 1, kRows};
     int rc = encode(&mq, a.q, 3, dims, strides, box);
@@ -582,8 +588,23 @@ int attention_run(const AttnArgs& a, cudaStream_t st) {
   p.v_offset = a.v_offset;
   p.scale = a.scale;
   p.out = a.out;
+  p.n_ranks = a.n_ranks > 0 ? a.n_ranks : 1;
+  int max_pairs = 0;
   for (int e = 0; e < a.n_entries; ++e) {
     if (a.n_vis[e] < 0 || a.n_vis[e] > BC_MAX_VIS) return bc_fail(BC_ERR_CONTRACT, "attention: bad visible count");
+    if (a.ranged) {
+      if (a.q_lo[e] < 0 || a.q_hi[e] > a.q_tokens || a.q_row[e] + (a.q_hi[e] - a.q_lo[e]) > a.q_rows)
+        return bc_fail(BC_ERR_CONTRACT, "attention: bad query row range (entry %d)", e);
+      p.q_lo[e] = a.q_lo[e];
+      p.q_hi[e] = a.q_hi[e];
+      p.q_row[e] = a.q_row[e];
+    } else {
+      p.q_lo[e] = 0;
+      p.q_hi[e] = a.q_tokens;
+      p.q_row[e] = e * a.q_tokens;
+    }
+    const int pairs = (p.q_hi[e] - p.q_lo[e] + 2 * kRows - 1) / (2 * kRows);
+    max_pairs = pairs > max_pairs ? pairs : max_pairs;
     p.n_vis[e] = a.n_vis[e];
     for (int v = 0; v < a.n_vis[e]; ++v) {
       p.vis_slot[e][v] = a.vis_slot[e][v];
@@ -617,7 +638,8 @@ int attention_run(const AttnArgs& a, cudaStream_t st) {
     if (fa.numRegs != kRegsLaunch)  // the setmaxnreg split assumes this allocation (else: deadlock)
       return bc_fail(BC_ERR_CUDA, "attention kernel built with %d registers, expected %d", fa.numRegs, kRegsLaunch);
   }
-  dim3 grid((a.q_tokens + 2 * kRows - 1) / (2 * kRows), a.n_entries, a.heads);
+  if (max_pairs == 0) return BC_OK;  // no query rows in this slice
+  dim3 grid(max_pairs, a.n_entries, a.heads);
   switch (poly) {
     case 2: attn_kernel<2><<<grid, kThreads, Smem::total + 1024, st>>>(mq, mkv, p); break;
     case 3: attn_kernel<3><<<grid, kThreads, Smem::total + 1024, st>>>(mq, mkv, p); break;

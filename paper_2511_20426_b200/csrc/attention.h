@@ -21,10 +21,16 @@ struct AttnParams {
   int n_vis[BC_MAX_ENTRIES];
   int vis_slot[BC_MAX_ENTRIES][BC_MAX_VIS];
   // multi-GPU: before the first tile of visible slot v, wait until
-  // flags[flag_base + slot] >= need[e][v] (0 = no wait; peers publish)
+  // flags[(flag_base + slot) * n_ranks + r] >= need >> 8 for every producer
+  // rank r in the mask need & 0xff (need = 0: no wait; peers publish)
   const uint32_t* flags;
   int flag_base;
+  int n_ranks;
   uint32_t need[BC_MAX_ENTRIES][BC_MAX_VIS];
+  // query rows of entry e handled by this launch: tokens [q_lo, q_hi), token
+  // q_lo at row q_row of the q / out buffers (row-sharded multi-GPU steps
+  // run a slice of the batch's rows; by default the whole entry)
+  int q_lo[BC_MAX_ENTRIES], q_hi[BC_MAX_ENTRIES], q_row[BC_MAX_ENTRIES];
 };
 
 struct AttnArgs {
@@ -39,7 +45,12 @@ struct AttnArgs {
   int vis_slot[BC_MAX_ENTRIES][BC_MAX_VIS];
   const uint32_t* flags;
   int flag_base;
+  int n_ranks;
   uint32_t need[BC_MAX_ENTRIES][BC_MAX_VIS];
+  // ranged = 0: every entry's q_tokens rows, entry e at row e * q_tokens;
+  // ranged = 1: q_lo / q_hi / q_row as in AttnParams, q / out have q_rows rows
+  int ranged, q_rows;
+  int q_lo[BC_MAX_ENTRIES], q_hi[BC_MAX_ENTRIES], q_row[BC_MAX_ENTRIES];
 };
 
 int attention_run(const AttnArgs& a, cudaStream_t st);

@@ -132,7 +132,7 @@ template <int BN, int MODE, int CG>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                 void* __restrict__ c_ptr, int M, int N, int K, const float* __restrict__ bias,
-                const float* __restrict__ gate, int gate_stride, int rows_per_gate) {
+                const float* __restrict__ gate, int gate_stride, int rows_per_gate, int gate_row0) {
   using Cfg = GemmCfg<BN, CG>;
   constexpr int S = Cfg::kStages;
   constexpr int TM = BM * CG;  // rows per (cluster) tile
@@ -315,7 +315,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (row < M) {
               res[i] = *reinterpret_cast<const float4*>(static_cast<float*>(c_ptr) + (size_t)row * N + col + sub_col);
               if (gate)
-                g[i] = __ldg(reinterpret_cast<const float4*>(gate + (size_t)(row / rows_per_gate) * gate_stride +
+                g[i] = __ldg(reinterpret_cast<const float4*>(gate + (size_t)((gate_row0 + row) / rows_per_gate) * gate_stride +
                                                              col + sub_col));
             }
           }
@@ -399,7 +399,7 @@ int sm_count() {
 
 template <int BN, int MODE, int CG>
 int launch(const CUtensorMap& ma, const CUtensorMap& mb, void* C, int M, int N, int K,
-           const float* bias, const float* gate, int gate_stride, int rows_per_gate,
+           const float* bias, const float* gate, int gate_stride, int rows_per_gate, int gate_row0,
            cudaStream_t st) {
   using Cfg = GemmCfg<BN, CG>;
   static bool attr = false;
@@ -439,19 +439,19 @@ int launch(const CUtensorMap& ma, const CUtensorMap& mb, void* C, int M, int N, 
   const int grid = (tiles < units ? tiles : units) * CG;
   cfg.gridDim = dim3(grid);
   BC_CUDA(cudaLaunchKernelEx(&cfg, gemm_kernel<BN, MODE, CG>, ma, mb, C, M, N, K, bias, gate, gate_stride,
-                             rows_per_gate));
+                             rows_per_gate, gate_row0));
   BC_LAUNCHED();
   return BC_OK;
 }
 
 template <int BN, int CG>
 int dispatch_mode(int mode, const CUtensorMap& ma, const CUtensorMap& mb, void* C, int M, int N,
-                  int K, const float* bias, const float* gate, int gs, int rpg, cudaStream_t st) {
+                  int K, const float* bias, const float* gate, int gs, int rpg, int gr0, cudaStream_t st) {
   switch (mode) {
-    case kEpiStoreBf16: return launch<BN, kEpiStoreBf16, CG>(ma, mb, C, M, N, K, bias, gate, gs, rpg, st);
-    case kEpiGeluBf16: return launch<BN, kEpiGeluBf16, CG>(ma, mb, C, M, N, K, bias, gate, gs, rpg, st);
-    case kEpiStoreF32: return launch<BN, kEpiStoreF32, CG>(ma, mb, C, M, N, K, bias, gate, gs, rpg, st);
-    case kEpiResidualF32: return launch<BN, kEpiResidualF32, CG>(ma, mb, C, M, N, K, bias, gate, gs, rpg, st);
+    case kEpiStoreBf16: return launch<BN, kEpiStoreBf16, CG>(ma, mb, C, M, N, K, bias, gate, gs, rpg, gr0, st);
+    case kEpiGeluBf16: return launch<BN, kEpiGeluBf16, CG>(ma, mb, C, M, N, K, bias, gate, gs, rpg, gr0, st);
+    case kEpiStoreF32: return launch<BN, kEpiStoreF32, CG>(ma, mb, C, M, N, K, bias, gate, gs, rpg, gr0, st);
+    case kEpiResidualF32: return launch<BN, kEpiResidualF32, CG>(ma, mb, C, M, N, K, bias, gate, gs, rpg, gr0, st);
   }
   return bc_fail(BC_ERR_CONTRACT, "gemm: unknown epilogue mode %d", mode);
 }
@@ -505,11 +505,11 @@ int gemm_run(const GemmArgs& g, cudaStream_t st) {
   rc = make_tmap_2d(&mb, g.B, g.K, g.N, (uint64_t)g.K * 2, BK, bn / cg);
   if (rc) return rc;
   if (cg == 2)
-    return dispatch_mode<256, 2>(g.mode, ma, mb, g.C, g.M, g.N, g.K, g.bias, g.gate, g.gate_stride, g.rows_per_gate, st);
+    return dispatch_mode<256, 2>(g.mode, ma, mb, g.C, g.M, g.N, g.K, g.bias, g.gate, g.gate_stride, g.rows_per_gate, g.gate_row0, st);
   switch (bn) {
-    case 256: return dispatch_mode<256, 1>(g.mode, ma, mb, g.C, g.M, g.N, g.K, g.bias, g.gate, g.gate_stride, g.rows_per_gate, st);
-    case 128: return dispatch_mode<128, 1>(g.mode, ma, mb, g.C, g.M, g.N, g.K, g.bias, g.gate, g.gate_stride, g.rows_per_gate, st);
-    case 64: return dispatch_mode<64, 1>(g.mode, ma, mb, g.C, g.M, g.N, g.K, g.bias, g.gate, g.gate_stride, g.rows_per_gate, st);
+    case 256: return dispatch_mode<256, 1>(g.mode, ma, mb, g.C, g.M, g.N, g.K, g.bias, g.gate, g.gate_stride, g.rows_per_gate, g.gate_row0, st);
+    case 128: return dispatch_mode<128, 1>(g.mode, ma, mb, g.C, g.M, g.N, g.K, g.bias, g.gate, g.gate_stride, g.rows_per_gate, g.gate_row0, st);
+    case 64: return dispatch_mode<64, 1>(g.mode, ma, mb, g.C, g.M, g.N, g.K, g.bias, g.gate, g.gate_stride, g.rows_per_gate, g.gate_row0, st);
   }
   return bc_fail(BC_ERR_CONTRACT, "gemm: bad tile width %d", bn);
 }
@@ -523,6 +523,6 @@ extern "C" int bc_gemm_bf16(const void* A, const void* B, void* C, int32_t M, in
   // mode bits 16-17: 1 = single-CTA tiles only, 2 = CTA pairs when possible
   bc::GemmArgs g{A, B, C, M, N, K, mode & 0xff, bias, gate, gate_stride,
                  rows_per_gate > 0 ? rows_per_gate : 1, (mode >> 8) & 0xff ? ((mode >> 8) & 0xff) * 64 : 0,
-                 (mode >> 16) & 3};
+                 (mode >> 16) & 3, 0};
   return bc::gemm_run(g, (cudaStream_t)stream);
 }

@@ -25,6 +25,7 @@ struct GemmArgs {
   int rows_per_gate;
   int bn;  // 0 = auto
   int cg;  // 0 = auto, 1 = single CTA, 2 = CTA pair
+  int gate_row0;  // gate row of C row r = (gate_row0 + r) / rows_per_gate
 };
 
 int gemm_run(const GemmArgs& g, cudaStream_t st);

@@ -81,18 +81,21 @@ __device__ __forceinline__ float bf(const __nv_bfloat16 v) { return __bfloat162f
 // ------------------------------------------------------------ patchify
 // x: (F,16,H,W) fp32 -> tokens (F*(H/2)*(W/2), 64) bf16; vector index
 // c*4 + kh*2 + kw (Conv3d weight order, kernel (1,2,2)).
-__global__ void patchify_kernel(EntryPtrs lat, int F, int H, int W, __nv_bfloat16* out, int T) {
-  const int e = blockIdx.y;
-  const float* x = lat.p[e];
+// Rows [row0, row0 + rows) of the concatenated batch (row = e * T + token);
+// out row 0 = global row row0.
+__global__ void patchify_kernel(EntryPtrs lat, int F, int H, int W, __nv_bfloat16* out, int T, int row0,
+                                int rows) {
   const int hp = H / 2, wp = W / 2;
-  const int total = T * 64;
-  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += gridDim.x * blockDim.x) {
-    const int n = idx >> 6, v = idx & 63;
+  const int64_t total = (int64_t)rows * 64;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int g = row0 + (int)(idx >> 6), v = (int)(idx & 63);
+    const int e = g / T, n = g % T;
     const int c = v >> 2, kh = (v >> 1) & 1, kw = v & 1;
     const int f = n / (hp * wp), rem = n % (hp * wp);
     const int i = rem / wp, j = rem % wp;
-    const float val = x[(((size_t)f * 16 + c) * H + 2 * i + kh) * W + 2 * j + kw];
-    out[(size_t)e * T * 64 + idx] = __float2bfloat16(val);
+    const float val = lat.p[e][(((size_t)f * 16 + c) * H + 2 * i + kh) * W + 2 * j + kw];
+    out[idx] = __float2bfloat16(val);
   }
 }
 
@@ -177,7 +180,7 @@ __global__ void ln_rows_kernel(const float* __restrict__ X, __nv_bfloat16* __res
   }
   const float rstd = rsqrtf(row_reduce<WPR>(q, red, slot, wir) / d + kEps);
   if (!active) return;
-  const int e = row / rows_per_entry;
+  const int e = (a.row0 + row) / rows_per_entry;
   const float* p_scale = a.base_scale;
   const float* p_shift = a.base_shift;
   const float* q_scale = a.mode == 0 ? a.pe_scale + (size_t)e * a.entry_stride : nullptr;
@@ -244,7 +247,8 @@ __global__ void __launch_bounds__(256) qk_norm_rope_kernel(const __nv_bfloat16* 
   const int li = wir * 32 + lane;
   const bool active = row < rows;
   wait_peers_done(a.peer);
-  const int rr = active ? row : 0;
+  const int lr = active ? row : 0;            // local row (q / qkv buffers)
+  const int rr = a.row0 + lr;                  // global row of the batch
   const int e = rr / T, t = rr % T;
   const int hw = a.hp * a.wp;
   const int fl = t / hw, rem = t % hw;
@@ -255,7 +259,7 @@ __global__ void __launch_bounds__(256) qk_norm_rope_kernel(const __nv_bfloat16* 
   const size_t mat = (size_t)T * d;
   __nv_bfloat16* kdst = a.arena + ((size_t)a.mat_base + (size_t)a.slot[e] * 2) * mat + (size_t)t * d;
   __nv_bfloat16* vdst = kdst + mat;
-  const __nv_bfloat16* src = qkv + (size_t)rr * 3 * d;
+  const __nv_bfloat16* src = qkv + (size_t)lr * 3 * d;
   // all of the row's q, k and v loads are issued before the first reduction
   // (3x the bytes in flight per warp of the q-then-k-then-v order)
   uint4 raw[3][VPL];
@@ -284,7 +288,7 @@ __global__ void __launch_bounds__(256) qk_norm_rope_kernel(const __nv_bfloat16* 
 #pragma unroll
     for (int which = 0; which < 2; ++which) {
       const float* wgt = which == 0 ? a.norm_q : a.norm_k;
-      __nv_bfloat16* dst = which == 0 ? a.qout + (size_t)row * d : kdst;
+      __nv_bfloat16* dst = which == 0 ? a.qout + (size_t)lr * d : kdst;
 #pragma unroll
       for (int i = 0; i < VPL; ++i) {
         const int idx = li + 32 * WPR * i;
@@ -323,9 +327,11 @@ __global__ void __launch_bounds__(256) qk_norm_rope_kernel(const __nv_bfloat16* 
   }
   if (a.peer.n_peers > 0 && a.peer.push) {
     last_cta_publish(a.peer.ctr, [&] {
-      const int n = rows / T;
+      const int e_lo = a.row0 / T, e_hi = (a.row0 + rows - 1) / T;  // entries with rows here
       for (int p = 0; p < a.peer.n_peers; ++p)
-        for (int e2 = 0; e2 < n; ++e2) st_release_sys(a.peer.flags[p] + a.peer.flag_base + a.slot[e2], a.peer.epoch);
+        for (int e2 = e_lo; e2 <= e_hi; ++e2)
+          st_release_sys(a.peer.flags[p] + (size_t)(a.peer.flag_base + a.slot[e2]) * a.peer.n_ranks + a.peer.my_rank,
+                         a.peer.epoch);
     });
   }
 }
@@ -458,9 +464,10 @@ int grid_for(int64_t work, int threads) {
 
 }  // namespace
 
-int launch_patchify(const EntryPtrs& lat, int n, int F, int H, int W, __nv_bfloat16* out, cudaStream_t st) {
+int launch_patchify(const EntryPtrs& lat, int F, int H, int W, int row0, int rows, __nv_bfloat16* out,
+                    cudaStream_t st) {
   const int T = F * (H / 2) * (W / 2);
-  patchify_kernel<<<dim3(grid_for((int64_t)T * 64, 256) / n + 1, n), 256, 0, st>>>(lat, F, H, W, out, T);
+  patchify_kernel<<<grid_for((int64_t)rows * 64, 256), 256, 0, st>>>(lat, F, H, W, out, T, row0, rows);
   BC_LAUNCHED();
   return BC_OK;
 }

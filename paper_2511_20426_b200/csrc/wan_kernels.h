@@ -26,17 +26,19 @@ struct LnArgs {
   const float* pe_shift;
   const float* pe_scale;
   int entry_stride;
+  int row0;  // global batch row of local row 0 (entry = (row0 + row) / rows_per_entry)
 };
 
 // Multi-GPU temporal parallelism: every rank keeps a full KV-arena replica;
-// the q/k kernel pushes each fresh K/V row to every peer's arena over
-// NVLink (P2P stores) and the last CTA publishes (layer, slot) ready epochs
-// into each peer's flag array; iteration-done epochs guard slot reuse.
+// fresh K/V rows reach every peer's arena over NVLink (copy engines, or P2P
+// stores from the q/k kernel) and (layer, slot, producer rank) ready epochs
+// are published into each peer's flag array [L][n_slots][n_ranks];
+// iteration-done epochs guard slot reuse.
 #define BC_MAX_PEERS 8
 struct PeerArgs {
   int n_peers;                          // 0 = single GPU
   __nv_bfloat16* arena[BC_MAX_PEERS];   // peers' arenas (same layout as ours)
-  uint32_t* flags[BC_MAX_PEERS];        // peers' [L][n_slots] ready epochs
+  uint32_t* flags[BC_MAX_PEERS];        // peers' [L][n_slots][n_ranks] ready epochs
   uint32_t* done[BC_MAX_PEERS];         // peers' [n_ranks] iteration-done epochs
   const uint32_t* my_done;              // ours, written by peers
   int my_rank, n_ranks;
@@ -59,6 +61,7 @@ struct QkArgs {
   const float2* rope_f;  // [max_frames][22] cos/sin, time pairs
   const float2* rope_h;  // [hp][21]
   const float2* rope_w;  // [wp][21]
+  int row0;              // global batch row of local row 0
   PeerArgs peer;
 };
 
@@ -73,7 +76,9 @@ struct UpdArgs {
   PeerArgs peer;  // iteration-done signal (flags/arena unused)
 };
 
-int launch_patchify(const EntryPtrs& lat, int n, int F, int H, int W, __nv_bfloat16* out, cudaStream_t st);
+// tokens of global rows [row0, row0 + rows) of the concatenated batch
+int launch_patchify(const EntryPtrs& lat, int F, int H, int W, int row0, int rows, __nv_bfloat16* out,
+                    cudaStream_t st);
 int launch_gemv(const float* in, int n, int K, const __nv_bfloat16* W, const float* b, float* out, int N,
                 int act_in, int act_out, cudaStream_t st);
 int launch_timestep_sin(const TimeArgs& a, int n, float* out, int freq_dim, cudaStream_t st);

@@ -55,7 +55,9 @@ struct bc_wan_ctx {
     bc_wan_update upd;
     int32_t* status;
     uint32_t epoch;
-    int n, R;
+    int n, R;       // entries; rows of this launch (local slice of the batch's n*T rows)
+    int row0;       // global batch row of local row 0
+    bool rows_mode; // row-sharded multi-GPU step: Y rows are exchanged, every rank updates all latents
     double self_flops;
     bc::AttnArgs sa, ca;
     bc::QkArgs qa;
@@ -128,8 +130,9 @@ int check_dims(const bc_wan_dims& dm) {
   } while (0)
 
 int gemm(const void* A, const void* B, void* C, int M, int N, int K, int mode, const float* bias,
-         const float* gate, int gate_stride, int rows_per_gate, cudaStream_t st) {
-  bc::GemmArgs g{A, B, C, M, N, K, mode, bias, gate, gate_stride, rows_per_gate, 0, 0};
+         const float* gate, int gate_stride, int rows_per_gate, cudaStream_t st, int gate_row0 = 0) {
+  if (M == 0) return BC_OK;  // empty row slice (row-sharded multi-GPU step)
+  bc::GemmArgs g{A, B, C, M, N, K, mode, bias, gate, gate_stride, rows_per_gate, 0, 0, gate_row0};
   return bc::gemm_run(g, st);
 }
 
@@ -164,6 +167,18 @@ int timed(int cls, double flops, double bytes, cudaStream_t st, F&& f) {
   cudaEventRecord(b, st);
   g_recs.push_back({a, b, cls, flops, bytes});
   return rc;
+}
+
+PFN_cuStreamWaitValue32_v11070 wait_value32() {
+  static PFN_cuStreamWaitValue32_v11070 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuStreamWaitValue32_v11070>(p);
+  }
+  return fn;
 }
 
 PFN_cuStreamWriteValue32_v11070 write_value32() {
@@ -329,8 +344,19 @@ int stage_begin(bc_wan_ctx* c, const bc_batch* batch, const bc_wan_update* upd, 
   const bc_wan_dims& dm = c->dims;
   const bc_wan_params& p = c->prm;
   const int n = batch->n_entries;
-  const int d = c->d, T = c->T, R = n * T, L = dm.layers, F = dm.block_size;
+  const int d = c->d, T = c->T, L = dm.layers, F = dm.block_size;
   const int H = dm.latent_h, W = dm.latent_w;
+  const bool multi = c->peers.n_peers > 0 && dist;
+  // row-sharded step: this rank runs global rows [row0, row1) of the n*T
+  // concatenated rows (every entry of the iteration, a slice of its tokens)
+  S.rows_mode = multi && dist->row1 > 0;
+  S.row0 = S.rows_mode ? dist->row0 : 0;
+  const int row1 = S.rows_mode ? dist->row1 : n * T;
+  if (S.row0 < 0 || row1 > n * T || row1 < S.row0)
+    return bc_fail(BC_ERR_CONTRACT, "bc_wan_step_dist: bad row slice [%d, %d) of %d rows", S.row0, row1, n * T);
+  if (S.rows_mode && (!c->peers.my_y || !c->peers.my_yready))
+    return bc_fail(BC_ERR_CONTRACT, "bc_wan_step_dist: row-sharded steps need shared Y buffers (bc_wan_peers.my_y)");
+  const int R = row1 - S.row0;
   S.n = n;
   S.R = R;
 
@@ -340,7 +366,8 @@ int stage_begin(bc_wan_ctx* c, const bc_batch* batch, const bc_wan_update* upd, 
     lat.block[e] = batch->block_index[e];
   }
   RC(timed(kBandwidth, 0.0, 4.0 * n * F * 16 * H * W, st, [&] { return bc::launch_check_finite(lat, n, F * 16 * H * W, status, st); }));
-  RC(timed(kBandwidth, 0.0, 6.0 * R * 64, st, [&] { return bc::launch_patchify(lat, n, F, H, W, c->patches, st); }));
+  if (R > 0)
+    RC(timed(kBandwidth, 0.0, 6.0 * R * 64, st, [&] { return bc::launch_patchify(lat, F, H, W, S.row0, R, c->patches, st); }));
   RC(timed(kGemm, 2.0 * R * d * 64, 0.0, st, [&] { return gemm(c->patches, p.patch_w, c->X, R, d, 64, bc::kEpiStoreF32, p.patch_b, nullptr, 0, 1, st); }));
 
   // time embedding: e = W2 silu(W1 sin(t) + b1) + b2 ; e0 = Wp silu(e) + bp
@@ -368,14 +395,24 @@ int stage_begin(bc_wan_ctx* c, const bc_batch* batch, const bc_wan_update* upd, 
   sa.scale = 0.08838834764831845f;  // 1/sqrt(128)
   sa.q = c->Q;
   sa.out = c->attn;
-  const bool multi = c->peers.n_peers > 0 && dist;
   sa.flags = multi ? c->peers.my_flags : nullptr;
+  sa.n_ranks = multi ? c->peers.n_ranks : 1;
+  sa.ranged = 1;
+  sa.q_rows = R;
   for (int e = 0; e < n; ++e) {
     sa.n_vis[e] = batch->n_vis[e];
     for (int v = 0; v < batch->n_vis[e]; ++v) {
       sa.vis_slot[e][v] = batch->vis_slot[e][v];
-      sa.need[e][v] = multi ? dist->need[e][v] : 0u;
+      // packed wait word: epoch << 8 | producer-rank mask (0 = no wait)
+      const uint32_t ep = multi ? dist->need[e][v] : 0u, pm = multi ? dist->pmask[e][v] : 0u;
+      if (ep >= (1u << 24)) return bc_fail(BC_ERR_CONTRACT, "bc_wan_step_dist: epoch overflow");
+      sa.need[e][v] = (ep && pm) ? (ep << 8) | pm : 0u;
     }
+    const int lo = S.row0 - e * T > 0 ? S.row0 - e * T : 0;
+    const int hi = row1 - e * T < T ? row1 - e * T : T;
+    sa.q_lo[e] = hi > lo ? lo : 0;
+    sa.q_hi[e] = hi > lo ? hi : 0;
+    sa.q_row[e] = hi > lo ? e * T + lo - S.row0 : 0;
   }
   bc::AttnArgs& ca = S.ca;
   ca = sa;
@@ -396,6 +433,7 @@ int stage_begin(bc_wan_ctx* c, const bc_batch* batch, const bc_wan_update* upd, 
   qa.rope_f = c->rope_f;
   qa.rope_h = c->rope_h;
   qa.rope_w = c->rope_w;
+  qa.row0 = S.row0;
   for (int e = 0; e < n; ++e) {
     qa.slot[e] = batch->slot[e];
     qa.frame0[e] = batch->block_index[e] * F;
@@ -404,7 +442,8 @@ int stage_begin(bc_wan_ctx* c, const bc_batch* batch, const bc_wan_update* upd, 
   }
   if (multi) qa.peer = peer_args(c, S.epoch);
   S.self_flops = 0.0;
-  for (int e = 0; e < n; ++e) S.self_flops += 4.0 * T * ((double)batch->n_vis[e] * T) * d;
+  for (int e = 0; e < n; ++e)
+    S.self_flops += 4.0 * (sa.q_hi[e] - sa.q_lo[e]) * ((double)batch->n_vis[e] * T) * d;
   return BC_OK;
 }
 
@@ -416,10 +455,6 @@ int stage_layer_a(bc_wan_ctx* c, int l, cudaStream_t st) {
   const bc_wan_params& p = c->prm;
   const int d = c->d, T = c->T, R = S.R, n = S.n;
   const float* mod = c->mod_all + (size_t)l * n * 6 * d;  // [e][6][d]
-  bc::LnArgs ln{0, nullptr, nullptr, mod + 0 * d, mod + 1 * d, 6 * d};
-  RC(timed(kBandwidth, 0.0, 6.0 * R * d, st, [&] { return bc::launch_ln_rows(c->X, c->xn, R, d, T, ln, st); }));
-  RC(timed(kGemm, 2.0 * R * 3.0 * d * d, 0.0, st, [&] { return gemm(c->xn, at<__nv_bfloat16>(p.qkv_w, (int64_t)l * 3 * d * d), c->qkv, R, 3 * d, d, bc::kEpiStoreBf16,
-          p.qkv_b + (size_t)l * 3 * d, nullptr, 0, 1, st); }));
   bc::QkArgs& qa = S.qa;
   qa.mat_base = (int64_t)l * dm.n_slots * 2;
   qa.norm_q = p.norm_q + (size_t)l * d;
@@ -429,29 +464,49 @@ int stage_layer_a(bc_wan_ctx* c, int l, cudaStream_t st) {
   // reading the previous iteration's KV (slot reuse / in-place rewrite)
   qa.peer.wait_done = (l == 0 && S.epoch > 1) ? S.epoch - 1 : 0u;
   qa.peer.push = (c->peers.n_peers > 0 && !c->push_by_copy) ? 1 : 0;
-  RC(timed(kBandwidth, 0.0, 12.0 * R * d, st, [&] { return bc::launch_qk_norm_rope(c->qkv, R, d, T, qa, st); }));
+  if (R > 0) {
+    bc::LnArgs ln{0, nullptr, nullptr, mod + 0 * d, mod + 1 * d, 6 * d, S.row0};
+    RC(timed(kBandwidth, 0.0, 6.0 * R * d, st, [&] { return bc::launch_ln_rows(c->X, c->xn, R, d, T, ln, st); }));
+    RC(timed(kGemm, 2.0 * R * 3.0 * d * d, 0.0, st, [&] { return gemm(c->xn, at<__nv_bfloat16>(p.qkv_w, (int64_t)l * 3 * d * d), c->qkv, R, 3 * d, d, bc::kEpiStoreBf16,
+            p.qkv_b + (size_t)l * 3 * d, nullptr, 0, 1, st); }));
+    RC(timed(kBandwidth, 0.0, 12.0 * R * d, st, [&] { return bc::launch_qk_norm_rope(c->qkv, R, d, T, qa, st); }));
+  }
   if (c->peers.n_peers > 0 && c->push_by_copy && S.epoch > 0) {
-    // copy engines move each local entry's fresh K/V (layer l, one
-    // contiguous [2][T][d] slot matrix) into every peer replica, then a
-    // stream memory op publishes the (layer, slot) epoch -- no SM is needed,
-    // so a peer's spinning attention can never starve the transfer.
+    // copy engines move this rank's fresh K/V rows of layer l (per entry: the
+    // token range it computed, K and V halves of the slot's [2][T][d]
+    // matrix) into every peer replica, then a stream memory op publishes
+    // flags[layer][slot][my_rank] = epoch -- no SM is needed, so a peer's
+    // spinning attention can never starve the transfer.
     auto wv = write_value32();
     if (!wv) return bc_fail(BC_ERR_CUDA, "cuStreamWriteValue32 unavailable");
     BC_CUDA(cudaEventRecord(c->ev_qk, st));
     BC_CUDA(cudaStreamWaitEvent(c->side, c->ev_qk, 0));
-    const size_t mat_bytes = (size_t)T * d * sizeof(__nv_bfloat16);
+    const size_t row_bytes = (size_t)d * sizeof(__nv_bfloat16);
+    const size_t mat_bytes = (size_t)T * row_bytes;
+    int e_used[BC_MAX_ENTRIES];
+    int n_used = 0;
     for (int e = 0; e < n; ++e) {
+      const int lo = S.sa.q_lo[e], hi = S.sa.q_hi[e];
+      if (hi <= lo) continue;
+      e_used[n_used++] = e;
       const size_t off = ((size_t)qa.mat_base + (size_t)S.batch.slot[e] * 2) * mat_bytes;
-      for (int pp = 0; pp < c->peers.n_peers; ++pp)
-        BC_CUDA(cudaMemcpyAsync(static_cast<char*>(c->peers.peer_arena[pp]) + off,
-                                reinterpret_cast<const char*>(c->arena) + off, 2 * mat_bytes,
-                                cudaMemcpyDeviceToDevice, c->side));
+      for (int pp = 0; pp < c->peers.n_peers; ++pp) {
+        char* dst = static_cast<char*>(c->peers.peer_arena[pp]) + off;
+        const char* src = reinterpret_cast<const char*>(c->arena) + off;
+        if (lo == 0 && hi == T) {  // the whole block: one [2][T][d] copy
+          BC_CUDA(cudaMemcpyAsync(dst, src, 2 * mat_bytes, cudaMemcpyDeviceToDevice, c->side));
+        } else {                   // a token range: K rows and V rows
+          const size_t r0 = (size_t)lo * row_bytes, nb = (size_t)(hi - lo) * row_bytes;
+          BC_CUDA(cudaMemcpyAsync(dst + r0, src + r0, nb, cudaMemcpyDeviceToDevice, c->side));
+          BC_CUDA(cudaMemcpyAsync(dst + mat_bytes + r0, src + mat_bytes + r0, nb, cudaMemcpyDeviceToDevice,
+                                  c->side));
+        }
+      }
     }
     for (int pp = 0; pp < c->peers.n_peers; ++pp)
-      for (int e = 0; e < n; ++e) {
-        CUresult rr = wv((CUstream)c->side,
-                         (CUdeviceptr)(c->peers.peer_flags[pp] + (size_t)l * dm.n_slots + S.batch.slot[e]), S.epoch,
-                         0);
+      for (int k = 0; k < n_used; ++k) {
+        const size_t fi = ((size_t)l * dm.n_slots + S.batch.slot[e_used[k]]) * c->peers.n_ranks + c->peers.my_rank;
+        CUresult rr = wv((CUstream)c->side, (CUdeviceptr)(c->peers.peer_flags[pp] + fi), S.epoch, 0);
         if (rr != CUDA_SUCCESS) return bc_fail(BC_ERR_CUDA, "cuStreamWriteValue32 failed (%d)", (int)rr);
       }
   }
@@ -463,14 +518,15 @@ int stage_layer_b(bc_wan_ctx* c, int l, cudaStream_t st) {
   StepState& S = c->step;
   const bc_wan_dims& dm = c->dims;
   const bc_wan_params& p = c->prm;
-  const int d = c->d, T = c->T, R = S.R, n = S.n;
+  const int d = c->d, T = c->T, R = S.R, n = S.n, r0 = S.row0;
+  if (R == 0) return BC_OK;
   const float* mod = c->mod_all + (size_t)l * n * 6 * d;
   S.sa.mat_base = l * dm.n_slots * 2;
   S.sa.flag_base = l * dm.n_slots;
   RC(timed(kSelfAttn, S.self_flops, 0.0, st, [&] { return bc::attention_run(S.sa, st); }));
   RC(timed(kGemm, 2.0 * R * d * d, 0.0, st, [&] { return gemm(c->attn, at<__nv_bfloat16>(p.o_w, (int64_t)l * d * d), c->X, R, d, d, bc::kEpiResidualF32,
-          p.o_b + (size_t)l * d, mod + 2 * d, 6 * d, T, st); }));
-  bc::LnArgs ln3{1, p.norm3_b + (size_t)l * d, p.norm3_w + (size_t)l * d, nullptr, nullptr, 0};
+          p.o_b + (size_t)l * d, mod + 2 * d, 6 * d, T, st, r0); }));
+  bc::LnArgs ln3{1, p.norm3_b + (size_t)l * d, p.norm3_w + (size_t)l * d, nullptr, nullptr, 0, r0};
   RC(timed(kBandwidth, 0.0, 6.0 * R * d, st, [&] { return bc::launch_ln_rows(c->X, c->xn, R, d, T, ln3, st); }));
   RC(timed(kGemm, 2.0 * R * d * d, 0.0, st, [&] { return gemm(c->xn, at<__nv_bfloat16>(p.cq_w, (int64_t)l * d * d), c->Q, R, d, d, bc::kEpiStoreBf16,
           p.cq_b + (size_t)l * d, nullptr, 0, 1, st); }));
@@ -479,24 +535,60 @@ int stage_layer_b(bc_wan_ctx* c, int l, cudaStream_t st) {
   RC(timed(kCrossAttn, 4.0 * R * (double)dm.text_len * d, 0.0, st, [&] { return bc::attention_run(S.ca, st); }));
   RC(timed(kGemm, 2.0 * R * d * d, 0.0, st, [&] { return gemm(c->attn, at<__nv_bfloat16>(p.co_w, (int64_t)l * d * d), c->X, R, d, d, bc::kEpiResidualF32,
           p.co_b + (size_t)l * d, nullptr, 0, 1, st); }));
-  bc::LnArgs ln2{0, nullptr, nullptr, mod + 3 * d, mod + 4 * d, 6 * d};
+  bc::LnArgs ln2{0, nullptr, nullptr, mod + 3 * d, mod + 4 * d, 6 * d, r0};
   RC(timed(kBandwidth, 0.0, 6.0 * R * d, st, [&] { return bc::launch_ln_rows(c->X, c->xn, R, d, T, ln2, st); }));
   RC(timed(kGemm, 2.0 * R * (double)dm.ffn_dim * d, 0.0, st, [&] { return gemm(c->xn, at<__nv_bfloat16>(p.ffn1_w, (int64_t)l * dm.ffn_dim * d), c->H1, R, dm.ffn_dim, d,
           bc::kEpiGeluBf16, p.ffn1_b + (size_t)l * dm.ffn_dim, nullptr, 0, 1, st); }));
   RC(timed(kGemm, 2.0 * R * (double)dm.ffn_dim * d, 0.0, st, [&] { return gemm(c->H1, at<__nv_bfloat16>(p.ffn2_w, (int64_t)l * d * dm.ffn_dim), c->X, R, d, dm.ffn_dim,
-          bc::kEpiResidualF32, p.ffn2_b + (size_t)l * d, mod + 5 * d, 6 * d, T, st); }));
+          bc::kEpiResidualF32, p.ffn2_b + (size_t)l * d, mod + 5 * d, 6 * d, T, st, r0); }));
   return BC_OK;
 }
 
-// stage 3: head LN + modulation -> head GEMM -> unpatchify + x0 + renoise/emit
-int stage_end(bc_wan_ctx* c, cudaStream_t st) {
+// stage 3: head LN + modulation -> head GEMM (this rank's rows of Y); a
+// row-sharded step pushes its Y rows into every peer's Y and publishes
+// yready[my_rank] = epoch there
+int stage_head(bc_wan_ctx* c, cudaStream_t st) {
+  StepState& S = c->step;
+  const bc_wan_params& p = c->prm;
+  const int d = c->d, T = c->T, R = S.R;
+  float* y = c->Y + (size_t)S.row0 * 64;
+  if (R > 0) {
+    bc::LnArgs lh{0, p.head_mod, p.head_mod + d, c->t_e, c->t_e, d, S.row0};
+    RC(timed(kBandwidth, 0.0, 6.0 * R * d, st, [&] { return bc::launch_ln_rows(c->X, c->xn, R, d, T, lh, st); }));
+    RC(timed(kGemm, 2.0 * R * 64.0 * d, 0.0, st, [&] { return gemm(c->xn, p.head_w, y, R, 64, d, bc::kEpiStoreF32, p.head_b, nullptr, 0, 1, st); }));
+  }
+  if (S.rows_mode) {
+    auto wv = write_value32();
+    if (!wv) return bc_fail(BC_ERR_CUDA, "cuStreamWriteValue32 unavailable");
+    BC_CUDA(cudaEventRecord(c->ev_qk, st));
+    BC_CUDA(cudaStreamWaitEvent(c->side, c->ev_qk, 0));
+    for (int pp = 0; pp < c->peers.n_peers; ++pp) {
+      if (R > 0)
+        BC_CUDA(cudaMemcpyAsync(static_cast<float*>(c->peers.peer_y[pp]) + (size_t)S.row0 * 64, y,
+                                (size_t)R * 64 * sizeof(float), cudaMemcpyDeviceToDevice, c->side));
+      CUresult rr = wv((CUstream)c->side, (CUdeviceptr)(c->peers.peer_yready[pp] + c->peers.my_rank), S.epoch, 0);
+      if (rr != CUDA_SUCCESS) return bc_fail(BC_ERR_CUDA, "cuStreamWriteValue32 failed (%d)", (int)rr);
+    }
+  }
+  return BC_OK;
+}
+
+// stage 4: unpatchify + x0 + renoise/emit of every entry of this launch (a
+// row-sharded step first waits for every peer's Y rows: each rank then
+// updates ALL latents identically, so latents never move between GPUs)
+int stage_update(bc_wan_ctx* c, cudaStream_t st) {
   StepState& S = c->step;
   const bc_wan_dims& dm = c->dims;
-  const bc_wan_params& p = c->prm;
-  const int d = c->d, T = c->T, R = S.R, n = S.n, F = dm.block_size;
-  bc::LnArgs lh{0, p.head_mod, p.head_mod + d, c->t_e, c->t_e, d};
-  RC(timed(kBandwidth, 0.0, 6.0 * R * d, st, [&] { return bc::launch_ln_rows(c->X, c->xn, R, d, T, lh, st); }));
-  RC(timed(kGemm, 2.0 * R * 64.0 * d, 0.0, st, [&] { return gemm(c->xn, p.head_w, c->Y, R, 64, d, bc::kEpiStoreF32, p.head_b, nullptr, 0, 1, st); }));
+  const int T = c->T, n = S.n, F = dm.block_size;
+  if (S.rows_mode) {
+    auto wt = wait_value32();
+    if (!wt) return bc_fail(BC_ERR_CUDA, "cuStreamWaitValue32 unavailable");
+    for (int r = 0; r < c->peers.n_ranks; ++r) {
+      if (r == c->peers.my_rank) continue;
+      CUresult rr = wt((CUstream)st, (CUdeviceptr)(c->peers.my_yready + r), S.epoch, CU_STREAM_WAIT_VALUE_GEQ);
+      if (rr != CUDA_SUCCESS) return bc_fail(BC_ERR_CUDA, "cuStreamWaitValue32 failed (%d)", (int)rr);
+    }
+  }
   bc::UpdArgs u{};
   for (int e = 0; e < n; ++e) {
     u.latents[e] = S.upd.latents[e];
@@ -509,13 +601,19 @@ int stage_end(bc_wan_ctx* c, cudaStream_t st) {
   }
   if (c->peers.n_peers > 0 && S.epoch > 0) {
     u.peer = peer_args(c, S.epoch);
-    if (c->push_by_copy) {  // this iteration's pushes are ordered before our done signal
+    if (c->push_by_copy || S.rows_mode) {  // this iteration's pushes are ordered before our done signal
       BC_CUDA(cudaEventRecord(c->ev_side, c->side));
       BC_CUDA(cudaStreamWaitEvent(st, c->ev_side, 0));
     }
   }
+  const int R = n * T;  // Y holds every entry's rows here
   RC(timed(kBandwidth, 0.0, (4.0 * 64 + 16.0 * 16) * R, st, [&] { return bc::launch_head_update(c->Y, n, T, F, dm.latent_h, dm.latent_w, u, S.status, st); }));
   return BC_OK;
+}
+
+int stage_end(bc_wan_ctx* c, cudaStream_t st) {
+  RC(stage_head(c, st));
+  return stage_update(c, st);
 }
 
 }  // namespace
@@ -544,6 +642,13 @@ extern "C" int bc_wan_set_peers(bc_wan_ctx* c, const bc_wan_peers* peers) {
   for (int p = 0; p < peers->n_peers; ++p)
     if (!peers->peer_arena[p] || !peers->peer_flags[p] || !peers->peer_done[p])
       return bc_fail(BC_ERR_CONTRACT, "bc_wan_set_peers: null peer pointer");
+  if (peers->my_y) {  // row-sharded steps: Y lives in memory the peers can write
+    if (!peers->my_yready) return bc_fail(BC_ERR_CONTRACT, "bc_wan_set_peers: my_y needs my_yready");
+    for (int p = 0; p < peers->n_peers; ++p)
+      if (!peers->peer_y[p] || !peers->peer_yready[p])
+        return bc_fail(BC_ERR_CONTRACT, "bc_wan_set_peers: null peer Y pointer");
+    c->Y = peers->my_y;
+  }
   c->peers = *peers;
   const char* how = getenv("BC_KV_PUSH");  // "kernel": P2P stores inside the q/k kernel
   c->push_by_copy = !(how && std::strcmp(how, "kernel") == 0);
@@ -580,7 +685,9 @@ extern "C" int bc_wan_step_dist(bc_wan_ctx* c, const bc_batch* batch, const bc_w
     case 2:
       return stage_layer_b(c, dist->layer, st);
     case 3:
-      return stage_end(c, st);
+      return stage_head(c, st);
+    case 4:
+      return stage_update(c, st);
   }
   return bc_fail(BC_ERR_CONTRACT, "bc_wan_step_dist: bad stage %d", dist->stage);
 }

@@ -1,22 +1,35 @@
-"""Multi-GPU temporal parallelism: one process per GPU.
+"""Multi-GPU temporal parallelism: one process
+per GPU.
 
-Units are the in-flight blocks of an iteration; a block is owned by rank
-``block % world`` for its whole life (so its latents never move -- outputs do
-not depend on the placement, the trace keeps the reference's positional
-``worker`` label).  Every rank runs the same host loop (scheduler, pool
-index, slot allocator are deterministic, so all ranks agree on slots) and
-executes only its own entries.  There is one exchange per layer: the q/k
-kernel of the owner writes the block's fresh K/V into its slot on *every*
-rank (NVLink P2P stores into IPC-mapped peer arenas) and publishes a
-``(layer, slot) -> epoch`` flag; a consumer's attention waits for the flag of
-a visible slot only before that slot's first key tile.  Pool slots come first
-in the ascending gather order, so the transfer overlaps the pool part of the
-attention and the summation order is the same for any world size.
+Every rank runs the same host loop (scheduler, pool index and slot
+allocator are deterministic, so all ranks agree on slots) and keeps a full
+KV-arena replica.  An iteration's work is partitioned in one of two ways
+(``BC_TEMPORAL_SHARD``):
 
-Host-side logic here is pure (``owner``, ``rank_entries``, ``need_table``) and
-covered by multi-process ``gloo`` tests on CPU; the device part is exercised
-on one GPU by :class:`EmulatedRanks`, which steps G rank contexts
-layer-interleaved on a single stream.
+* ``rows`` (default): every rank runs EVERY in-flight entry, but only a
+  contiguous slice of the batch's n*T concatenated query rows (balanced in
+  128-row query tiles, :func:`row_slices`).  Any world size is load
+  balanced, including G > cascade width (8 GPUs for a width-5 cascade) and
+  the fill/drain iterations.  A rank's fresh K/V rows go to every peer
+  replica; its head-GEMM rows (Y, 64 floats per token) go to every peer's
+  Y; every rank then applies the same flow->x0 + renoise to every entry, so
+  latents are replicated and never move.
+* ``blocks``: block ``b`` is executed by rank ``b % world`` for its whole
+  life (whole entries per rank; ranks beyond the width idle).
+
+In both, the exchange is one per layer: fresh K/V rows reach the peers'
+replicas over NVLink (copy engines + a stream memory op publishing
+``flags[layer][slot][producer] = epoch``), and a consumer's attention waits
+for the flags of a visible slot's producers only before that slot's first
+key tile.  Pool slots come first in the ascending gather order, so the
+transfer overlaps the pool part of the attention, and the summation order
+(and every row's arithmetic) is the same for any world size: outputs are
+bit-identical for every G and either partition.
+
+Host-side logic here is pure (``owner``, ``rank_entries``, ``row_slices``,
+``need_table``) and covered by multi-process ``gloo`` tests on CPU; the
+device part is exercised on one GPU by :class:`EmulatedRanks`, which steps G
+rank contexts stage-interleaved on a single stream.
 """
 
 from __future__ import annotations
@@ -31,6 +44,15 @@ from .errors import ContractViolation, InvalidInputError
 
 # Tests flip this to run `workers > 1` sessions as emulated ranks on one GPU.
 EMULATE = os.environ.get("BC_EMULATE_RANKS", "0") == "1"
+ROW_TILE = 128  # query rows per attention tile: the unit of the rows partition
+ROW_UNIT_SMALL = 16  # unit when a batch has fewer than 2 tiles per rank
+
+
+def shard_mode() -> str:
+    m = os.environ.get("BC_TEMPORAL_SHARD", "rows")
+    if m not in ("rows", "blocks"):
+        raise InvalidInputError(f"BC_TEMPORAL_SHARD must be 'rows' or 'blocks', not {m!r}")
+    return m
 
 
 def owner(block: int, world: int) -> int:
@@ -38,58 +60,112 @@ def owner(block: int, world: int) -> int:
 
 
 def rank_entries(blocks, world: int, rank: int) -> list:
-    """Positions (in plan order) of the entries this rank executes."""
+    """blocks partition: positions (in plan order) of this rank's entries."""
     return [i for i, b in enumerate(blocks) if owner(b, world) == rank]
 
 
-def need_table(local_blocks, vis_lists_local, batch_blocks, slot_epoch: dict, epoch: int,
-               world: int, rank: int, slot_of) -> list:
-    """Per local entry, per visible block: the flag epoch to wait for before
-    reading that slot (0 = written by this rank, stream-ordered).  Fresh
-    batch blocks of other ranks need this iteration's epoch; pool blocks
-    need the epoch of the iteration that last wrote them (their cache pass)."""
-    fresh = set(batch_blocks)
-    table = []
-    for lst in vis_lists_local:
-        row = []
-        for vb in lst:
-            if owner(vb, world) == rank:
-                row.append(0)
-            elif vb in fresh:
-                row.append(epoch)
-            else:
-                row.append(int(slot_epoch[slot_of(vb)]))
-        table.append(row)
-    return table
+def row_slices(n: int, T: int, world: int) -> list:
+    """rows partition: per rank the global row slice [r0, r1) of the n*T
+    concatenated rows.  The unit is a query tile (128 rows, the last tile of
+    an entry shorter); rank r gets tiles [r*K/G, (r+1)*K/G).  Tiny blocks
+    (fewer than 2 tiles per rank) fall back to 16-row units so every rank
+    still gets rows.  An empty slice is (n*T, n*T)."""
+    unit = ROW_TILE if n * -(-T // ROW_TILE) >= 2 * world else ROW_UNIT_SMALL
+    tiles = [(e * T + t, e * T + min(t + unit, T)) for e in range(n) for t in range(0, T, unit)]
+    K = len(tiles)
+    out = []
+    for r in range(world):
+        a, b = r * K // world, (r + 1) * K // world
+        out.append((tiles[a][0], tiles[b - 1][1]) if b > a else (n * T, n * T))
+    return out
+
+
+def entry_producers(slices, n: int, T: int) -> list:
+    """rows partition: per entry position, the bit mask of ranks whose slice
+    holds some of its rows (they write its K/V)."""
+    masks = []
+    for i in range(n):
+        lo, hi = i * T, (i + 1) * T
+        m = 0
+        for r, (a, b) in enumerate(slices):
+            if a < hi and b > lo:
+                m |= 1 << r
+        masks.append(m)
+    return masks
 
 
 class SlotEpochs:
-    """Epoch of the last write of every arena slot (identical on all ranks)."""
+    """Epoch of the last write of every arena slot and the ranks that wrote
+    it (identical on all ranks)."""
 
     def __init__(self, n_slots):
         self.epoch = np.zeros(n_slots, dtype=np.int64)
+        self.mask = np.zeros(n_slots, dtype=np.int64)
 
     def __getitem__(self, slot):
         return self.epoch[slot]
 
-    def wrote(self, slots, epoch):
-        for s in slots:
+    def wrote(self, slots, epoch, masks=None):
+        for i, s in enumerate(slots):
             self.epoch[s] = epoch
+            if masks is not None:
+                self.mask[s] = masks[i]
 
 
-def make_dist(epoch: int, need_rows, stage: int = -1, layer: int = 0):
+def need_table(local_blocks, vis_lists_local, batch_blocks, slot_epoch: SlotEpochs, epoch: int,
+               world: int, rank: int, slot_of, producers=None) -> tuple:
+    """Per local entry, per visible block: (epoch to wait for, producer-rank
+    mask) before reading that slot.  Rows written by this rank are stream-
+    ordered (not in the mask).  Fresh batch blocks need this iteration's
+    epoch from their producers this iteration; pool blocks need the epoch of
+    the iteration that last wrote them, from the ranks that wrote it then.
+    ``producers``: block -> mask this iteration (rows partition); None =
+    blocks partition (the owner is the only producer)."""
+    fresh = set(batch_blocks)
+    me = 1 << rank
+    need, pmask = [], []
+    for lst in vis_lists_local:
+        nrow, mrow = [], []
+        for vb in lst:
+            s = slot_of(vb)
+            if producers is None:
+                m = (1 << owner(vb, world)) & ~me
+                ep = epoch if vb in fresh else int(slot_epoch[s])
+            elif vb in fresh:
+                m, ep = producers[vb] & ~me, epoch
+            else:
+                m, ep = int(slot_epoch.mask[s]) & ~me, int(slot_epoch[s])
+            nrow.append(ep if m else 0)
+            mrow.append(m if m else 0)
+        need.append(nrow)
+        pmask.append(mrow)
+    return need, pmask
+
+
+def make_dist(epoch: int, need_rows, pmask_rows, stage: int = -1, layer: int = 0, rows=None):
     d = N.WanDist()
     d.epoch = epoch
     d.stage = stage
     d.layer = layer
-    for e, row in enumerate(need_rows):
-        for v, x in enumerate(row):
+    for e, (nrow, mrow) in enumerate(zip(need_rows, pmask_rows)):
+        for v, (x, m) in enumerate(zip(nrow, mrow)):
             d.need[e][v] = int(x)
+            d.pmask[e][v] = int(m)
+    if rows is not None:
+        d.row0, d.row1 = rows
     return d
 
 
+def flag_layout(L: int, n_slots: int, world: int) -> dict:
+    """u32 word offsets in a rank's flag buffer:
+    [L][n_slots][world] K/V ready | done[world] | yready[world] | counters[4]."""
+    kv = L * n_slots * world
+    return {"done": kv, "yready": kv + world, "counters": kv + 2 * world, "words": kv + 2 * world + 4}
+
+
 class _RankState:
-    """Device buffers of one rank: arena, flags, done, counters + context."""
+    """Device buffers of one rank: arena, flags (+done, yready, counters), Y
+    (rows partition) + context."""
 
     def __init__(self, weights, cfg, max_entries, n_slots, world, rank, ipc: bool):
         torch = N.torch_mod()
@@ -97,43 +173,47 @@ class _RankState:
         self.world, self.rank = world, rank
         self.ipc = ipc
         L = cfg.layers
-        flag_words = L * n_slots + world + 4
+        self.lay = flag_layout(L, n_slots, world)
+        y_bytes = max_entries * cfg.tokens_per_block * 64 * 4
         if ipc:
             self.arena_bytes = L * n_slots * 2 * cfg.tokens_per_block * cfg.model_dim * 2
             self.arena_ptr, self.arena_handle = _ipc_alloc(self.arena_bytes)
-            self.flags_ptr, self.flags_handle = _ipc_alloc(flag_words * 4)
+            self.flags_ptr, self.flags_handle = _ipc_alloc(self.lay["words"] * 4)
+            self.y_ptr, self.y_handle = _ipc_alloc(y_bytes)
             arena = _raw_tensor(self.arena_ptr, (L, n_slots, 2, cfg.tokens_per_block, cfg.model_dim),
                                 torch.bfloat16)
         else:
             arena = torch.zeros((L, n_slots, 2, cfg.tokens_per_block, cfg.model_dim),
                                 dtype=torch.bfloat16, device="cuda")
-            self.flag_buf = torch.zeros(flag_words, dtype=torch.int32, device="cuda")
+            self.flag_buf = torch.zeros(self.lay["words"], dtype=torch.int32, device="cuda")
+            self.y_buf = torch.zeros(y_bytes // 4, dtype=torch.float32, device="cuda")
             self.arena_ptr, self.flags_ptr = N.ptr(arena), N.ptr(self.flag_buf)
+            self.y_ptr = N.ptr(self.y_buf)
         self.ctx = _Ctx(weights, max_entries, n_slots, arena=arena)
         self.L, self.n_slots = L, n_slots
 
-    def my_flags(self):
-        return self.flags_ptr
+    def word(self, name, base=None):
+        return (self.flags_ptr if base is None else base) + 4 * self.lay[name]
 
-    def my_done(self):
-        return self.flags_ptr + 4 * self.L * self.n_slots
-
-    def counters(self):
-        return self.my_done() + 4 * self.world
-
-    def attach(self, peers):
-        """peers: list of (rank, arena_ptr, flags_ptr) for every other rank."""
+    def attach(self, peers, rows: bool):
+        """peers: list of (rank, arena_ptr, flags_ptr, y_ptr) for every other rank."""
         P = N.WanPeers()
         P.n_peers = len(peers)
         P.my_rank = self.rank
         P.n_ranks = self.world
-        for i, (r, arena, flags) in enumerate(peers):
+        for i, (r, arena, flags, y) in enumerate(peers):
             P.peer_arena[i] = arena
             P.peer_flags[i] = flags
-            P.peer_done[i] = flags + 4 * self.L * self.n_slots
-        P.my_flags = self.my_flags()
-        P.my_done = self.my_done()
-        P.counters = self.counters()
+            P.peer_done[i] = self.word("done", flags)
+            if rows:
+                P.peer_y[i] = y
+                P.peer_yready[i] = self.word("yready", flags)
+        P.my_flags = self.flags_ptr
+        P.my_done = self.word("done")
+        P.counters = self.word("counters")
+        if rows:
+            P.my_y = self.y_ptr
+            P.my_yready = self.word("yready")
         N.check(N.lib().bc_wan_set_peers(self.ctx.handle, P), "bc_wan_set_peers")
 
 
@@ -163,6 +243,85 @@ def _raw_tensor(ptr, shape, dtype):
     return t.view(dtype) if dtype == torch.bfloat16 else t
 
 
+class _RankWork:
+    """Host-side step description of one rank (shared by the real and the
+    emulated multi-rank sessions)."""
+
+    def __init__(self, mode, plan, vis_lists, posts, world, rank, slots, slot_epoch, epoch, T):
+        blocks = plan.blocks
+        n = len(blocks)
+        self.rows = None
+        producers = None
+        if mode == "rows":
+            sl = row_slices(n, T, world)
+            masks = entry_producers(sl, n, T)
+            producers = dict(zip(blocks, masks))
+            self.local = list(range(n))
+            self.rows = sl[rank]
+            self.masks = masks
+        else:
+            self.local = rank_entries(blocks, world, rank)
+            self.masks = [1 << owner(b, world) for b in blocks]
+        lb = [blocks[i] for i in self.local]
+        vis_local = [vis_lists[i] for i in self.local]
+        self.blocks = lb
+        self.need, self.pmask = need_table(lb, vis_local, blocks, slot_epoch, epoch, world, rank,
+                                           slots.slot_of, producers)
+        self.vis_local = vis_local
+        self.epoch = epoch
+
+    def dist(self, stage=-1, layer=0):
+        return make_dist(self.epoch, self.need, self.pmask, stage, layer, self.rows)
+
+
+class _Replica:
+    """Per-rank latents / noise / outputs of a session.  In the rows
+    partition every rank holds every in-flight block's latents (it applies
+    the same update to all of them); in the blocks partition only its own."""
+
+    def __init__(self, torch, cfg, width):
+        self.torch = torch
+        self.shape = (cfg.block_size, cfg.latent_channels, cfg.latent_height, cfg.latent_width)
+        self.latents, self.final = {}, {}
+        self.eps = [torch.empty(self.shape, dtype=torch.float32, device="cuda") for _ in range(width)]
+
+    def prepare(self, plan, posts, local, init_req, init_dst, eps_req, eps_dst):
+        """Allocates this step's buffers; returns (latents, eps, outs, next_levels) per local entry."""
+        from .wan import POST_EMIT, POST_RENOISE
+        torch = self.torch
+        lats, eps, outs, nexts = [], [], [], []
+        for k, i in enumerate(local):
+            e = plan.entries[i]
+            kind, next_pass, next_level = posts[i]
+            b = e.block_index
+            if e.pass_index == 0 and b not in self.latents:
+                t = torch.empty(self.shape, dtype=torch.float32, device="cuda")
+                self.latents[b] = t
+                init_req.append((b, 0))
+                init_dst.append(t)
+            lats.append(self.latents[b])
+            if kind == POST_RENOISE:
+                eps_req.append((b, next_pass))
+                eps_dst.append(self.eps[k])
+                eps.append(self.eps[k])
+            else:
+                eps.append(None)
+            if kind == POST_EMIT:
+                out = torch.empty(self.shape, dtype=torch.float32, device="cuda")
+                self.final[b] = out
+                outs.append(out)
+            else:
+                outs.append(None)
+            nexts.append(next_level)
+        return lats, eps, outs, nexts
+
+    def retire(self, plan, posts, local):
+        from .wan import POST_CACHE
+        for i in local:
+            if posts[i][0] == POST_CACHE:
+                self.latents.pop(plan.entries[i].block_index, None)
+
+
 class DistWanSession:
     """Engine session for one rank of a torch.distributed job (one GPU per
     process).  Implements the same protocol as :class:`wan.WanSession`."""
@@ -174,34 +333,34 @@ class DistWanSession:
         torch = N.torch_mod()
         self.torch, self.dist = torch, dist
         self.cfg = config
+        self.mode = shard_mode()
         self.world, self.rank = dist.get_world_size(), dist.get_rank()
         width = min(config.cascade_width, config.num_blocks)
         n_slots = config.window_blocks + config.sink_blocks + width + 1
         self.state = _RankState(rt.weights, config, width, n_slots, self.world, self.rank, ipc=True)
-        mine = (self.rank, self.state.arena_handle, self.state.flags_handle)
+        mine = (self.rank, self.state.arena_handle, self.state.flags_handle, self.state.y_handle)
         everyone = [None] * self.world
         dist.all_gather_object(everyone, mine)
         self._opened = []
         peers = []
-        for r, ah, fh in everyone:
+        for r, ah, fh, yh in everyone:
             if r == self.rank:
                 continue
-            a, f = _ipc_open(ah), _ipc_open(fh)
-            self._opened += [a, f]
-            peers.append((r, a, f))
-        self.state.attach(peers)
+            a, f, y = _ipc_open(ah), _ipc_open(fh), _ipc_open(yh)
+            self._opened += [a, f, y]
+            peers.append((r, a, f, y))
+        self.state.attach(peers, rows=self.mode == "rows")
         dist.barrier()
         self.slots = SlotAllocator(n_slots)
         self.slot_epoch = SlotEpochs(n_slots)
-        self.shape = (config.block_size, config.latent_channels, config.latent_height,
-                      config.latent_width)
+        self.rep = _Replica(torch, config, width)
+        self.shape = self.rep.shape
         self.noise = noise_feed if noise_feed is not None else HostNoiseFeed(session_seed, config)
-        self.latents, self.final, self.tags, self.host_out = {}, {}, {}, {}
+        self.tags, self.host_out = {}, {}
         # one pinned staging area for every emitted block (no per-emission
         # cudaHostAlloc, which would serialise against the device)
         self.host_buf = torch.empty((config.num_blocks,) + tuple(self.shape),
                                     dtype=torch.float32).pin_memory()
-        self.eps = [torch.empty(self.shape, dtype=torch.float32, device="cuda") for _ in range(width)]
         self.events = []
         self.set_conditioning(conditioning)
         self._mark()
@@ -226,62 +385,38 @@ class DistWanSession:
         self.state.ctx.set_text(cond)
 
     def step(self, plan, mask, pool, vis_lists, posts):
-        from .wan import POST_CACHE, POST_EMIT, POST_RENOISE, _make_update
-        torch = self.torch
+        from .wan import POST_EMIT, _make_update
         epoch = plan.iteration + 1
         blocks = plan.blocks
         for b in blocks:
             self.slots.acquire(b)
-        local = rank_entries(blocks, self.world, self.rank)
-        if not local:
+        work = _RankWork(self.mode, plan, vis_lists, posts, self.world, self.rank, self.slots,
+                         self.slot_epoch, epoch, self.cfg.tokens_per_block)
+        if not work.local:
             N.check(N.lib().bc_wan_signal_done(self.state.ctx.handle, epoch, N.stream_ptr()),
                     "bc_wan_signal_done")
         else:
-            init_req, init_dst, eps_req, eps_dst, eps_ptrs, outs, nexts = [], [], [], [], [], [], []
-            for k, i in enumerate(local):
-                e = plan.entries[i]
-                kind, next_pass, next_level = posts[i]
-                if e.pass_index == 0 and e.block_index not in self.latents:
-                    t = torch.empty(self.shape, dtype=torch.float32, device="cuda")
-                    self.latents[e.block_index] = t
-                    init_req.append((e.block_index, 0))
-                    init_dst.append(t)
-                if kind == POST_RENOISE:
-                    eps_req.append((e.block_index, next_pass))
-                    eps_dst.append(self.eps[k])
-                    eps_ptrs.append(self.eps[k])
-                else:
-                    eps_ptrs.append(None)
-                if kind == POST_EMIT:
-                    out = torch.empty(self.shape, dtype=torch.float32, device="cuda")
-                    self.final[e.block_index] = out
-                    outs.append(out)
-                else:
-                    outs.append(None)
-                nexts.append(next_level)
+            init_req, init_dst, eps_req, eps_dst = [], [], [], []
+            lats, eps, outs, nexts = self.rep.prepare(plan, posts, work.local, init_req, init_dst,
+                                                      eps_req, eps_dst)
             if init_req or eps_req:
                 self.noise.fetch(init_req + eps_req, init_dst + eps_dst)
-            lb = [blocks[i] for i in local]
-            vis_local = [vis_lists[i] for i in local]
-            bt = N.make_batch(self.cfg.block_size, lb, [plan.entries[i].noise_level for i in local],
-                              [self.slots.slot_of(b) for b in lb],
-                              [[self.slots.slot_of(v) for v in lst] for lst in vis_local])
-            need = need_table(lb, vis_local, blocks, self.slot_epoch, epoch, self.world, self.rank,
-                              self.slots.slot_of)
-            upd = _make_update([posts[i][0] for i in local], [self.latents[b] for b in lb], eps_ptrs,
-                               outs, nexts)
-            N.check(N.lib().bc_wan_step_dist(self.state.ctx.handle, bt, upd, make_dist(epoch, need),
+            bt = N.make_batch(self.cfg.block_size, work.blocks,
+                              [plan.entries[i].noise_level for i in work.local],
+                              [self.slots.slot_of(b) for b in work.blocks],
+                              [[self.slots.slot_of(v) for v in lst] for lst in work.vis_local])
+            upd = _make_update([posts[i][0] for i in work.local], lats, eps, outs, nexts)
+            N.check(N.lib().bc_wan_step_dist(self.state.ctx.handle, bt, upd, work.dist(),
                                              N.ptr(self.state.ctx.status), N.stream_ptr()),
                     "bc_wan_step_dist")
-            for k, i in enumerate(local):
-                e = plan.entries[i]
+            for i in work.local:
+                b = plan.entries[i].block_index
                 if posts[i][0] == POST_EMIT:
-                    host = self.host_buf[e.block_index]
-                    host.copy_(self.final[e.block_index], non_blocking=True)
-                    self.host_out[e.block_index] = host
-                elif posts[i][0] == POST_CACHE:
-                    self.latents.pop(e.block_index, None)
-        self.slot_epoch.wrote([self.slots.slot_of(b) for b in blocks], epoch)
+                    host = self.host_buf[b]
+                    host.copy_(self.rep.final[b], non_blocking=True)
+                    self.host_out[b] = host
+            self.rep.retire(plan, posts, work.local)
+        self.slot_epoch.wrote([self.slots.slot_of(b) for b in blocks], epoch, work.masks)
         for e in plan.entries:
             self.tags[e.block_index] = (e.noise_level, self.cond.id)
         self._mark()
@@ -302,7 +437,10 @@ class DistWanSession:
         return None
 
     def gather_outputs(self, blocks):
-        """Every rank gets every emitted block (owner -> all)."""
+        """Every rank gets every emitted block (rows: already replicated;
+        blocks: owner -> all)."""
+        if self.mode == "rows":
+            return {b: self.emitted_host(b) for b in blocks}
         mine = {b: self.emitted_host(b) for b in blocks if owner(b, self.world) == self.rank}
         parts = [None] * self.world
         self.dist.all_gather_object(parts, mine)
@@ -329,40 +467,41 @@ class DistWanSession:
             N.lib().bc_ipc_close(p)
         self._opened = []
         self.state.ctx.close()
-        N.lib().bc_free(self.state.arena_ptr)
-        N.lib().bc_free(self.state.flags_ptr)
+        for p in (self.state.arena_ptr, self.state.flags_ptr, self.state.y_ptr):
+            N.lib().bc_free(p)
 
 
 class EmulatedRanks:
-    """G rank contexts on ONE GPU, stepped layer-interleaved on one stream:
+    """G rank contexts on ONE GPU, stepped stage-interleaved on one stream:
     every rank's stage 0, then for each layer all ranks' part A (K/V write +
     peer push + flag publish) before any rank's part B (attention waits on
-    the flags), then all ranks' stage 3.  Exercises exactly the device code
-    of the multi-GPU path (P2P pushes become same-device stores)."""
+    the flags), then all ranks' head (+ Y push), then all ranks' update.
+    Exercises exactly the device code of the multi-GPU path (P2P pushes
+    become same-device copies); each rank has its own latents replica."""
 
     def __init__(self, rt, config, conditioning, session_seed, world, noise_feed=None):
         from .kvpool import SlotAllocator
         from .wan import HostNoiseFeed
         torch = N.torch_mod()
         self.torch, self.cfg, self.world = torch, config, world
+        self.mode = shard_mode()
         width = min(config.cascade_width, config.num_blocks)
         n_slots = config.window_blocks + config.sink_blocks + width + 1
         self.ranks = [_RankState(rt.weights, config, width, n_slots, world, r, ipc=False)
                       for r in range(world)]
         for st in self.ranks:
-            st.attach([(o.rank, o.arena_ptr, o.flags_ptr) for o in self.ranks if o.rank != st.rank])
+            st.attach([(o.rank, o.arena_ptr, o.flags_ptr, o.y_ptr) for o in self.ranks if o.rank != st.rank],
+                      rows=self.mode == "rows")
         self.slots = SlotAllocator(n_slots)
         self.slot_epoch = SlotEpochs(n_slots)
-        self.shape = (config.block_size, config.latent_channels, config.latent_height,
-                      config.latent_width)
+        self.reps = [_Replica(torch, config, width) for _ in range(world)]
+        self.shape = self.reps[0].shape
         self.noise = noise_feed if noise_feed is not None else HostNoiseFeed(session_seed, config)
-        self.latents, self.final, self.tags, self.host_out = {}, {}, {}, {}
+        self.tags, self.host_out = {}, {}
         # one pinned staging area for every emitted block (no per-emission
         # cudaHostAlloc, which would serialise against the device)
         self.host_buf = torch.empty((config.num_blocks,) + tuple(self.shape),
                                     dtype=torch.float32).pin_memory()
-        self.eps = [torch.empty(self.shape, dtype=torch.float32, device="cuda")
-                    for _ in range(width * world)]
         self.events = []
         self.set_conditioning(conditioning)
         ev = torch.cuda.Event(enable_timing=True)
@@ -385,88 +524,65 @@ class EmulatedRanks:
             st.ctx.set_text(cond)
 
     def step(self, plan, mask, pool, vis_lists, posts):
-        from .wan import POST_CACHE, POST_EMIT, POST_RENOISE, _make_update
-        torch = self.torch
+        from .wan import POST_EMIT, _make_update
         epoch = plan.iteration + 1
         blocks = plan.blocks
         for b in blocks:
             self.slots.acquire(b)
-        work = []
+        items = []
         init_req, init_dst, eps_req, eps_dst = [], [], [], []
         for r, st in enumerate(self.ranks):
-            local = rank_entries(blocks, self.world, r)
-            if not local:
-                work.append((st, None))
+            work = _RankWork(self.mode, plan, vis_lists, posts, self.world, r, self.slots,
+                             self.slot_epoch, epoch, self.cfg.tokens_per_block)
+            if not work.local:
+                items.append((st, work, None, None))
                 continue
-            eps_ptrs, outs, nexts = [], [], []
-            for k, i in enumerate(local):
-                e = plan.entries[i]
-                kind, next_pass, next_level = posts[i]
-                if e.pass_index == 0 and e.block_index not in self.latents:
-                    t = torch.empty(self.shape, dtype=torch.float32, device="cuda")
-                    self.latents[e.block_index] = t
-                    init_req.append((e.block_index, 0))
-                    init_dst.append(t)
-                if kind == POST_RENOISE:
-                    buf = self.eps[r * len(self.eps) // self.world + k]
-                    eps_req.append((e.block_index, next_pass))
-                    eps_dst.append(buf)
-                    eps_ptrs.append(buf)
-                else:
-                    eps_ptrs.append(None)
-                if kind == POST_EMIT:
-                    out = torch.empty(self.shape, dtype=torch.float32, device="cuda")
-                    self.final[e.block_index] = out
-                    outs.append(out)
-                else:
-                    outs.append(None)
-                nexts.append(next_level)
-            lb = [blocks[i] for i in local]
-            vis_local = [vis_lists[i] for i in local]
-            bt = N.make_batch(self.cfg.block_size, lb, [plan.entries[i].noise_level for i in local],
-                              [self.slots.slot_of(b) for b in lb],
-                              [[self.slots.slot_of(v) for v in lst] for lst in vis_local])
-            need = need_table(lb, vis_local, blocks, self.slot_epoch, epoch, self.world, r,
-                              self.slots.slot_of)
-            upd = _make_update([posts[i][0] for i in local], [self.latents[b] for b in lb], eps_ptrs,
-                               outs, nexts)
-            work.append((st, (bt, upd, need)))
+            lats, eps, outs, nexts = self.reps[r].prepare(plan, posts, work.local, init_req, init_dst,
+                                                          eps_req, eps_dst)
+            bt = N.make_batch(self.cfg.block_size, work.blocks,
+                              [plan.entries[i].noise_level for i in work.local],
+                              [self.slots.slot_of(b) for b in work.blocks],
+                              [[self.slots.slot_of(v) for v in lst] for lst in work.vis_local])
+            upd = _make_update([posts[i][0] for i in work.local], lats, eps, outs, nexts)
+            items.append((st, work, bt, upd))
         if init_req or eps_req:
             self.noise.fetch(init_req + eps_req, init_dst + eps_dst)
         sp = N.stream_ptr()
         lib = N.lib()
 
-        def run(st, item, stage, layer=0):
-            bt, upd, need = item
-            N.check(lib.bc_wan_step_dist(st.ctx.handle, bt, upd, make_dist(epoch, need, stage, layer),
+        def run(st, work, bt, upd, stage, layer=0):
+            N.check(lib.bc_wan_step_dist(st.ctx.handle, bt, upd, work.dist(stage, layer),
                                          N.ptr(st.ctx.status), sp), "bc_wan_step_dist")
 
-        for st, item in work:
-            if item is not None:
-                run(st, item, 0)
+        live = [it for it in items if it[2] is not None]
+        for it in live:
+            run(*it, 0)
         for layer in range(self.cfg.layers):
-            for st, item in work:
-                if item is not None:
-                    run(st, item, 1, layer)
-            for st, item in work:
-                if item is not None:
-                    run(st, item, 2, layer)
-        for st, item in work:
-            if item is not None:
-                run(st, item, 3)
-            else:
+            for it in live:
+                run(*it, 1, layer)
+            for it in live:
+                run(*it, 2, layer)
+        for it in live:
+            run(*it, 3)
+        for it in live:
+            run(*it, 4)
+        for st, work, bt, _ in items:
+            if bt is None:
                 N.check(lib.bc_wan_signal_done(st.ctx.handle, epoch, sp), "bc_wan_signal_done")
-        for e, (kind, _, _) in zip(plan.entries, posts):
+        for r, (st, work, bt, _) in enumerate(items):
+            if bt is None:
+                continue
+            for i in work.local:
+                b = plan.entries[i].block_index
+                if posts[i][0] == POST_EMIT and b not in self.host_out:
+                    host = self.host_buf[b]
+                    host.copy_(self.reps[r].final[b], non_blocking=True)
+                    self.host_out[b] = host
+            self.reps[r].retire(plan, posts, work.local)
+        for e in plan.entries:
             self.tags[e.block_index] = (e.noise_level, self.cond.id)
-            if kind == POST_EMIT:
-                host = self.host_buf[e.block_index]
-                host.copy_(self.final[e.block_index], non_blocking=True)
-                self.host_out[e.block_index] = host
-            elif kind == POST_CACHE:
-                self.latents.pop(e.block_index, None)
-        self.slot_epoch.wrote([self.slots.slot_of(b) for b in blocks], epoch)
-        ev = torch.cuda.Event(enable_timing=True)
-        ev.record()
+        self.slot_epoch.wrote([self.slots.slot_of(b) for b in blocks], epoch, items[0][1].masks)
+        ev = torch_event(self.torch)
         self.events.append(ev)
 
     def kv_handle(self, block):
@@ -484,6 +600,11 @@ class EmulatedRanks:
             st.ctx.check_status()
         return self.host_out[block].numpy().reshape(self.cfg.block_size, -1).astype(np.float64)
 
+    def replica_outputs(self, block):
+        """Every rank's emitted copy of `block` (rows partition: all ranks)."""
+        self.torch.cuda.current_stream().synchronize()
+        return [rep.final[block].cpu().numpy() for rep in self.reps if block in rep.final]
+
     def fill_wall_times(self, events):
         if not events:
             return
@@ -500,3 +621,9 @@ class EmulatedRanks:
     def close(self):
         for st in self.ranks:
             st.ctx.close()
+
+
+def torch_event(torch):
+    ev = torch.cuda.Event(enable_timing=True)
+    ev.record()
+    return ev

@@ -302,27 +302,34 @@ class HostNoiseFeed:
         self.h2d_bytes = 0
 
     def fetch(self, requests, dests):
-        """requests: [(block, pass)], dests: device tensors of self.shape."""
+        """requests: [(block, pass)], dests: device tensors of self.shape.
+        A key requested for several destinations (per-rank replicas) is
+        generated once; more keys than ring buffers go in chunks."""
         torch = N.torch_mod()
-        bufs = []
-        for _ in requests:
-            i = self.next
-            self.next = (self.next + 1) % len(self.ring)
-            if self.events[i] is not None:
-                self.events[i].synchronize()
-            bufs.append(i)
-        tasks = []
-        for (block, pass_index), i in zip(requests, bufs):
-            host = self.ring[i].numpy().reshape(self.S, -1)
-            tasks += [(self.stream.session_seed, 0, (block, pass_index, block * self.S + f, 0), host[f])
-                      for f in range(self.S)]
-        N.run_noise_tasks(tasks, 1)
-        for i, dst in zip(bufs, dests):
-            dst.copy_(self.ring[i], non_blocking=True)
-            ev = torch.cuda.Event()
-            ev.record()
-            self.events[i] = ev
-            self.h2d_bytes += dst.numel() * 4
+        uniq = list(dict.fromkeys(requests))
+        for c0 in range(0, len(uniq), len(self.ring)):
+            chunk = uniq[c0:c0 + len(self.ring)]
+            bufs = []
+            for _ in chunk:
+                i = self.next
+                self.next = (self.next + 1) % len(self.ring)
+                if self.events[i] is not None:
+                    self.events[i].synchronize()
+                bufs.append(i)
+            tasks = []
+            for (block, pass_index), i in zip(chunk, bufs):
+                host = self.ring[i].numpy().reshape(self.S, -1)
+                tasks += [(self.stream.session_seed, 0, (block, pass_index, block * self.S + f, 0), host[f])
+                          for f in range(self.S)]
+            N.run_noise_tasks(tasks, 1)
+            for key, i in zip(chunk, bufs):
+                for k, dst in zip(requests, dests):
+                    if k == key:
+                        dst.copy_(self.ring[i], non_blocking=True)
+                        self.h2d_bytes += dst.numel() * 4
+                ev = torch.cuda.Event()
+                ev.record()
+                self.events[i] = ev
 
 
 class ResidentNoiseFeed:

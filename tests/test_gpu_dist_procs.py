@@ -19,8 +19,8 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _rank(rank, world, port, q, mode):
-    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+def _rank(rank, world, port, q, mode, shard):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), BC_TEMPORAL_SHARD=shard)
     import torch
     import torch.distributed as dist
     torch.cuda.set_device(0)
@@ -37,8 +37,9 @@ def _rank(rank, world, port, q, mode):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("mode", ["bidirectional", "causal"])
-def test_two_processes_one_gpu(mode):
+@pytest.mark.parametrize("mode,shard", [("bidirectional", "rows"), ("causal", "rows"),
+                                        ("bidirectional", "blocks")])
+def test_two_processes_one_gpu(mode, shard):
     import torch.multiprocessing as mp
     import paper_2511_20426_b200 as bc
     from paper_2511_20426_b200.wan import WanWeights
@@ -47,7 +48,7 @@ def test_two_processes_one_gpu(mode):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_rank, args=(r, 2, port, q, mode)) for r in range(2)]
+    procs = [ctx.Process(target=_rank, args=(r, 2, port, q, mode, shard)) for r in range(2)]
     for p in procs:
         p.start()
     got = q.get(timeout=600)

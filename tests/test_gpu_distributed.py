@@ -25,14 +25,20 @@ def _stack(run):
     return np.stack([run.outputs[k] for k in sorted(run.outputs)])
 
 
-@pytest.mark.parametrize("mode,push", [("bidirectional", "copy"), ("causal", "copy"),
-                                       ("bidirectional", "kernel")])
-def test_emulated_ranks_bit_identical(tiny, monkeypatch, mode, push):
-    """push = copy: copy engines + stream memory ops move the fresh K/V and
-    publish the flags; push = kernel: P2P stores from the q/k kernel."""
+@pytest.mark.parametrize("shard,mode,push", [("rows", "bidirectional", "copy"), ("rows", "causal", "copy"),
+                                             ("rows", "bidirectional", "kernel"),
+                                             ("blocks", "bidirectional", "copy"), ("blocks", "causal", "copy"),
+                                             ("blocks", "bidirectional", "kernel")])
+def test_emulated_ranks_bit_identical(tiny, monkeypatch, shard, mode, push):
+    """shard = rows: every rank runs a slice of every entry's query rows
+    (Y rows exchanged, latents replicated); shard = blocks: whole entries
+    per rank.  push = copy: copy engines + stream memory ops move the fresh
+    K/V and publish the flags; push = kernel: P2P stores from the q/k
+    kernel."""
     import paper_2511_20426_b200 as bc
     from paper_2511_20426_b200 import distributed
     monkeypatch.setenv("BC_KV_PUSH", push)
+    monkeypatch.setenv("BC_TEMPORAL_SHARD", shard)
     cfg, w = tiny
     cfg = bc.with_fields(cfg, attention_mode=mode)
     base = bc.run_cascade(cfg, "a lighthouse in a storm", weights=w)
@@ -43,10 +49,12 @@ def test_emulated_ranks_bit_identical(tiny, monkeypatch, mode, push):
         assert run.pool.state_dump() == base.pool.state_dump()
 
 
-def test_emulated_replicas_agree(tiny, monkeypatch):
+@pytest.mark.parametrize("shard", ["rows", "blocks"])
+def test_emulated_replicas_agree(tiny, monkeypatch, shard):
     import paper_2511_20426_b200 as bc
     from paper_2511_20426_b200 import distributed, engine
     cfg, w = tiny
+    monkeypatch.setenv("BC_TEMPORAL_SHARD", shard)
     monkeypatch.setattr(distributed, "EMULATE", True)
     captured = {}
     orig_close = distributed.EmulatedRanks.close
@@ -58,20 +66,57 @@ def test_emulated_replicas_agree(tiny, monkeypatch):
         orig_close(self)
 
     monkeypatch.setattr(distributed.EmulatedRanks, "close", close)
+    orig_step = distributed.EmulatedRanks.step
+    finals = {}
+
+    def step(self, *a, **k):
+        orig_step(self, *a, **k)
+        for b in list(self.host_out):
+            if b not in finals:
+                finals[b] = self.replica_outputs(b)
+
+    monkeypatch.setattr(distributed.EmulatedRanks, "step", step)
     run = bc.run_cascade(bc.with_fields(cfg, workers=3), "p", weights=w)
     arenas, slots = captured["arenas"], captured["slots"]
     for b in run.pool.block_indices:
         s = slots[b]
         for a in arenas[1:]:
             assert torch.equal(a[:, s], arenas[0][:, s]), b
+    # rows partition: every rank emitted every block, identically
+    for b, copies in finals.items():
+        assert len(copies) == (3 if shard == "rows" else 1)
+        for c in copies[1:]:
+            assert np.array_equal(c, copies[0]), b
 
 
-def test_emulated_prompt_switch(tiny, monkeypatch):
+@pytest.mark.parametrize("shard", ["rows", "blocks"])
+def test_emulated_prompt_switch(tiny, monkeypatch, shard):
     import paper_2511_20426_b200 as bc
     from paper_2511_20426_b200 import distributed
+    monkeypatch.setenv("BC_TEMPORAL_SHARD", shard)
     cfg, w = tiny
     sw = [bc.SwitchSpec("second scene", "cascade", at_block=2)]
     base = bc.run_cascade(cfg, "first", weights=w, switches=sw)
     monkeypatch.setattr(distributed, "EMULATE", True)
     run = bc.run_cascade(bc.with_fields(cfg, workers=2), "first", weights=w, switches=sw)
+    assert np.array_equal(_stack(run), _stack(base))
+
+
+def test_emulated_rows_ragged_slices(monkeypatch):
+    """Row slices that cut entries mid-tile-range and ranks with no rows at
+    all (G = 8 > tiles): still bit-identical."""
+    import paper_2511_20426_b200 as bc
+    from paper_2511_20426_b200 import distributed
+    from paper_2511_20426_b200.wan import WanWeights
+    cfg = bc.wan_config("tiny", total_frames=12)
+    w = WanWeights.random(cfg, 3)
+    base = bc.run_cascade(cfg, "ragged", weights=w)
+    monkeypatch.setenv("BC_TEMPORAL_SHARD", "rows")
+    monkeypatch.setattr(distributed, "EMULATE", True)
+    monkeypatch.setattr(distributed, "ROW_TILE", 64)
+    run = bc.run_cascade(bc.with_fields(cfg, workers=3), "ragged", weights=w)
+    assert np.array_equal(_stack(run), _stack(base))
+    monkeypatch.setattr(distributed, "ROW_UNIT_SMALL", 192)   # one unit per entry: idle ranks
+    assert sum(a == b for a, b in distributed.row_slices(2, 192, 7)) == 5   # 5 of 7 ranks idle
+    run = bc.run_cascade(bc.with_fields(cfg, workers=7), "ragged", weights=w)
     assert np.array_equal(_stack(run), _stack(base))
