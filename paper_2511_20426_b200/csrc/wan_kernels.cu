@@ -100,24 +100,33 @@ __global__ void patchify_kernel(EntryPtrs lat, int F, int H, int W, __nv_bfloat1
 }
 
 // ------------------------------------------------------------ GEMV (time MLP)
-// out[e][o] = act_out( sum_k act_in(in[e][k]) W[o][k] + b[o] ), one warp per o.
-__global__ void gemv_kernel(const float* in, int n, int K, const __nv_bfloat16* W, const float* b,
-                            float* out, int N, int act_in, int act_out) {
+// out[e][o] = act( sum_k in[e][k] W[o][k] + b[o] ), one warp per o, 16-byte
+// weight loads (8 bf16 per lane per step); act 0: none, 1: silu, 2: out gets
+// the raw value and out2 its silu (t_e feeds the head modulation raw and the
+// 6d projection through a silu).  K % 8 == 0.
+__global__ void gemv_kernel(const float* __restrict__ in, int n, int K, const __nv_bfloat16* __restrict__ W,
+                            const float* __restrict__ b, float* __restrict__ out, int N, int act,
+                            float* __restrict__ out2) {
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (warp >= N) return;
-  const __nv_bfloat16* w = W + (size_t)warp * K;
+  const uint4* w = reinterpret_cast<const uint4*>(W + (size_t)warp * K);
   float acc[BC_MAX_ENTRIES];
 #pragma unroll
   for (int e = 0; e < BC_MAX_ENTRIES; ++e) acc[e] = 0.0f;
-  for (int k = lane; k < K; k += 32) {
-    const float wk = bf(w[k]);
+  for (int k8 = lane; k8 < K / 8; k8 += 32) {
+    const uint4 u = __ldg(w + k8);
+    const __nv_bfloat16* h = reinterpret_cast<const __nv_bfloat16*>(&u);
+    float wk[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) wk[j] = bf(h[j]);
 #pragma unroll
     for (int e = 0; e < BC_MAX_ENTRIES; ++e) {
       if (e < n) {
-        float v = in[(size_t)e * K + k];
-        if (act_in == 1) v = silu(v);
-        acc[e] += wk * v;
+        const float4* x = reinterpret_cast<const float4*>(in + (size_t)e * K) + 2 * k8;
+        const float4 x0 = x[0], x1 = x[1];
+        acc[e] += wk[0] * x0.x + wk[1] * x0.y + wk[2] * x0.z + wk[3] * x0.w + wk[4] * x1.x + wk[5] * x1.y +
+                  wk[6] * x1.z + wk[7] * x1.w;
       }
     }
   }
@@ -127,8 +136,8 @@ __global__ void gemv_kernel(const float* in, int n, int K, const __nv_bfloat16* 
       float v = warp_sum(acc[e]);
       if (lane == 0) {
         v += b ? b[warp] : 0.0f;
-        if (act_out == 1) v = silu(v);
-        out[(size_t)e * N + warp] = v;
+        out[(size_t)e * N + warp] = act == 1 ? silu(v) : v;
+        if (act == 2) out2[(size_t)e * N + warp] = silu(v);
       }
     }
   }
@@ -253,9 +262,17 @@ __global__ void __launch_bounds__(256) qk_norm_rope_kernel(const __nv_bfloat16* 
   const int hw = a.hp * a.wp;
   const int fl = t / hw, rem = t % hw;
   const int f = a.frame0[e] + fl, ph = rem / a.wp, pw = rem % a.wp;
-  const float2* rf = a.rope_f + (size_t)f * 22;
-  const float2* rh = a.rope_h + (size_t)ph * 21;
-  const float2* rw = a.rope_w + (size_t)pw * 21;
+  // the row's 64 (cos, sin) pairs -- 22 time, 21 height, 21 width -- staged
+  // in shared memory once, so the per-element lookup is one lane-indexed load
+  // (a per-element 3-way table select diverges inside every warp)
+  __shared__ float2 tab[8][64];
+  {
+    const float2* rf = a.rope_f + (size_t)f * 22;
+    const float2* rh = a.rope_h + (size_t)ph * 21;
+    const float2* rw = a.rope_w + (size_t)pw * 21;
+    for (int pi = li; pi < 64; pi += 32 * WPR) tab[slot][pi] = pi < 22 ? rf[pi] : (pi < 43 ? rh[pi - 22] : rw[pi - 43]);
+  }
+  __syncthreads();
   const size_t mat = (size_t)T * d;
   __nv_bfloat16* kdst = a.arena + ((size_t)a.mat_base + (size_t)a.slot[e] * 2) * mat + (size_t)t * d;
   __nv_bfloat16* vdst = kdst + mat;
@@ -296,14 +313,17 @@ __global__ void __launch_bounds__(256) qk_norm_rope_kernel(const __nv_bfloat16* 
         const int c0 = idx * 8;                 // element index in [0, d)
         const int pair0 = (c0 & 127) >> 1;      // pair index inside the head
         const __nv_bfloat16* h = reinterpret_cast<const __nv_bfloat16*>(&raw[which][i]);
+        const float4 w0 = __ldg(reinterpret_cast<const float4*>(wgt + c0));
+        const float4 w1 = __ldg(reinterpret_cast<const float4*>(wgt + c0) + 1);
+        const float wv[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
         uint4 u;
         __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(&u);
 #pragma unroll
         for (int j = 0; j < 8; j += 2) {
-          const float x0 = bf(h[j]) * inv[which] * wgt[c0 + j];
-          const float x1 = bf(h[j + 1]) * inv[which] * wgt[c0 + j + 1];
+          const float x0 = bf(h[j]) * inv[which] * wv[j];
+          const float x1 = bf(h[j + 1]) * inv[which] * wv[j + 1];
           const int pi = pair0 + j / 2;
-          const float2 cs = pi < 22 ? rf[pi] : (pi < 43 ? rh[pi - 22] : rw[pi - 43]);
+          const float2 cs = tab[slot][pi];
           o[j] = __float2bfloat16(x0 * cs.x - x1 * cs.y);
           o[j + 1] = __float2bfloat16(x0 * cs.y + x1 * cs.x);
         }
@@ -369,10 +389,15 @@ __global__ void rms_rows_kernel(__nv_bfloat16* x, int rows, int d, int ld, const
   for (int i = 0; i < VPL; ++i) {
     const int idx = li + 32 * WPR * i;
     if (idx * 8 >= d) continue;
+    // weights as two 16-byte loads (8 scalar loads strided 32 B apart across
+    // the warp made this kernel L1-wavefront bound)
+    const float4 w0 = __ldg(reinterpret_cast<const float4*>(w) + 2 * idx);
+    const float4 w1 = __ldg(reinterpret_cast<const float4*>(w) + 2 * idx + 1);
+    const float wv[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
     uint4 u;
     __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(&u);
 #pragma unroll
-    for (int j = 0; j < 8; ++j) o[j] = __float2bfloat16(vals[i][j] * inv * w[idx * 8 + j]);
+    for (int j = 0; j < 8; ++j) o[j] = __float2bfloat16(vals[i][j] * inv * wv[j]);
     d4[idx] = u;
   }
 }
@@ -472,10 +497,11 @@ int launch_patchify(const EntryPtrs& lat, int F, int H, int W, int row0, int row
   return BC_OK;
 }
 
-int launch_gemv(const float* in, int n, int K, const __nv_bfloat16* W, const float* b, float* out, int N,
-                int act_in, int act_out, cudaStream_t st) {
+int launch_gemv(const float* in, int n, int K, const __nv_bfloat16* W, const float* b, float* out, int N, int act,
+                float* out2, cudaStream_t st) {
+  if (K % 8 || (act == 2 && !out2)) return bc_fail(BC_ERR_CONTRACT, "gemv: K %% 8 != 0 or missing out2");
   const int threads = 256;
-  gemv_kernel<<<(N * 32 + threads - 1) / threads, threads, 0, st>>>(in, n, K, W, b, out, N, act_in, act_out);
+  gemv_kernel<<<(N * 32 + threads - 1) / threads, threads, 0, st>>>(in, n, K, W, b, out, N, act, out2);
   BC_LAUNCHED();
   return BC_OK;
 }

@@ -79,8 +79,9 @@ struct UpdArgs {
 // tokens of global rows [row0, row0 + rows) of the concatenated batch
 int launch_patchify(const EntryPtrs& lat, int F, int H, int W, int row0, int rows, __nv_bfloat16* out,
                     cudaStream_t st);
-int launch_gemv(const float* in, int n, int K, const __nv_bfloat16* W, const float* b, float* out, int N,
-                int act_in, int act_out, cudaStream_t st);
+// act 0: none, 1: silu, 2: out raw + out2 silu
+int launch_gemv(const float* in, int n, int K, const __nv_bfloat16* W, const float* b, float* out, int N, int act,
+                float* out2, cudaStream_t st);
 int launch_timestep_sin(const TimeArgs& a, int n, float* out, int freq_dim, cudaStream_t st);
 int launch_ln_rows(const float* X, __nv_bfloat16* out, int rows, int d, int rows_per_entry, const LnArgs& a,
                    cudaStream_t st);

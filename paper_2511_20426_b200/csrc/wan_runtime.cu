@@ -41,7 +41,7 @@ struct bc_wan_ctx {
   float* X;
   __nv_bfloat16 *xn, *qkv, *Q, *attn, *H1, *patches;
   float* Y;
-  float *t_sin, *t_h, *t_e, *t_e0, *mod_all;
+  float *t_sin, *t_h, *t_e, *t_es, *t_e0, *mod_all;
   __nv_bfloat16 *text_in, *text_h, *ctx, *text_tmp, *textkv;
   float2 *rope_f, *rope_h, *rope_w;
   bool text_ready, rope_ready;
@@ -98,6 +98,7 @@ int64_t carve(bc_wan_ctx* c, const bc_wan_dims& dm, char* base) {
   t->t_sin = cv.take<float>(E * dm.freq_dim);
   t->t_h = cv.take<float>(E * d);
   t->t_e = cv.take<float>(E * d);
+  t->t_es = cv.take<float>(E * d);
   t->t_e0 = cv.take<float>(E * 6 * d);
   t->mod_all = cv.take<float>((int64_t)dm.layers * E * 6 * d);
   t->text_in = cv.take<__nv_bfloat16>((int64_t)dm.text_len * dm.text_dim);
@@ -375,10 +376,11 @@ int stage_begin(bc_wan_ctx* c, const bc_batch* batch, const bc_wan_update* upd, 
   for (int e = 0; e < n; ++e) ta.t[e] = batch->level[e];
   RC(bc::launch_timestep_sin(ta, n, c->t_sin, dm.freq_dim, st));
   RC(bc::launch_gemv(c->t_sin, n, dm.freq_dim, static_cast<const __nv_bfloat16*>(p.time_w1), p.time_b1, c->t_h, d,
-                     0, 1, st));
-  RC(bc::launch_gemv(c->t_h, n, d, static_cast<const __nv_bfloat16*>(p.time_w2), p.time_b2, c->t_e, d, 0, 0, st));
-  RC(bc::launch_gemv(c->t_e, n, d, static_cast<const __nv_bfloat16*>(p.tproj_w), p.tproj_b, c->t_e0, 6 * d, 1, 0,
+                     1, nullptr, st));
+  RC(bc::launch_gemv(c->t_h, n, d, static_cast<const __nv_bfloat16*>(p.time_w2), p.time_b2, c->t_e, d, 2, c->t_es,
                      st));
+  RC(bc::launch_gemv(c->t_es, n, d, static_cast<const __nv_bfloat16*>(p.tproj_w), p.tproj_b, c->t_e0, 6 * d, 0,
+                     nullptr, st));
   RC(bc::launch_mod_combine(p.modulation, c->t_e0, L, n, d, c->mod_all, st));
 
   bc::AttnArgs& sa = S.sa;
