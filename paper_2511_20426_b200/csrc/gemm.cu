@@ -47,7 +47,9 @@ struct GemmCfg {
   static constexpr int kBBytes = (BN / CG) * BK * 2;
   static constexpr int kStageBytes = kABytes + kBBytes;
   static constexpr int kStages = (192 * 1024) / kStageBytes > 8 ? 8 : (192 * 1024) / kStageBytes;
-  static constexpr int kTmemCols = 2 * BN >= 32 ? 2 * BN : 32;
+  // two accumulators, rounded up to the power-of-two column count
+  // tcgen05.alloc requires (BN = 192 -> 512)
+  static constexpr int kTmemCols = 2 * BN <= 32 ? 32 : 2 * BN <= 64 ? 64 : 2 * BN <= 128 ? 128 : 2 * BN <= 256 ? 256 : 512;
   static constexpr size_t kSmem = 1024 /*align slack*/ + (size_t)kStages * kStageBytes + 256 + kEpiStageBytes;
 };
 
@@ -123,9 +125,18 @@ __device__ __forceinline__ void tile_coords(int tile, int num_m, int num_n, int&
   n_blk = r / gm;
 }
 
+// GELU (tanh form) with the MUFU tanh (tanh.approx.f32, rel. error ~2^-11,
+// well below the bf16 output's 2^-8): libm tanhf made the FFN1 epilogue
+// ~27 instructions per output and capped the tensor pipe at 79% (ncu)
+__device__ __forceinline__ float tanh_fast(float x) {
+  float y;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
 __device__ __forceinline__ float gelu_tanh(float x) {
   const float k0 = 0.7978845608028654f, k1 = 0.044715f;
-  return 0.5f * x * (1.0f + tanhf(k0 * (x + k1 * x * x * x)));
+  const float hx = 0.5f * x;
+  return fmaf(hx, tanh_fast(k0 * fmaf(k1 * x, x * x, x)), hx);
 }
 
 template <int BN, int MODE, int CG>
@@ -478,9 +489,21 @@ int num_sms() { return sm_count(); }
 int gemm_plan_bn(int M, int N) {
   // 128x256 tiles amortise the A panel over twice the columns and measured
   // 10-20% faster per tile than 128x128; fall back to narrower tiles only
-  // when N does not divide or the wide tiling cannot fill one wave.
+  // when N does not divide or the wide tiling cannot fill one wave.  When
+  // CTA-pair 256-row tiles quantise badly onto the pairs (N = 1536 at
+  // 23,400 rows: 552 tiles = 7.46 waves of 74 pairs), 192-column pair tiles
+  // can fill the last wave better (736 tiles = 9.95 waves): pick the width
+  // with the smaller (waves x width).
   const int mt = (M + BM - 1) / BM;
-  if (N % 256 == 0 && mt * (N / 256) >= sm_count()) return 256;
+  if (N % 256 == 0 && mt * (N / 256) >= sm_count()) {
+    if (N % 192 == 0) {
+      const int pairs = sm_count() / 2, m2 = (M + 2 * BM - 1) / (2 * BM);
+      const long w256 = (long)((m2 * (N / 256) + pairs - 1) / pairs) * 256;
+      const long w192 = (long)((m2 * (N / 192) + pairs - 1) / pairs) * 192;
+      if (w192 < w256) return 192;
+    }
+    return 256;
+  }
   if (N % 128 == 0) return 128;
   return 64;
 }
@@ -497,13 +520,18 @@ int gemm_run(const GemmArgs& g, cudaStream_t st) {
     pair_env = e ? atoi(e) : -1;
   }
   const int pair_tiles = ((g.M + 2 * BM - 1) / (2 * BM)) * (g.N / (bn ? bn : 1));
-  const bool pair = bn == 256 && g.cg != 1 && (g.cg == 2 || (pair_env >= 0 ? pair_env == 1 : pair_tiles >= sm_count() / 2));
+  const bool pair = (bn == 256 || bn == 192) && g.cg != 1 &&
+                    (g.cg == 2 || bn == 192 || (pair_env >= 0 ? pair_env == 1 : pair_tiles >= sm_count() / 2));
   const int cg = pair ? 2 : 1;
+  if (g.N % bn || (bn == 192 && cg != 2))
+    return bc_fail(BC_ERR_CONTRACT, "gemm: tile width %d does not fit N=%d (192 needs CTA pairs)", bn, g.N);
   CUtensorMap ma, mb;
   int rc = make_tmap_2d(&ma, g.A, g.K, g.M, (uint64_t)g.K * 2, BK, BM);
   if (rc) return rc;
   rc = make_tmap_2d(&mb, g.B, g.K, g.N, (uint64_t)g.K * 2, BK, bn / cg);
   if (rc) return rc;
+  if (cg == 2 && bn == 192)
+    return dispatch_mode<192, 2>(g.mode, ma, mb, g.C, g.M, g.N, g.K, g.bias, g.gate, g.gate_stride, g.rows_per_gate, g.gate_row0, st);
   if (cg == 2)
     return dispatch_mode<256, 2>(g.mode, ma, mb, g.C, g.M, g.N, g.K, g.bias, g.gate, g.gate_stride, g.rows_per_gate, g.gate_row0, st);
   switch (bn) {

@@ -28,9 +28,9 @@ SHAPES = [(128, 256, 64), (300, 128, 128), (4680, 1536, 1536), (1000, 768, 256),
 
 
 @pytest.mark.parametrize("M,Nn,K", SHAPES)
-@pytest.mark.parametrize("bn,cg", [(0, 0), (64, 1), (128, 1), (256, 1), (256, 2)])
+@pytest.mark.parametrize("bn,cg", [(0, 0), (64, 1), (128, 1), (256, 1), (256, 2), (192, 2)])
 def test_gemm_modes(M, Nn, K, bn, cg):
-    """cg = 2: tcgen05.mma.cta_group::2 CTA pairs (256 x 256 tiles)."""
+    """cg = 2: tcgen05.mma.cta_group::2 CTA pairs (256 x 256 / 256 x 192 tiles)."""
     if bn and Nn % bn:
         pytest.skip("tile width does not divide N")
     g = torch.Generator(device="cuda").manual_seed(M * 7 + Nn + K)
@@ -73,7 +73,9 @@ def test_gemm_tilings_bitwise_equal(M, Nn, K):
     B = (torch.randn(Nn, K, device="cuda", generator=g) / K ** 0.5).bfloat16()
     bias = torch.randn(Nn, device="cuda", generator=g)
     outs = []
-    for bn, cg in ((64, 1), (128, 1), (256, 1), (256, 2), (0, 0)):
+    for bn, cg in ((64, 1), (128, 1), (256, 1), (256, 2), (192, 2), (0, 0)):
+        if Nn % (bn or 64):
+            continue
         C = torch.empty(M, Nn, device="cuda")
         gemm(A, B, C, 2, bias=bias, bn=bn, cg=cg)
         outs.append(C)
