@@ -74,9 +74,13 @@ struct Smem {
 };
 
 __device__ __forceinline__ float ex2(float x) {
+#ifdef BC_ATTN_FAKE_EXP  // timing experiment only (wrong numerics): no MUFU
+  return fmaf(x, 0.0009765625f, 1.0f);
+#else
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
+#endif
 }
 
 // 3-input max (FMNMX3, sm_100+): halves the ALU ops of the row max
@@ -628,11 +632,12 @@ int attention_run(const AttnArgs& a, cudaStream_t st) {
     // polynomial instead of MUFU.EX2
     const char* env = getenv("BC_ATTN_POLY");
     poly = env ? atoi(env) : kDefaultPoly;
-    if (poly != 0 && poly != 2 && poly != 3 && poly != 4) poly = kDefaultPoly;
+    if (poly != 0 && poly != 2 && poly != 3 && poly != 4 && poly != 8) poly = kDefaultPoly;
     BC_CUDA(cudaFuncSetAttribute(attn_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, Smem::total + 1024));
     BC_CUDA(cudaFuncSetAttribute(attn_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, Smem::total + 1024));
     BC_CUDA(cudaFuncSetAttribute(attn_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, Smem::total + 1024));
     BC_CUDA(cudaFuncSetAttribute(attn_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, Smem::total + 1024));
+    BC_CUDA(cudaFuncSetAttribute(attn_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, Smem::total + 1024));
     cudaFuncAttributes fa;
     BC_CUDA(cudaFuncGetAttributes(&fa, attn_kernel<0>));
     if (fa.numRegs != kRegsLaunch)  // the setmaxnreg split assumes this allocation (else: deadlock)
@@ -644,6 +649,7 @@ int attention_run(const AttnArgs& a, cudaStream_t st) {
     case 2: attn_kernel<2><<<grid, kThreads, Smem::total + 1024, st>>>(mq, mkv, p); break;
     case 3: attn_kernel<3><<<grid, kThreads, Smem::total + 1024, st>>>(mq, mkv, p); break;
     case 4: attn_kernel<4><<<grid, kThreads, Smem::total + 1024, st>>>(mq, mkv, p); break;
+    case 8: attn_kernel<8><<<grid, kThreads, Smem::total + 1024, st>>>(mq, mkv, p); break;
     default: attn_kernel<0><<<grid, kThreads, Smem::total + 1024, st>>>(mq, mkv, p);
   }
   BC_LAUNCHED();
