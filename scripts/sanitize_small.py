@@ -21,6 +21,13 @@ for mode, dt in ((0, torch.bfloat16), (1, torch.bfloat16), (2, torch.float32), (
     g = torch.ones(6, 512, device="cuda")
     N.check(N.lib().bc_gemm_bf16(N.ptr(A2), N.ptr(B2), N.ptr(C), 600, 512, 256, mode | (4 << 8) | (2 << 16), 0,
                                  N.ptr(g) if mode == 3 else 0, 512, 100, N.stream_ptr()), "gemm pair")
+# 192-column CTA-pair tiles (N = 384), ragged M
+B3 = torch.randn(384, 256, device="cuda").bfloat16()
+for mode, dt in ((0, torch.bfloat16), (3, torch.float32)):
+    C = torch.zeros(600, 384, device="cuda", dtype=dt)
+    g = torch.ones(6, 384, device="cuda")
+    N.check(N.lib().bc_gemm_bf16(N.ptr(A2), N.ptr(B3), N.ptr(C), 600, 384, 256, mode | (3 << 8) | (2 << 16), 0,
+                                 N.ptr(g) if mode == 3 else 0, 384, 100, N.stream_ptr()), "gemm pair 192")
 # attention, ragged q/kv
 T, H = 200, 2
 arena = torch.randn(4, 2, T, H * 128, device="cuda").bfloat16()
@@ -33,5 +40,15 @@ N.check(N.lib().bc_attention_paged(N.ptr(q), N.ptr(arena), N.ptr(arena) + mat * 
 cfg = bc.wan_config("tiny", total_frames=9)
 bc.run_cascade(cfg, "p", weights=WanWeights.random(cfg, 1))
 bc.run_cascade(bc.CascadeConfig(total_frames=9).validate(), "p")
+# multi-rank device path (row partition, 3 emulated ranks: peer copies, flags,
+# stream-memop waits, Y exchange) and the recache baseline
+from paper_2511_20426_b200 import distributed
+distributed.EMULATE = True
+os.environ["BC_TEMPORAL_SHARD"] = "rows"
+bc.run_cascade(bc.with_fields(cfg, workers=3), "p", weights=WanWeights.random(cfg, 1))
+distributed.EMULATE = False
+cfg12 = bc.wan_config("tiny", total_frames=12)
+bc.run_cascade(cfg12, "p", weights=WanWeights.random(cfg12, 1),
+               switches=[bc.SwitchSpec("q", "recache", at_block=2)])
 torch.cuda.synchronize()
 print("sanitize workload done")
