@@ -141,7 +141,10 @@ class _Ctx:
         need = N.lib().bc_wan_workspace_bytes(dims)
         if need < 0:
             raise ContractViolation("bc_wan_workspace_bytes rejected the dims")
-        self.arena = arena if arena is not None else torch.zeros(
+        # no zero fill (11-54 GB): a slot is always written (its block's K/V
+        # in layer part A) before any attention reads it, and key rows past a
+        # slot's end are TMA out-of-bounds zero fill
+        self.arena = arena if arena is not None else torch.empty(
             (cfg.layers, n_slots, 2, self.T, self.d), dtype=torch.bfloat16, device="cuda")
         self.workspace = torch.empty(int(need), dtype=torch.uint8, device="cuda")
         prm = N.WanParams()
