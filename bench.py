@@ -214,10 +214,23 @@ def run_ours(args, cfg):
     from paper_2511_20426_b200.wan import ResidentNoiseFeed, WanWeights, run_noise_keys
 
     world, rank, local = dist_env()
-    torch.cuda.set_device(local)
+    # BC_FORCE_DEVICE / BC_DIST_BACKEND: test hooks to run the multi-rank
+    # bench with several ranks on one GPU over gloo (NCCL refuses duplicate
+    # GPUs); the driver's runs use one GPU per rank and NCCL
+    dev = int(os.environ.get("BC_FORCE_DEVICE", local))
+    backend = os.environ.get("BC_DIST_BACKEND", "nccl")
+    torch.cuda.set_device(dev)
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl")
+        dist.init_process_group(backend)
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        import torch.distributed as dist
+        t = torch.tensor([x], dtype=torch.float64, device="cuda" if backend == "nccl" else "cpu")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
     weights = WanWeights.random(cfg, WEIGHT_SEED)
     seq_cfg = bc.with_fields(cfg, offset=cfg.passes)
     feed = ResidentNoiseFeed(SESSION_SEED, cfg, run_noise_keys(cfg))
@@ -244,7 +257,7 @@ def run_ours(args, cfg):
     barrier()
     torch.cuda.synchronize()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clocks:
+    with ClockSampler(dev) as clocks:
         ev0.record()
         runs = [one_run() for _ in range(args.steps)]
         ev1.record()
@@ -253,12 +266,7 @@ def run_ours(args, cfg):
     launches = N.launch_count() - launches0
     prof = N.profile_collect()
     N.profile_enable(False)
-    ms = ev0.elapsed_time(ev1)
-    if world > 1:
-        import torch.distributed as dist
-        t = torch.tensor([ms], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+    ms = max_over_ranks(ev0.elapsed_time(ev1))
     # temporal parallelism: all ranks cooperate on ONE video (strong scaling)
     frames = cfg.num_blocks * FRAMES_PER_BLOCK
     value = frames * args.steps / (ms / 1e3)
@@ -272,17 +280,13 @@ def run_ours(args, cfg):
     bc.run_cascade(cfg, PROMPT, session_seed=SESSION_SEED, weights=weights, switches=switches)
     barrier()
     torch.cuda.synchronize()
-    with ClockSampler(local) as clocks_e2e:
+    with ClockSampler(dev) as clocks_e2e:
         t0 = time.perf_counter()
         e2e_runs = [bc.run_cascade(cfg, PROMPT, session_seed=SESSION_SEED, weights=weights,
                                    switches=switches) for _ in range(args.steps)]
         torch.cuda.synchronize()
         e2e_s = time.perf_counter() - t0
-    if world > 1:
-        import torch.distributed as dist
-        t = torch.tensor([e2e_s], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_s = float(t.item())
+    e2e_s = max_over_ranks(e2e_s)
     e2e_value = frames * args.steps / e2e_s
     # ---- sequential block-causal rollout, same weights / inputs ----
     seq_e2e = seq_stream = None
