@@ -652,8 +652,17 @@ extern "C" int bc_wan_set_peers(bc_wan_ctx* c, const bc_wan_peers* peers) {
     c->Y = peers->my_y;
   }
   c->peers = *peers;
-  const char* how = getenv("BC_KV_PUSH");  // "kernel": P2P stores inside the q/k kernel
-  c->push_by_copy = !(how && std::strcmp(how, "kernel") == 0);
+  // Default: the q/k kernel itself stores each fresh K/V row into every
+  // peer's replica (NVLink P2P) and its last CTA publishes the flags, so a
+  // consumer's spinning attention only ever waits on work that precedes it
+  // on some stream -- deadlock-free whatever else occupies the SMs.
+  // BC_KV_PUSH=copy: cudaMemcpyAsync on a side stream + stream-memop flags;
+  // overlaps the transfer with compute but needs the copy to run on a copy
+  // engine -- a same-device copy (one-GPU emulation of the ranks) is an SM
+  // kernel that a spinning attention can starve (measured: hangs at full
+  // Wan-1.3B geometry, scripts/emulated_full.py).
+  const char* how = getenv("BC_KV_PUSH");
+  c->push_by_copy = how && std::strcmp(how, "copy") == 0;
   if (peers->n_peers > 0 && !c->side) {
     BC_CUDA(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
     BC_CUDA(cudaEventCreateWithFlags(&c->ev_qk, cudaEventDisableTiming));

@@ -18,8 +18,8 @@ KV-arena replica.  An iteration's work is partitioned in one of two ways
   life (whole entries per rank; ranks beyond the width idle).
 
 In both, the exchange is one per layer: fresh K/V rows reach the peers'
-replicas over NVLink (copy engines + a stream memory op publishing
-``flags[layer][slot][producer] = epoch``), and a consumer's attention waits
+replicas over NVLink (P2P stores from the q/k kernel, whose last CTA
+publishes ``flags[layer][slot][producer] = epoch``), and a consumer's attention waits
 for the flags of a visible slot's producers only before that slot's first
 key tile.  Pool slots come first in the ascending gather order, so the
 transfer overlaps the pool part of the attention, and the summation order

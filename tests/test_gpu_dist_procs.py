@@ -1,5 +1,5 @@
 """The real one-process-per-rank path (DistWanSession: CUDA-IPC-mapped peer
-KV replicas, copy-engine K/V pushes, stream-memop flags, done epochs, output
+KV replicas, P2P K/V stores, ready flags, stream-memop Y waits, done epochs, output
 gather) with two processes sharing cuda:0 over a gloo group.  The GPU
 time-slices the two contexts; outputs must equal the single-process run
 bit-for-bit (placement independence, reference test_acceptance.py:58-76)."""

@@ -120,3 +120,23 @@ def test_emulated_rows_ragged_slices(monkeypatch):
     assert sum(a == b for a, b in distributed.row_slices(2, 192, 7)) == 5   # 5 of 7 ranks idle
     run = bc.run_cascade(bc.with_fields(cfg, workers=7), "ragged", weights=w)
     assert np.array_equal(_stack(run), _stack(base))
+
+
+@pytest.mark.parametrize("shard", ["rows", "blocks"])
+def test_emulated_full_geometry(monkeypatch, shard):
+    """Full Wan-1.3B token geometry (4680 tokens / block, d = 1536, 60,840-key
+    windows; 2 layers, 5 blocks) with 2 and 8 emulated ranks: row slices at
+    128-row tile granularity, multi-entry slices, bit-identical outputs.
+    (With BC_KV_PUSH=copy this configuration hangs on one device: the
+    same-device copy is an SM kernel starved by the spinning attention.)"""
+    import paper_2511_20426_b200 as bc
+    from paper_2511_20426_b200 import distributed
+    from paper_2511_20426_b200.wan import WanWeights
+    cfg = bc.wan_config("1.3b", total_frames=15, layers=2)
+    w = WanWeights.random(cfg, 5)
+    base = bc.run_cascade(cfg, "full geometry", weights=w)
+    monkeypatch.setenv("BC_TEMPORAL_SHARD", shard)
+    monkeypatch.setattr(distributed, "EMULATE", True)
+    for g in (2, 8):
+        run = bc.run_cascade(bc.with_fields(cfg, workers=g), "full geometry", weights=w)
+        assert np.array_equal(_stack(run), _stack(base)), g
