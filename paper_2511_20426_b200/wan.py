@@ -19,6 +19,7 @@ from __future__ import annotations
 
 import ctypes
 import math
+import os
 
 import numpy as np
 
@@ -303,6 +304,11 @@ class HostNoiseFeed:
         self.events = [None] * ring
         self.next = 0
         self.h2d_bytes = 0
+        # host threads for the generator: the node's cores shared by the ranks
+        # on it (every rank of the rows partition draws every entry's noise)
+        env = os.environ.get("BC_NOISE_THREADS")
+        local = max(1, int(os.environ.get("LOCAL_WORLD_SIZE", "1")))
+        self.threads = int(env) if env else max(1, (os.cpu_count() or 1) // local)
 
     def fetch(self, requests, dests):
         """requests: [(block, pass)], dests: device tensors of self.shape.
@@ -324,7 +330,7 @@ class HostNoiseFeed:
                 host = self.ring[i].numpy().reshape(self.S, -1)
                 tasks += [(self.stream.session_seed, 0, (block, pass_index, block * self.S + f, 0), host[f])
                           for f in range(self.S)]
-            N.run_noise_tasks(tasks, 1)
+            N.run_noise_tasks(tasks, 1, self.threads)
             for key, i in zip(chunk, bufs):
                 for k, dst in zip(requests, dests):
                     if k == key:
