@@ -496,6 +496,8 @@ class EmulatedRanks:
         self.slot_epoch = SlotEpochs(n_slots)
         self.reps = [_Replica(torch, config, width) for _ in range(world)]
         self.shape = self.reps[0].shape
+        # BC_EMULATE_TIMING=1: per iteration, each rank's own device time (ms)
+        self.rank_times = [] if os.environ.get("BC_EMULATE_TIMING") == "1" else None
         self.noise = noise_feed if noise_feed is not None else HostNoiseFeed(session_seed, config)
         self.tags, self.host_out = {}, {}
         # one pinned staging area for every emitted block (no per-emission
@@ -550,9 +552,18 @@ class EmulatedRanks:
         sp = N.stream_ptr()
         lib = N.lib()
 
+        timing = self.rank_times is not None
+        marks = {}
+
         def run(st, work, bt, upd, stage, layer=0):
+            if timing:  # device time of this rank's own kernels (the work one GPU would do)
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
             N.check(lib.bc_wan_step_dist(st.ctx.handle, bt, upd, work.dist(stage, layer),
                                          N.ptr(st.ctx.status), sp), "bc_wan_step_dist")
+            if timing:
+                e1.record()
+                marks.setdefault(st.rank, []).append((e0, e1))
 
         live = [it for it in items if it[2] is not None]
         for it in live:
@@ -581,6 +592,10 @@ class EmulatedRanks:
             self.reps[r].retire(plan, posts, work.local)
         for e in plan.entries:
             self.tags[e.block_index] = (e.noise_level, self.cond.id)
+        if timing:
+            torch.cuda.synchronize()
+            self.rank_times.append([sum(a.elapsed_time(b) for a, b in marks.get(r, []))
+                                    for r in range(self.world)])
         self.slot_epoch.wrote([self.slots.slot_of(b) for b in blocks], epoch, items[0][1].masks)
         ev = torch_event(self.torch)
         self.events.append(ev)
