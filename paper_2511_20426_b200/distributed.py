@@ -527,6 +527,7 @@ class EmulatedRanks:
 
     def step(self, plan, mask, pool, vis_lists, posts):
         from .wan import POST_EMIT, _make_update
+        torch = self.torch
         epoch = plan.iteration + 1
         blocks = plan.blocks
         for b in blocks:
