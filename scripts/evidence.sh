@@ -7,6 +7,8 @@ cd "$(dirname "$0")/.."
 mkdir -p gpurun_out
 timeout 900 python -m pytest tests -m gpu -q 2>&1 | tail -3 > gpurun_out/ev_tests.txt
 timeout 900 python bench.py 2>gpurun_out/ev_bench.err | tail -1 > gpurun_out/ev_bench.json
+timeout 600 python scripts/wan_parity_report.py > gpurun_out/ev_parity.json 2>>gpurun_out/ev_bench.err
+timeout 600 python scripts/attn_compare.py 2>/dev/null | grep -v Warn > gpurun_out/ev_attn_compare.txt
 timeout 900 python bench.py --preset 14b --steps 2 --no-cpu --no-switch 2>>gpurun_out/ev_bench.err | tail -1 > gpurun_out/ev_bench_14b.json
 timeout 900 python bench.py --blocks 80 --sink 0 --switch-every 20 --steps 2 --no-cpu --no-seq --no-switch 2>>gpurun_out/ev_bench.err | tail -1 > gpurun_out/ev_bench_longlive.json
 timeout 900 ncu --profile-from-start off --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum \
