@@ -173,26 +173,10 @@ __device__ __forceinline__ void ring_item(int i, int n, int& j, int& is_v) {
 struct SoftmaxBars {
   uint64_t* s_full;
   uint64_t* s_empty;
-  uint64_t* p_half;  // keys [0, 64) of P in smem (split-P pipelining)
   uint64_t* p_full;
   uint64_t* o_ready;
 };
 
-// Split-P pipelining (BC_ATTN_SPLITP): the softmax stores P's first 64 keys
-// and signals the MMA warp before exponentiating the second half, so PV's
-// first four MMAs run under the second half's exps (the single MMA issuer is
-// paced by the tensor pipe -- ~1 queued instruction -- so every wait on a
-// late P drains the pipe).  BC_ATTN_SPEC additionally starts the first
-// half's exps with the current reference max and computes the tile max
-// under them (bit-identical results).  Measured (scripts/attn_variants.sh,
-// 5 entries x 13 blocks): split 1305, split+spec 1343, baseline 1331
-// TFLOP/s -- within run-to-run noise, so both stay off.
-#ifndef BC_ATTN_SPLITP
-#define BC_ATTN_SPLITP 0
-#endif
-#ifndef BC_ATTN_SPEC
-#define BC_ATTN_SPEC 0
-#endif
 
 // One softmax warpgroup: 128 threads, thread <-> query row of its tile.
 template <int kPoly>
@@ -262,94 +246,6 @@ __device__ __forceinline__ void softmax_tile(const AttnParams& prm, uint32_t tme
     };
     float alpha = 1.0f;
     bool bump;
-#if BC_ATTN_SPLITP && BC_ATTN_SPEC
-    // Speculative exponentials: the reference max only moves when a row's
-    // tile max exceeds it by 2^8 (lazy rescale), so for j > 0 the first
-    // half's exps start with the current reference max at once and the tile
-    // max (ALU) is computed under them (MUFU); a row that does need to move
-    // its max redoes the half -- results are bit-identical to max-first.
-    const uint64_t c2 = f2(c, c);
-    uint64_t sum2[2];
-    uint32_t pk0[32];
-    auto half_exps = [&](int hh, float m, uint32_t (&pk)[32]) {
-      const uint64_t nm2 = f2(-m, -m);
-#pragma unroll
-      for (int t = 0; t < 32; ++t) {
-        const int tt = hh * 32 + t;
-        float x0, x1;
-        f2_split(ffma2(f2(s[2 * tt], s[2 * tt + 1]), c2, nm2), x0, x1);
-        const float p0 = ex2(x0);
-        const float p1 = ex2(x1);
-        sum2[t & 1] = fadd2(sum2[t & 1], f2(p0, p1));
-        pk[t] = pack_bf16(p0, p1);
-      }
-    };
-    if (quad == 0) ATRACE(1 + tile_x * 8, j);
-    if (j == 0) {
-      m_used = row_max() * c;
-      alpha = 0.0f;
-      bump = true;
-      sum2[0] = sum2[1] = 0ull;
-      half_exps(0, m_used, pk0);
-    } else {
-      sum2[0] = sum2[1] = 0ull;
-      half_exps(0, m_used, pk0);          // independent of the tile max
-      const float mt = row_max() * c;
-      bump = mt > m_used + kRescaleThresh;
-      if (__any_sync(0xffffffffu, bump)) {
-        if (bump) {
-          const float m_new = fmaxf(m_used, mt);
-          alpha = ex2(m_used - m_new);
-          m_used = m_new;
-        }
-        sum2[0] = sum2[1] = 0ull;
-        half_exps(0, m_used, pk0);
-      }
-    }
-    if (quad == 0) ATRACE(2 + tile_x * 8, j);
-    // PV(j-1) must be complete before O is rescaled or P is overwritten
-    if (j > 0) {
-      mbar_wait(b.o_ready, (j - 1) & 1);
-      tc_fence_after();
-      if (quad == 0) ATRACE(5 + tile_x * 8, j);
-      if (__any_sync(0xffffffffu, bump)) {
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          uint32_t r[32];
-          tmem_ld32(tmem_o + lane_base + k * 32, r);
-          tmem_ld_wait();
-#pragma unroll
-          for (int i = 0; i < 32; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * alpha);
-          tmem_st32(tmem_o + lane_base + k * 32, r);
-        }
-        tmem_st_wait();
-      }
-    }
-#pragma unroll
-    for (int ch = 0; ch < 8; ++ch)
-      sts128(sp_u32 + row * 128 + ((ch ^ (row & 7)) << 4), pk0[4 * ch], pk0[4 * ch + 1], pk0[4 * ch + 2],
-             pk0[4 * ch + 3]);
-    fence_async_shared();
-    tc_fence_before();
-    mbar_arrive(b.p_half);
-    {
-      uint32_t pk1[32];
-      half_exps(1, m_used, pk1);
-#pragma unroll
-      for (int ch = 0; ch < 8; ++ch)
-        sts128(sp_u32 + kHalf + row * 128 + ((ch ^ (row & 7)) << 4), pk1[4 * ch], pk1[4 * ch + 1],
-               pk1[4 * ch + 2], pk1[4 * ch + 3]);
-    }
-    fence_async_shared();
-    tc_fence_before();
-    mbar_arrive(b.p_full);
-    {
-      float sa, sb, sc, sd;
-      f2_split(sum2[0], sa, sb);
-      f2_split(sum2[1], sc, sd);
-      l_sum = l_sum * alpha + ((sa + sc) + (sb + sd));
-    }
-#else
     {
       const float mt = row_max() * c;
       bump = (j == 0) || (mt > m_used + kRescaleThresh);
@@ -359,59 +255,6 @@ __device__ __forceinline__ void softmax_tile(const AttnParams& prm, uint32_t tme
         m_used = m_new;
       }
     }
-#if BC_ATTN_SPLITP
-    const uint64_t c2 = f2(c, c), nm2 = f2(-m_used, -m_used);
-    uint64_t sum2[2] = {0ull, 0ull};  // (+0.0f, +0.0f) pairs
-    if (quad == 0) ATRACE(1 + tile_x * 8, j);
-#pragma unroll
-    for (int hh = 0; hh < 2; ++hh) {
-      uint32_t pk[32];
-#pragma unroll
-      for (int t = 0; t < 32; ++t) {
-        const int tt = hh * 32 + t;
-        float x0, x1;
-        f2_split(ffma2(f2(s[2 * tt], s[2 * tt + 1]), c2, nm2), x0, x1);
-        const float p0 = ex2(x0);
-        const float p1 = ex2(x1);
-        sum2[t & 1] = fadd2(sum2[t & 1], f2(p0, p1));
-        pk[t] = pack_bf16(p0, p1);
-      }
-      if (hh == 0) {
-        if (quad == 0) ATRACE(2 + tile_x * 8, j);
-        // PV(j-1) must be complete before O is rescaled or P is overwritten
-        if (j > 0) {
-          mbar_wait(b.o_ready, (j - 1) & 1);
-          tc_fence_after();
-          if (quad == 0) ATRACE(5 + tile_x * 8, j);
-          if (__any_sync(0xffffffffu, bump)) {
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-              uint32_t r[32];
-              tmem_ld32(tmem_o + lane_base + k * 32, r);
-              tmem_ld_wait();
-#pragma unroll
-              for (int i = 0; i < 32; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * alpha);
-              tmem_st32(tmem_o + lane_base + k * 32, r);
-            }
-            tmem_st_wait();
-          }
-        }
-      }
-      // P half hh -> smem in the UMMA K-major SW128 layout: half h holds keys
-      // [64h, 64h+64); 16-byte chunk q of row r sits at chunk (q ^ (r & 7)).
-#pragma unroll
-      for (int ch = 0; ch < 8; ++ch)
-        sts128(sp_u32 + hh * kHalf + row * 128 + ((ch ^ (row & 7)) << 4), pk[4 * ch], pk[4 * ch + 1],
-               pk[4 * ch + 2], pk[4 * ch + 3]);
-      fence_async_shared();
-      tc_fence_before();
-      mbar_arrive(hh == 0 ? b.p_half : b.p_full);
-    }
-    float sa, sb, sc, sd;
-    f2_split(sum2[0], sa, sb);
-    f2_split(sum2[1], sc, sd);
-    l_sum = l_sum * alpha + ((sa + sc) + (sb + sd));
-#else
     // P = 2^(s*c - m) -> packed bf16 in registers (s dies as P is formed)
     uint64_t sum2[2] = {0ull, 0ull};  // (+0.0f, +0.0f) pairs
     const uint64_t c2 = f2(c, c), nm2 = f2(-m_used, -m_used);
@@ -476,10 +319,7 @@ __device__ __forceinline__ void softmax_tile(const AttnParams& prm, uint32_t tme
     l_sum = l_sum * alpha + ((sa + sc) + (sb + sd));
     fence_async_shared();
     tc_fence_before();
-    mbar_arrive(b.p_half);
     mbar_arrive(b.p_full);
-#endif
-#endif  // BC_ATTN_SPEC
     if (quad == 0) ATRACE(3 + tile_x * 8, j);
   }
   // epilogue: O / l -> bf16
@@ -525,7 +365,6 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* s_full = bars + 7;      // [2] (A, B)
   uint64_t* s_empty = bars + 9;     // [2]
   uint64_t* p_full = bars + 11;     // [2]
-  uint64_t* p_half = bars + 15;     // [2]
   uint64_t* o_ready = bars + 13;    // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 20);
 
@@ -552,7 +391,6 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&s_full[i], 1);
       mbar_init(&s_empty[i], 128);
       mbar_init(&p_full[i], 128);
-      mbar_init(&p_half[i], 128);
       mbar_init(&o_ready[i], 1);
     }
     fence_barrier_init();
@@ -680,15 +518,12 @@ __global__ void __launch_bounds__(kThreads, 1)
           // slot (with V_{j+1}) one MMA group earlier
           if (x == n_q - 1) release(kpos(j + 1));
         }
-        mbar_wait(&p_half[x], j & 1);  // keys [0, 64) of P_x(j) stored
+        mbar_wait(&p_full[x], j & 1);
         ATRACE(18 + x * 4, j);
         if (x == 0) ring_wait(vpos(j, n_tiles));
         if (x == 0) ATRACE(25, j);
         tc_fence_after();
-        issue_pv(x, j, 0, 4);
-        mbar_wait(&p_full[x], j & 1);
-        tc_fence_after();
-        issue_pv(x, j, 4, 8);
+        issue_pv(x, j, 0, kKeys / 16);
         ATRACE(19 + x * 4, j);
       }
       release(vpos(j, n_tiles));
@@ -697,7 +532,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegsSoftmax));
     const int x = (warp >= 8) ? 1 : 0;
     if (x == 0 || has_b) {
-      SoftmaxBars b{&s_full[x], &s_empty[x], &p_half[x], &p_full[x], &o_ready[x]};
+      SoftmaxBars b{&s_full[x], &s_empty[x], &p_full[x], &o_ready[x]};
       softmax_tile<kPoly>(prm, tmem + x * 128, tmem + 256 + x * 128, smem + (x ? Smem::pb : Smem::pa), b, n_tiles,
                    tiles_per_slot, warp & 3, q0 + x * kRows, e, head, x);
     }
