@@ -187,3 +187,33 @@ def test_engine_properties_on_oracle(oracle_engine, default_config):
         assert np.array_equal(seq.outputs[k], cas.outputs[k])
     assert bc.attention_cost(bc.run_cascade(bc.with_fields(cfg, total_frames=3), "p").trace) == 45
     bc.verify_schedule_consistency(base.trace, cfg)
+
+
+def test_row_slices_partition_properties():
+    """rows partition: contiguous, disjoint, covering slices of the n*T rows,
+    balanced to one unit, cut only at query-tile boundaries of an entry, and
+    producer masks consistent with the slices."""
+    from paper_2511_20426_b200.distributed import ROW_TILE, entry_producers, row_slices
+    for n in range(1, 6):
+        for T in (48, 192, 300, 4680):
+            for g in range(1, 9):
+                sl = row_slices(n, T, g)
+                assert len(sl) == g
+                nonempty = [s for s in sl if s[1] > s[0]]
+                assert nonempty[0][0] == 0 and nonempty[-1][1] == n * T
+                for (a0, a1), (b0, b1) in zip(nonempty, nonempty[1:]):
+                    assert a1 == b0
+                unit = ROW_TILE if n * -(-T // ROW_TILE) >= 2 * g else 16
+                for a, b in sl:
+                    for x in (a, b):
+                        assert x == n * T or (x % T) % unit == 0     # tile boundary inside its entry
+                tiles = [len(range(0, T, unit)) * n]
+                counts = []
+                for a, b in sl:
+                    c = sum(1 for e in range(n) for t in range(0, T, unit) if a <= e * T + t < b)
+                    counts.append(c)
+                assert sum(counts) == tiles[0] and max(counts) - min(counts) <= 1
+                masks = entry_producers(sl, n, T)
+                for e, m in enumerate(masks):
+                    owners = {r for r, (a, b) in enumerate(sl) if a < (e + 1) * T and b > e * T}
+                    assert m == sum(1 << r for r in owners) and m
