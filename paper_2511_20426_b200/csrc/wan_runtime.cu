@@ -25,12 +25,20 @@
 
 #include <cstring>
 #include <new>
+#include <string>
 #include <vector>
+
+#include <nvtx3/nvToolsExt.h>
 
 #include "attention.h"
 #include "bc_common.h"
 #include "gemm.h"
 #include "wan_kernels.h"
+
+struct NvtxScope {
+  explicit NvtxScope(const char* name) { nvtxRangePushA(name); }
+  ~NvtxScope() { nvtxRangePop(); }
+};
 
 struct bc_wan_ctx {
   bc_wan_dims dims;
@@ -45,6 +53,7 @@ struct bc_wan_ctx {
   __nv_bfloat16 *text_in, *text_h, *ctx, *text_tmp, *textkv;
   float2 *rope_f, *rope_h, *rope_w;
   bool text_ready, rope_ready;
+  std::vector<std::string> layer_names;  // NVTX range names "layer N"
   bc_wan_peers peers;
   // copy-engine push of fresh K/V to the peers' replicas (multi-GPU)
   bool push_by_copy;
@@ -252,6 +261,7 @@ extern "C" int bc_wan_create(const bc_wan_dims* dims, const bc_wan_params* param
   c->R = c->E * c->T;
   carve(c, *dims, static_cast<char*>(workspace));
   c->text_ready = false;
+  for (int l = 0; l < dims->layers; ++l) c->layer_names.push_back("layer " + std::to_string(l));
   *out = c;
   return BC_OK;
 }
@@ -626,8 +636,12 @@ extern "C" int bc_wan_step(bc_wan_ctx* c, const bc_batch* batch, const bc_wan_up
   if (!c->text_ready) return bc_fail(BC_ERR_CONTRACT, "bc_wan_step: bc_wan_set_text not called");
   if (c->peers.n_peers > 0) return bc_fail(BC_ERR_CONTRACT, "bc_wan_step: peers attached, use bc_wan_step_dist");
   cudaStream_t st = (cudaStream_t)stream;
+  // NVTX ranges (free without a tool attached): one per step and per layer,
+  // so ncu --nvtx / nsys timelines map launches to (iteration, layer)
+  NvtxScope step_range("bc_wan_step");
   RC(stage_begin(c, batch, upd, nullptr, status, st));
   for (int l = 0; l < c->dims.layers; ++l) {
+    NvtxScope layer_range(c->layer_names[l].c_str());
     RC(stage_layer_a(c, l, st));
     RC(stage_layer_b(c, l, st));
   }
@@ -679,6 +693,9 @@ extern "C" int bc_wan_step_dist(bc_wan_ctx* c, const bc_batch* batch, const bc_w
   if (!c->text_ready) return bc_fail(BC_ERR_CONTRACT, "bc_wan_step_dist: bc_wan_set_text not called");
   if (dist->epoch < 1) return bc_fail(BC_ERR_CONTRACT, "bc_wan_step_dist: epoch must be >= 1");
   cudaStream_t st = (cudaStream_t)stream;
+  static const char* kStageNames[] = {"bc_wan_step_dist", "begin", "layer part A", "layer part B", "head",
+                                      "update"};
+  NvtxScope range(kStageNames[(dist->stage >= -1 && dist->stage <= 4) ? dist->stage + 1 : 0]);
   switch (dist->stage) {
     case -1:
       if (!batch || !upd) return bc_fail(BC_ERR_CONTRACT, "bc_wan_step_dist: null batch");
