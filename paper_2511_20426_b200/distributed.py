@@ -400,7 +400,7 @@ class DistWanSession:
             lats, eps, outs, nexts = self.rep.prepare(plan, posts, work.local, init_req, init_dst,
                                                       eps_req, eps_dst)
             if init_req or eps_req:
-                self.noise.fetch(init_req + eps_req, init_dst + eps_dst)
+                self._fetch_noise(init_req + eps_req, init_dst + eps_dst)
             bt = N.make_batch(self.cfg.block_size, work.blocks,
                               [plan.entries[i].noise_level for i in work.local],
                               [self.slots.slot_of(b) for b in work.blocks],
@@ -420,6 +420,33 @@ class DistWanSession:
         for e in plan.entries:
             self.tags[e.block_index] = (e.noise_level, self.cond.id)
         self._mark()
+
+    def _fetch_noise(self, keys, dests):
+        """Counter-keyed noise for this step.  In the rows partition every
+        rank needs every entry's noise; with NCCL the host generation is
+        split round-robin over the ranks and the draws are all-gathered on
+        the device (a few MB per iteration) instead of every rank drawing
+        all of them on the node's shared host cores.  Bit-identical either
+        way: each key's draw is a pure function of the key."""
+        dist, torch = self.dist, self.torch
+        nccl = dist.get_backend() == "nccl"
+        forced = os.environ.get("BC_NOISE_GATHER") == "1"   # test hook (gloo: gathers on the host)
+        if self.mode != "rows" or not (nccl or forced) or not hasattr(self.noise, "stream"):
+            self.noise.fetch(keys, dests)
+            return
+        G = self.world
+        chunk = -(-len(keys) // G)
+        mine = keys[self.rank::G]
+        where = "cuda" if nccl else "cpu"
+        buf = torch.zeros((chunk,) + tuple(self.shape), dtype=torch.float32, device=where)
+        if mine:
+            self.noise.fetch(mine, [buf[i] for i in range(len(mine))])
+            if where == "cpu":
+                torch.cuda.current_stream().synchronize()
+        gathered = torch.empty((G * chunk,) + tuple(self.shape), dtype=torch.float32, device=where)
+        dist.all_gather_into_tensor(gathered, buf)
+        for i, dst in enumerate(dests):   # key i was drawn by rank i % G as its (i // G)-th
+            dst.copy_(gathered[(i % G) * chunk + i // G], non_blocking=where == "cuda")
 
     def kv_handle(self, block):
         from .kvpool import SlotKV

@@ -20,7 +20,9 @@ def _free_port():
 
 
 def _rank(rank, world, port, q, mode, shard):
-    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), BC_TEMPORAL_SHARD=shard)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port),
+                      BC_TEMPORAL_SHARD=shard.split("+")[0],
+                      BC_NOISE_GATHER="1" if shard.endswith("+gather") else "0")
     import torch
     import torch.distributed as dist
     torch.cuda.set_device(0)
@@ -38,8 +40,10 @@ def _rank(rank, world, port, q, mode, shard):
 
 
 @pytest.mark.parametrize("mode,shard", [("bidirectional", "rows"), ("causal", "rows"),
-                                        ("bidirectional", "blocks")])
+                                        ("bidirectional", "blocks"), ("bidirectional", "rows+gather")])
 def test_two_processes_one_gpu(mode, shard):
+    """rows+gather: the host noise draws are split over the ranks and
+    all-gathered (the NCCL path, here over gloo through the host)."""
     import torch.multiprocessing as mp
     import paper_2511_20426_b200 as bc
     from paper_2511_20426_b200.wan import WanWeights
