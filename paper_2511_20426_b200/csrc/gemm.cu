@@ -288,12 +288,42 @@ __global__ void __launch_bounds__(kThreads, 1)
       int mb, nb;
       tile_coords(tile, num_m, num_n, mb, nb);
       const int m0 = mb * TM + (int)rank * BM, n0 = nb * BN;
+      const int row_base = m0 + (int)quad * 32;
+      // residual epilogue: the C / gate loads of chunk c + 1 are issued before
+      // chunk c is processed (and chunk 0's before the accumulator wait), so
+      // one DRAM round trip per 16-column chunk no longer serialises the
+      // epilogue -- at K = 1536 the epilogue was longer than the mainloop
+      float4 res_n[4], g_n[4];
+      auto load_res = [&](int c) {
+        const int colc = n0 + c;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int row = row_base + i * 8 + sub_row;
+          res_n[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+          g_n[i] = make_float4(1.f, 1.f, 1.f, 1.f);
+          if (row < M) {
+            res_n[i] = *reinterpret_cast<const float4*>(static_cast<float*>(c_ptr) + (size_t)row * N + colc + sub_col);
+            if (gate)
+              g_n[i] = __ldg(reinterpret_cast<const float4*>(gate + (size_t)((gate_row0 + row) / rows_per_gate) * gate_stride +
+                                                             colc + sub_col));
+          }
+        }
+      };
+      if (MODE == kEpiResidualF32) load_res(c_begin);
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       if (ew == 0 && lane_id() == 0) GEMM_TRACE(2, it);
-      const int row_base = m0 + (int)quad * 32;
 #pragma unroll 1
       for (int c = c_begin; c < c_begin + BN / 2; c += kChunk) {
+        float4 res[4], g[4];
+        if (MODE == kEpiResidualF32) {
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            res[i] = res_n[i];
+            g[i] = g_n[i];
+          }
+          if (c + kChunk < c_begin + BN / 2) load_res(c + kChunk);
+        }
         uint32_t r[16];
         __syncwarp();
         tmem_ld16(tmem_base + ((quad * 32) << 16) + acc * BN + c, r);
@@ -317,19 +347,6 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         __syncwarp();
         if (MODE == kEpiResidualF32) {
-          float4 res[4], g[4];
-#pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            const int row = row_base + i * 8 + sub_row;
-            res[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-            g[i] = make_float4(1.f, 1.f, 1.f, 1.f);
-            if (row < M) {
-              res[i] = *reinterpret_cast<const float4*>(static_cast<float*>(c_ptr) + (size_t)row * N + col + sub_col);
-              if (gate)
-                g[i] = __ldg(reinterpret_cast<const float4*>(gate + (size_t)((gate_row0 + row) / rows_per_gate) * gate_stride +
-                                                             col + sub_col));
-            }
-          }
 #pragma unroll
           for (int i = 0; i < 4; ++i) {
             const int lr = i * 8 + sub_row;
