@@ -164,6 +164,46 @@ def cpu_sample_desc(cfg):
             f"fps = 12 frames / (sample x {cfg.layers * min(cfg.cascade_width, cfg.num_blocks)})")
 
 
+TOY_CFG1 = dict(layers=4, latent_dim=256, heads=2, head_dim=128, cond_dim=256, total_frames=18,
+                offset=1, window_blocks=7, sink_blocks=1, attention_mode="bidirectional")
+
+
+def toy_config1_times(bc):
+    """BASELINE configs[0]: the reference toy model (L4, D256, 6 blocks, o=1,
+    bidirectional) through run_cascade on the device (fp64 kernels) and through
+    the same engine driven by the numpy oracle forward on the host."""
+    import torch
+    from paper_2511_20426_b200 import engine
+    from oracle.loop import oracle_runtime
+    cfg1 = bc.CascadeConfig(**TOY_CFG1).validate()
+    w = bc.init_model(WEIGHT_SEED, cfg1.layers, cfg1.heads, cfg1.latent_dim, cfg1.cond_dim)
+
+    def med(f, n):
+        ts = []
+        for _ in range(n):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            f()
+            torch.cuda.synchronize()
+            ts.append(time.perf_counter() - t0)
+        return statistics.median(ts) * 1e3
+    gpu = bc.run_cascade(cfg1, "a red cube", weights=w)
+    gpu_ms = med(lambda: bc.run_cascade(cfg1, "a red cube", weights=w), 5)
+    orig = engine._runtime_for
+    engine._runtime_for = oracle_runtime
+    try:
+        cpu = bc.run_cascade(cfg1, "a red cube", weights=w)
+        cpu_ms = med(lambda: bc.run_cascade(cfg1, "a red cube", weights=w), 3)
+    finally:
+        engine._runtime_for = orig
+    import numpy as np
+    rel = max(float(np.linalg.norm(gpu.outputs[b] - cpu.outputs[b]) / np.linalg.norm(cpu.outputs[b]))
+              for b in cpu.outputs)
+    return {"workload": "reference toy model, L4 D256 2x128 heads, 6 blocks (18 frames), o=1, bidirectional",
+            "device_fp64_ms_per_run": round(gpu_ms, 2), "oracle_cpu_ms_per_run": round(cpu_ms, 2),
+            "max_block_rel_l2_vs_oracle": rel}
+
+
 def metric_name(args):
     return f"generated frames/sec (cascaded, Wan2.1-{args.preset.upper()}-shaped, 480x832)"
 
@@ -318,6 +358,13 @@ def run_ours(args, cfg):
                                                     (nxt.wall_clock - prev), 2),
                             "e2e_fps": end_to_end_fps(r.trace)}
 
+    # ---- the reference's own CPU-runnable case (BASELINE configs[0]): the toy
+    # model of the reference package, fp64 on the device, vs the oracle port
+    # of it on the host (the reference code itself is not on the box) ----
+    toy = None
+    if world == 1 and not args.no_cpu:
+        toy = toy_config1_times(bc)
+
     S = cfg.block_size
     lat_bytes = S * cfg.latent_dim * 4
     h2d = len(run_noise_keys(cfg)) * lat_bytes + cfg.text_len * cfg.text_dim * 4
@@ -359,6 +406,7 @@ def run_ours(args, cfg):
         "sequential": {"e2e_fps": seq_e2e, "streaming_fps": seq_stream},
         "cascade_over_sequential_streaming": stream_fps / seq_stream if seq_stream else None,
         "prompt_switch": switch,
+        "config1_toy": toy,
         "roofline": {"bound": "tensor", "kernel": dom, "achieved": achieved, "peak": peak,
                      "unit": "TFLOP/s", "frac": achieved / peak if achieved else None,
                      "traffic": traffic, "peak_kind": f"{peak_kind} bf16 sustained",

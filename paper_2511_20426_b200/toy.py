@@ -151,6 +151,7 @@ class ToySession:
                    for _ in range(N.MAX_ENTRIES)]
         self.events = []
         self.stalls = {}
+        self._staged = []
         self.set_conditioning(conditioning)
         self._mark()
 
@@ -160,8 +161,12 @@ class ToySession:
         self.events.append(ev)
 
     def _upload_noise(self, block, pass_index):
-        host = self.noise.block_noise(block, pass_index, block * self.S, self.S)
-        return self.torch.from_numpy(host).cuda(non_blocking=False)
+        # pinned staging + asynchronous copy: a pageable .cuda() waits for the
+        # whole queue and made the host loop wait on the device every draw
+        host = self.torch.from_numpy(self.noise.block_noise(block, pass_index, block * self.S, self.S))
+        pinned = host.pin_memory()
+        self._staged.append(pinned)   # alive until the session ends
+        return pinned.cuda(non_blocking=True)
 
     def set_conditioning(self, cond):
         self.cond = cond
@@ -245,4 +250,5 @@ class ToySession:
                 ev.wall_seconds -= s0.elapsed_time(s1) / 1e3
 
     def close(self):
-        pass
+        self.torch.cuda.current_stream().synchronize()
+        self._staged.clear()
