@@ -181,8 +181,8 @@ int bc_wan_step(bc_wan_ctx* ctx, const bc_batch* batch, const bc_wan_update* upd
 
 /* ---- multi-GPU temporal parallelism (one process per GPU, NVLink P2P) ----
  * Every rank holds a full KV-arena replica.  Fresh K/V rows computed by a
- * rank are copied into every peer's replica (copy engines, or P2P stores
- * from the q/k kernel with BC_KV_PUSH=kernel) and the rank publishes
+ * rank are stored into every peer's replica (P2P stores from the q/k
+ * kernel; BC_KV_PUSH=copy: side-stream cudaMemcpyAsync) and the rank publishes
  * epoch into peers' flags[layer][slot][my_rank]; attention waits (per
  * visible slot) until the flag of every producer rank in pmask is >= need
  * before its first tile of that slot; the head kernel publishes

@@ -30,8 +30,8 @@ struct LnArgs {
 };
 
 // Multi-GPU temporal parallelism: every rank keeps a full KV-arena replica;
-// fresh K/V rows reach every peer's arena over NVLink (copy engines, or P2P
-// stores from the q/k kernel) and (layer, slot, producer rank) ready epochs
+// fresh K/V rows reach every peer's arena over NVLink (P2P stores from the
+// q/k kernel; BC_KV_PUSH=copy: side-stream copies) and (layer, slot, producer rank) ready epochs
 // are published into each peer's flag array [L][n_slots][n_ranks];
 // iteration-done epochs guard slot reuse.
 #define BC_MAX_PEERS 8

@@ -55,7 +55,7 @@ struct bc_wan_ctx {
   bool text_ready, rope_ready;
   std::vector<std::string> layer_names;  // NVTX range names "layer N"
   bc_wan_peers peers;
-  // copy-engine push of fresh K/V to the peers' replicas (multi-GPU)
+  // BC_KV_PUSH=copy: side-stream push of fresh K/V to the peers' replicas
   bool push_by_copy;
   cudaStream_t side;
   cudaEvent_t ev_qk, ev_side;
@@ -484,11 +484,11 @@ int stage_layer_a(bc_wan_ctx* c, int l, cudaStream_t st) {
     RC(timed(kBandwidth, 0.0, 12.0 * R * d, st, [&] { return bc::launch_qk_norm_rope(c->qkv, R, d, T, qa, st); }));
   }
   if (c->peers.n_peers > 0 && c->push_by_copy && S.epoch > 0) {
-    // copy engines move this rank's fresh K/V rows of layer l (per entry: the
-    // token range it computed, K and V halves of the slot's [2][T][d]
-    // matrix) into every peer replica, then a stream memory op publishes
-    // flags[layer][slot][my_rank] = epoch -- no SM is needed, so a peer's
-    // spinning attention can never starve the transfer.
+    // (BC_KV_PUSH=copy) cudaMemcpyAsync moves this rank's fresh K/V rows of
+    // layer l (per entry: the token range it computed, K and V halves of the
+    // slot's [2][T][d] matrix) into every peer replica, then a stream memory
+    // op publishes flags[layer][slot][my_rank] = epoch.  Safe only when the
+    // copy runs on a copy engine (see bc_wan_set_peers).
     auto wv = write_value32();
     if (!wv) return bc_fail(BC_ERR_CUDA, "cuStreamWriteValue32 unavailable");
     BC_CUDA(cudaEventRecord(c->ev_qk, st));
