@@ -223,10 +223,51 @@ def _make_update(posts, latents, eps, outs, next_levels):
     return u
 
 
+class _Lease:
+    """A session's view of a (pooled) context for the pool's KV handles:
+    revoked when the session closes, so a finished run's handles can never
+    read a later session's KV out of a reused arena."""
+
+    def __init__(self, ctx):
+        self.ctx = ctx
+        self.layers = ctx.layers
+
+    def read(self, slot, layer, which):
+        if self.ctx is None:
+            raise ContractViolation("KV of a closed session is no longer resident")
+        return self.ctx.read_kv(slot, layer, which)
+
+
 class WanRuntime:
     def __init__(self, weights: WanWeights):
         self.weights = weights
         self.cfg = weights.config
+        self._cached = None   # (key, _Ctx) kept between sessions (arena, workspace, text K/V)
+
+    def acquire_ctx(self, width, n_slots):
+        """A context for a session: the cached one when the geometry matches
+        (no allocation / arena setup / text re-projection for a repeated
+        prompt), else a new one."""
+        key = (width, n_slots)
+        if self._cached is not None:
+            ck, ctx = self._cached
+            self._cached = None
+            if ck == key:
+                return ctx
+            ctx.close()
+        return _Ctx(self.weights, width, n_slots)
+
+    def release_ctx(self, ctx):
+        N.torch_mod().cuda.current_stream().synchronize()
+        if self._cached is not None:
+            self._cached[1].close()
+        self._cached = ((ctx.max_entries, ctx.n_slots), ctx)
+
+    def release_cached(self):
+        """Free the cached context's device memory (KV arena + workspace)."""
+        if self._cached is not None:
+            self._cached[1].close()
+            self._cached = None
 
     # reference operator contract (denoiser.forward) ----------------------
     def forward(self, batch, pool_kv, mask):
@@ -376,7 +417,8 @@ class WanSession:
         self.torch = torch
         self.rt, self.cfg = rt, config
         width = min(config.cascade_width, config.num_blocks)
-        self.ctx = _Ctx(rt.weights, width, config.window_blocks + config.sink_blocks + width + 1)
+        self.ctx = rt.acquire_ctx(width, config.window_blocks + config.sink_blocks + width + 1)
+        self.lease = _Lease(self.ctx)
         self.slots = SlotAllocator(self.ctx.n_slots)
         self.shape = (config.block_size, config.latent_channels, config.latent_height,
                       config.latent_width)
@@ -474,7 +516,7 @@ class WanSession:
 
     def kv_handle(self, block):
         level, cid = self.tags[block]
-        return SlotKV(self.ctx, self.slots.slot_of(block), block, level, cid, self.cfg.block_size)
+        return SlotKV(self.lease, self.slots.slot_of(block), block, level, cid, self.cfg.block_size)
 
     def release(self, block):
         self.slots.release(block)
@@ -489,7 +531,9 @@ class WanSession:
 
     def release_device(self):
         self.torch.cuda.current_stream().synchronize()
-        self.ctx.close()
+        if self.lease.ctx is not None:
+            self.lease.ctx = None
+            self.rt.release_ctx(self.ctx)
         self.latents.clear()
         self.final.clear()
 
