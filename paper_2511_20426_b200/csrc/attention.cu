@@ -434,13 +434,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint32_t ep = need >> 8;
             const uint32_t* f = prm.flags + (size_t)(prm.flag_base + kv_slot) * prm.n_ranks;
             for (uint32_t m = need & 0xffu; m; m &= m - 1) {
-              const uint32_t* fr = f + (__ffs(m) - 1);
-              uint32_t v;
-              for (;;) {
-                asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(fr) : "memory");
-                if (v >= ep) break;
-                __nanosleep(256);
-              }
+              spin_until_geq(f + (__ffs(m) - 1), ep, 256);
             }
             asm volatile("fence.proxy.async.global;" ::: "memory");
           }

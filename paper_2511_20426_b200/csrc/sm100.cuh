@@ -223,4 +223,27 @@ __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
   return *reinterpret_cast<uint32_t*>(&v);
 }
 
+
+// Bounded spin on a cross-GPU flag: a peer that died (or a protocol bug)
+// must not hang the device forever -- after `timeout_ns` of global time the
+// kernel traps, the context reports an error and the host raises.
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ void spin_until_geq(const uint32_t* flag, uint32_t want, uint32_t sleep_ns,
+                                               uint64_t timeout_ns = 60ull * 1000 * 1000 * 1000) {
+  uint32_t v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
+  if (v >= want) return;
+  const uint64_t t0 = globaltimer_ns();
+  for (;;) {
+    __nanosleep(sleep_ns);
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
+    if (v >= want) return;
+    if (globaltimer_ns() - t0 > timeout_ns) asm volatile("trap;");
+  }
+}
+
 }  // namespace bc

@@ -14,6 +14,7 @@
 
 #include "bc_common.h"
 #include "wan_kernels.h"
+#include "sm100.cuh"
 
 namespace bc {
 namespace {
@@ -40,7 +41,7 @@ __device__ __forceinline__ void wait_peers_done(const PeerArgs& pa) {
   if (threadIdx.x == 0) {
     for (int r = 0; r < pa.n_ranks; ++r) {
       if (r == pa.my_rank) continue;
-      while (ld_acquire_sys(pa.my_done + r) < pa.wait_done) __nanosleep(128);
+      spin_until_geq(pa.my_done + r, pa.wait_done, 128);
     }
   }
   __syncthreads();
