@@ -54,6 +54,14 @@ struct bc_wan_ctx {
   float2 *rope_f, *rope_h, *rope_w;
   bool text_ready, rope_ready;
   std::vector<std::string> layer_names;  // NVTX range names "layer N"
+  // CUDA graphs of the single-GPU step, one executable per batch width
+  // (the kernel sequence -- incl. the GEMM tile variants -- depends on it);
+  // each step is re-captured and its parameters pushed with
+  // cudaGraphExecUpdate, so the ~400 launches reach the GPU as one graph
+  cudaGraphExec_t graph_exec[BC_MAX_ENTRIES + 1] = {};
+  bool width_seen[BC_MAX_ENTRIES + 1] = {};
+  cudaStream_t gstream = nullptr;  // capture / launch stream (the caller's may be the legacy stream)
+  cudaEvent_t gev_in = nullptr, gev_out = nullptr;
   bc_wan_peers peers;
   // BC_KV_PUSH=copy: side-stream push of fresh K/V to the peers' replicas
   bool push_by_copy;
@@ -267,6 +275,19 @@ extern "C" int bc_wan_create(const bc_wan_dims* dims, const bc_wan_params* param
 }
 
 extern "C" int bc_wan_destroy(bc_wan_ctx* ctx) {
+  if (ctx) {
+    for (auto& ex : ctx->graph_exec)
+      if (ex) {
+        cudaGraphExecDestroy(ex);
+        ex = nullptr;
+      }
+    if (ctx->gstream) {
+      cudaStreamSynchronize(ctx->gstream);
+      cudaStreamDestroy(ctx->gstream);
+      cudaEventDestroy(ctx->gev_in);
+      cudaEventDestroy(ctx->gev_out);
+    }
+  }
   if (ctx && ctx->side) {
     cudaStreamSynchronize(ctx->side);
     cudaStreamDestroy(ctx->side);
@@ -639,13 +660,72 @@ extern "C" int bc_wan_step(bc_wan_ctx* c, const bc_batch* batch, const bc_wan_up
   // NVTX ranges (free without a tool attached): one per step and per layer,
   // so ncu --nvtx / nsys timelines map launches to (iteration, layer)
   NvtxScope step_range("bc_wan_step");
-  RC(stage_begin(c, batch, upd, nullptr, status, st));
-  for (int l = 0; l < c->dims.layers; ++l) {
-    NvtxScope layer_range(c->layer_names[l].c_str());
-    RC(stage_layer_a(c, l, st));
-    RC(stage_layer_b(c, l, st));
+  auto run_all = [&]() -> int {
+    RC(stage_begin(c, batch, upd, nullptr, status, st));
+    for (int l = 0; l < c->dims.layers; ++l) {
+      NvtxScope layer_range(c->layer_names[l].c_str());
+      RC(stage_layer_a(c, l, st));
+      RC(stage_layer_b(c, l, st));
+    }
+    return stage_end(c, st);
+  };
+  static int graphs = -1;
+  if (graphs < 0) {
+    const char* e = getenv("BC_GRAPHS");
+    graphs = e ? atoi(e) != 0 : 1;
   }
-  return stage_end(c, st);
+  // per-kernel profiling needs events between the launches, and the first
+  // step of each batch width initialises per-kernel static state (function
+  // attributes, cluster occupancy of its GEMM tile variants) that must not
+  // happen inside a capture: run those eagerly
+  const int n = batch->n_entries;
+  if (!graphs || g_prof || n < 1 || n > BC_MAX_ENTRIES || !c->width_seen[n]) {
+    if (n >= 1 && n <= BC_MAX_ENTRIES) c->width_seen[n] = true;
+    return run_all();
+  }
+  if (!c->gstream) {
+    BC_CUDA(cudaStreamCreateWithFlags(&c->gstream, cudaStreamNonBlocking));
+    BC_CUDA(cudaEventCreateWithFlags(&c->gev_in, cudaEventDisableTiming));
+    BC_CUDA(cudaEventCreateWithFlags(&c->gev_out, cudaEventDisableTiming));
+  }
+  // capture on the context's own stream; ordered after the caller's stream
+  // work before the launch and before the caller's later work after it
+  const cudaStream_t caller = st;
+  st = c->gstream;
+  cudaGraph_t graph = nullptr;
+  BC_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+  const int rc = run_all();
+  const cudaError_t ec = cudaStreamEndCapture(st, &graph);
+  if (rc || ec != cudaSuccess) {
+    if (graph) cudaGraphDestroy(graph);
+    (void)cudaGetLastError();
+    if (rc) return rc;
+    return bc_fail(BC_ERR_CUDA, "bc_wan_step: graph capture -> %s", cudaGetErrorString(ec));
+  }
+  cudaGraphExec_t& ex = c->graph_exec[n];
+  if (ex) {
+    cudaGraphExecUpdateResultInfo info;
+    if (cudaGraphExecUpdate(ex, graph, &info) != cudaSuccess) {
+      (void)cudaGetLastError();
+      cudaGraphExecDestroy(ex);
+      ex = nullptr;
+    }
+  }
+  if (!ex) {
+    const cudaError_t ei = cudaGraphInstantiate(&ex, graph, 0);
+    if (ei != cudaSuccess) {
+      cudaGraphDestroy(graph);
+      ex = nullptr;
+      return bc_fail(BC_ERR_CUDA, "bc_wan_step: graph instantiate -> %s", cudaGetErrorString(ei));
+    }
+  }
+  cudaGraphDestroy(graph);
+  BC_CUDA(cudaEventRecord(c->gev_in, caller));
+  BC_CUDA(cudaStreamWaitEvent(st, c->gev_in, 0));
+  BC_CUDA(cudaGraphLaunch(ex, st));
+  BC_CUDA(cudaEventRecord(c->gev_out, st));
+  BC_CUDA(cudaStreamWaitEvent(caller, c->gev_out, 0));
+  return BC_OK;
 }
 
 extern "C" int bc_wan_set_peers(bc_wan_ctx* c, const bc_wan_peers* peers) {
