@@ -175,9 +175,12 @@ typedef struct {
   float* out[BC_MAX_ENTRIES];         /* post 1 / 3 */
 } bc_wan_update;
 
-/* One cascade iteration: batched forward of every entry + fused update. */
+/* One cascade iteration: batched forward of every entry + fused update.
+ * Launched as a CUDA graph (re-captured per step, one executable per batch
+ * width) unless disabled; results are identical either way. */
 int bc_wan_step(bc_wan_ctx* ctx, const bc_batch* batch, const bc_wan_update* upd,
                 int32_t* status, void* stream);
+int bc_wan_set_graphs(int on); /* 1: CUDA graphs (default, or BC_GRAPHS env), 0: eager launches */
 
 /* ---- multi-GPU temporal parallelism (one process per GPU, NVLink P2P) ----
  * Every rank holds a full KV-arena replica.  Fresh K/V rows computed by a

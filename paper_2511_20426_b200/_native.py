@@ -107,6 +107,7 @@ _SIGS = {
     "bc_wan_create": (C.c_int, [C.POINTER(WanDims), C.POINTER(WanParams), C.c_void_p,
                                 C.c_void_p, C.c_int64, C.POINTER(C.c_void_p)]),
     "bc_wan_destroy": (C.c_int, [C.c_void_p]),
+    "bc_wan_set_graphs": (C.c_int, [C.c_int]),
     "bc_wan_set_text": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
     "bc_wan_step": (C.c_int, [C.c_void_p, C.POINTER(Batch), C.POINTER(WanUpdate),
                               C.c_void_p, C.c_void_p]),

@@ -162,6 +162,7 @@ struct ProfRec {
   double flops, bytes;
 };
 bool g_prof = false;
+int g_graphs = -1;  // -1: BC_GRAPHS env (default on)
 std::vector<ProfRec> g_recs;
 std::vector<cudaEvent_t> g_free_events;
 
@@ -217,6 +218,12 @@ const T* at(const void* base, int64_t elems) {
 }
 
 }  // namespace
+
+// Launch single-GPU steps as CUDA graphs (1, default) or eagerly (0).
+extern "C" int bc_wan_set_graphs(int on) {
+  g_graphs = on ? 1 : 0;
+  return BC_OK;
+}
 
 extern "C" int bc_profile_enable(int on) {
   g_prof = on != 0;
@@ -669,11 +676,11 @@ extern "C" int bc_wan_step(bc_wan_ctx* c, const bc_batch* batch, const bc_wan_up
     }
     return stage_end(c, st);
   };
-  static int graphs = -1;
-  if (graphs < 0) {
+  if (g_graphs < 0) {
     const char* e = getenv("BC_GRAPHS");
-    graphs = e ? atoi(e) != 0 : 1;
+    g_graphs = e ? atoi(e) != 0 : 1;
   }
+  const int graphs = g_graphs;
   // per-kernel profiling needs events between the launches, and the first
   // step of each batch width initialises per-kernel static state (function
   // attributes, cluster occupancy of its GEMM tile variants) that must not

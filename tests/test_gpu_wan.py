@@ -228,3 +228,22 @@ def test_wan_longlive_style_run(tiny, monkeypatch):
         cpu = bc.run_cascade(cfg, "scene 0", weights=w, switches=sw)
     for b in range(cfg.num_blocks):
         assert rel(gpu.outputs[b], cpu.outputs[b]) < RUN_TOL, b
+
+
+def test_wan_graph_launch_bit_identical(tiny):
+    """CUDA-graph launches of the step (the default) and eager launches give
+    bit-identical results (same kernels, same arguments)."""
+    import paper_2511_20426_b200 as bc
+    from paper_2511_20426_b200 import _native as N
+    cfg, w, _ = tiny
+    cfg = bc.with_fields(cfg, total_frames=21)
+    try:
+        N.lib().bc_wan_set_graphs(1)
+        a = bc.run_cascade(cfg, "graphs", weights=w)
+        b = bc.run_cascade(cfg, "graphs", weights=w)     # steps replayed through the cached graphs
+        N.lib().bc_wan_set_graphs(0)
+        c = bc.run_cascade(cfg, "graphs", weights=w)
+    finally:
+        N.lib().bc_wan_set_graphs(1)
+    for k in a.outputs:
+        assert np.array_equal(a.outputs[k], c.outputs[k]) and np.array_equal(b.outputs[k], c.outputs[k])
