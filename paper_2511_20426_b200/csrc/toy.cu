@@ -2,11 +2,11 @@
 // float64 on the device, plus the renoise kernel shared by both model
 // families.
 //
-// The toy has one token per latent frame and D <= a few hundred, so each
-// phase is one CTA per batch entry; the whole forward is 2 + 2L launches.
-// The work is launch-bound by construction -- this path exists for
-// numeric parity with the reference's float64 forward (its only
-// reference-pinned numeric oracle), not for throughput.
+// The toy has one token per latent frame and D <= a few hundred; every
+// phase is a grid of (entry, 32-column chunk) CTAs with warp-level dot
+// products, 2 + 3L launches per forward.  This path exists for numeric
+// parity with the reference's float64 forward (its only reference-pinned
+// numeric oracle); it is launch-bound by construction.
 //
 // Phase order per layer mirrors forward() (denoiser.py:333-353): QKV for
 // every entry (fresh K/V written to the entry's arena slot), then attention
@@ -31,24 +31,51 @@ struct ToyPtrs {
   double* x0[BC_MAX_ENTRIES];
 };
 
-__device__ __forceinline__ double block_sum(double v, double* red) {
+
+// Every kernel below spreads one entry's work over many CTAs: grid
+// (entry, 32-column chunk of the output), one warp per output element with
+// the dot product split over the lanes (fixed xor-tree reduction order, so
+// results are deterministic and independent of the batch).  The first
+// version ran each phase as ONE CTA per entry with thread-serial 256-long
+// dot products and a single-thread softmax: ~1 ms per iteration, no faster
+// than the numpy oracle on the host.
+
+__device__ __forceinline__ double warp_sum_d(double v) {
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  return v;
+}
+__device__ __forceinline__ double warp_max_d(double v) {
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+// sum_k a[k] * b[k] over k < n, lanes interleaved, then the xor tree
+__device__ __forceinline__ double warp_dot(const double* a, const double* b, int n) {
+  const int lane = threadIdx.x & 31;
+  double acc = 0.0;
+  for (int k = lane; k < n; k += 32) acc += a[k] * b[k];
+  return warp_sum_d(acc);
+}
+
+constexpr int kCols = 32;  // output columns per CTA
+
+// RMS-normalise the S rows of h into smem hn (every CTA of the entry redoes
+// this: S*D reads, negligible)
+__device__ __forceinline__ void rms_rows_smem(const double* h, double* hn, int S, int D) {
+  const int warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int i = warp; i < S; i += nw) {
+    const double ss = warp_dot(h + (size_t)i * D, h + (size_t)i * D, D);
+    const double inv = 1.0 / sqrt(ss / (double)D + kRmsEps);
+    for (int k = threadIdx.x & 31; k < D; k += 32) hn[i * D + k] = h[(size_t)i * D + k] * inv;
+  }
   __syncthreads();
-  if (lane == 0) red[warp] = v;
-  __syncthreads();
-  double t = 0.0;
-  // fixed order over warps -> deterministic
-  for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
-  return t;
 }
 
 // h[e] = x W_in^T + pos(b*S+i) + W_level feats(level) + W_cond cond
 // (embed_entry, denoiser.py:234-250; _position_encoding 214-221;
-//  _level_features 224-227)
+//  _level_features 224-227).  grid (n, D / 32)
 __global__ void toy_embed(bc_toy_weights w, bc_batch bt, ToyPtrs p, double* hidden,
                           int32_t* status) {
-  const int e = blockIdx.x;
+  const int e = blockIdx.x, j0 = blockIdx.y * kCols;
   const int S = bt.block_size, D = w.dim, Dc = w.cond_dim;
   const double* x = p.x[e];
   const double* c = p.cond[e];
@@ -60,135 +87,129 @@ __global__ void toy_embed(bc_toy_weights w, bc_batch bt, ToyPtrs p, double* hidd
     feat[k] = sin(2.0 * M_PI * s * (double)(k + 1));
     feat[k + kLevelFeats / 2] = cos(2.0 * M_PI * s * (double)(k + 1));
   }
-  for (int idx = threadIdx.x; idx < S * D; idx += blockDim.x) {
-    const int i = idx / D, j = idx % D;
-    const double* xi = x + (size_t)i * D;
-    if (!isfinite(xi[j])) atomicCAS(status, 0, 1 + bt.block_index[e]);
-    double acc = 0.0;
-    const double* wr = w.w_in + (size_t)j * D;
-    for (int k = 0; k < D; ++k) acc += xi[k] * wr[k];
-    const double pos = (double)(bt.block_index[e] * S + i);
-    const double expo = 2.0 * (double)(j >> 1) / (double)D;
-    const double ang = pos / pow(10000.0, expo);
-    acc += (j & 1) ? cos(ang) : sin(ang);
-    double lv = 0.0;
-    for (int f = 0; f < kLevelFeats; ++f) lv += w.w_level[(size_t)j * kLevelFeats + f] * feat[f];
-    double cv = 0.0;
-    for (int f = 0; f < Dc; ++f) cv += w.w_cond[(size_t)j * Dc + f] * c[f];
-    h[idx] = acc + lv + cv;
+  if (blockIdx.y == 0)
+    for (int idx = threadIdx.x; idx < S * D; idx += blockDim.x)
+      if (!isfinite(x[idx])) atomicCAS(status, 0, 1 + bt.block_index[e]);
+  const int warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int o = warp; o < S * kCols; o += nw) {
+    const int i = o / kCols, j = j0 + o % kCols;
+    if (j >= D) continue;
+    double acc = warp_dot(x + (size_t)i * D, w.w_in + (size_t)j * D, D);
+    const double cv = warp_dot(w.w_cond + (size_t)j * Dc, c, Dc);
+    if ((threadIdx.x & 31) == 0) {
+      const double pos = (double)(bt.block_index[e] * S + i);
+      const double expo = 2.0 * (double)(j >> 1) / (double)D;
+      const double ang = pos / pow(10000.0, expo);
+      acc += (j & 1) ? cos(ang) : sin(ang);
+      double lv = 0.0;
+      for (int f = 0; f < kLevelFeats; ++f) lv += w.w_level[(size_t)j * kLevelFeats + f] * feat[f];
+      h[(size_t)i * D + j] = acc + lv + cv;
+    }
   }
 }
 
 // hn = rmsnorm(h); out = hn W^T for W in {q,k,v} (layer_qkv, 253-261).
-// grid (n_entries, 3): y = 0 -> q workspace, 1 -> K slot, 2 -> V slot.
+// grid (n, 3, D / 32): y = 0 -> q workspace, 1 -> K slot, 2 -> V slot.
 __global__ void toy_qkv(bc_toy_weights w, bc_batch bt, int layer, const double* hidden,
                         double* qbuf, double* arena, int n_slots) {
   extern __shared__ double sm[];
-  const int e = blockIdx.x, which = blockIdx.y;
+  const int e = blockIdx.x, which = blockIdx.y, j0 = blockIdx.z * kCols;
   const int S = bt.block_size, D = w.dim;
-  double* hn = sm;              // S*D
-  double* red = sm + S * D;     // 32
-  const double* h = hidden + (size_t)e * S * D;
-  for (int i = 0; i < S; ++i) {
-    double ss = 0.0;
-    for (int k = threadIdx.x; k < D; k += blockDim.x) ss += h[(size_t)i * D + k] * h[(size_t)i * D + k];
-    const double tot = block_sum(ss, red);
-    const double inv = 1.0 / sqrt(tot / (double)D + kRmsEps);
-    for (int k = threadIdx.x; k < D; k += blockDim.x) hn[i * D + k] = h[(size_t)i * D + k] * inv;
-  }
-  __syncthreads();
+  double* hn = sm;  // S*D
+  rms_rows_smem(hidden + (size_t)e * S * D, hn, S, D);
   const double* W = (which == 0 ? w.w_q : which == 1 ? w.w_k : w.w_v) + (size_t)layer * D * D;
-  double* dst;
-  if (which == 0) {
-    dst = qbuf + (size_t)e * S * D;
-  } else {
-    dst = arena + ((((size_t)layer * n_slots + bt.slot[e]) * 2 + (which - 1)) * S) * D;
-  }
-  for (int idx = threadIdx.x; idx < S * D; idx += blockDim.x) {
-    const int i = idx / D, j = idx % D;
-    const double* wr = W + (size_t)j * D;
-    double acc = 0.0;
-    for (int k = 0; k < D; ++k) acc += hn[i * D + k] * wr[k];
-    dst[idx] = acc;
+  double* dst = which == 0 ? qbuf + (size_t)e * S * D
+                           : arena + ((((size_t)layer * n_slots + bt.slot[e]) * 2 + (which - 1)) * S) * D;
+  const int warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int o = warp; o < S * kCols; o += nw) {
+    const int i = o / kCols, j = j0 + o % kCols;
+    if (j >= D) continue;
+    const double acc = warp_dot(hn + i * D, W + (size_t)j * D, D);
+    if ((threadIdx.x & 31) == 0) dst[(size_t)i * D + j] = acc;
   }
 }
 
-// Per head: softmax(q K^T / sqrt(hd)) V over the visible slots in order,
-// then h += out W_o^T (layer_attend, 264-277).
-__global__ void toy_attend(bc_toy_weights w, bc_batch bt, int layer, double* hidden,
-                           const double* qbuf, const double* arena, int n_slots) {
+// One head of one entry: softmax(q K^T / sqrt(hd)) V over the visible slots
+// in order (layer_attend 264-277, _gather 284-296); the head's output
+// overwrites its own q columns in qbuf (q was copied to smem first).
+// grid (n, H)
+__global__ void toy_attend(bc_toy_weights w, bc_batch bt, int layer, double* qbuf, const double* arena,
+                           int n_slots) {
   extern __shared__ double sm[];
-  const int e = blockIdx.x;
+  const int e = blockIdx.x, hh = blockIdx.y;
   const int S = bt.block_size, D = w.dim, H = w.heads, hd = D / H;
   const int nk = bt.n_vis[e] * S;
-  double* att = sm;              // S*D
-  double* sc = sm + S * D;       // nk
+  double* q = sm;            // S*hd
+  double* sc = sm + S * hd;  // S*nk
   const double scale = 1.0 / sqrt((double)hd);
-  const double* q = qbuf + (size_t)e * S * D;
-  for (int i = 0; i < S; ++i) {
-    for (int hh = 0; hh < H; ++hh) {
-      for (int t = threadIdx.x; t < nk; t += blockDim.x) {
-        const int slot = bt.vis_slot[e][t / S], r = t % S;
-        const double* k = arena + ((((size_t)layer * n_slots + slot) * 2 + 0) * S + r) * D + hh * hd;
-        double acc = 0.0;
-        for (int d = 0; d < hd; ++d) acc += q[(size_t)i * D + hh * hd + d] * k[d];
-        sc[t] = acc * scale;
-      }
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        double m = sc[0];
-        for (int t = 1; t < nk; ++t) m = fmax(m, sc[t]);
-        double z = 0.0;
-        for (int t = 0; t < nk; ++t) {
-          sc[t] = exp(sc[t] - m);
-          z += sc[t];
-        }
-        for (int t = 0; t < nk; ++t) sc[t] /= z;
-      }
-      __syncthreads();
-      for (int d = threadIdx.x; d < hd; d += blockDim.x) {
-        double acc = 0.0;
-        for (int t = 0; t < nk; ++t) {
-          const int slot = bt.vis_slot[e][t / S], r = t % S;
-          acc += sc[t] * arena[((((size_t)layer * n_slots + slot) * 2 + 1) * S + r) * D + hh * hd + d];
-        }
-        att[i * D + hh * hd + d] = acc;
-      }
-      __syncthreads();
-    }
+  double* qg = qbuf + (size_t)e * S * D + hh * hd;
+  for (int idx = threadIdx.x; idx < S * hd; idx += blockDim.x) q[idx] = qg[(size_t)(idx / hd) * D + idx % hd];
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, nw = blockDim.x >> 5, lane = threadIdx.x & 31;
+  for (int o = warp; o < S * nk; o += nw) {
+    const int i = o / nk, t = o % nk;
+    const int slot = bt.vis_slot[e][t / S], r = t % S;
+    const double* k = arena + ((((size_t)layer * n_slots + slot) * 2 + 0) * S + r) * D + hh * hd;
+    const double acc = warp_dot(q + i * hd, k, hd);
+    if (lane == 0) sc[i * nk + t] = acc * scale;
   }
-  double* h = hidden + (size_t)e * S * D;
-  const double* Wo = w.w_o + (size_t)layer * D * D;
-  for (int idx = threadIdx.x; idx < S * D; idx += blockDim.x) {
-    const int i = idx / D, j = idx % D;
+  __syncthreads();
+  for (int i = warp; i < S; i += nw) {  // max-subtracted softmax of row i
+    double* row = sc + i * nk;
+    double m = -INFINITY;
+    for (int t = lane; t < nk; t += 32) m = fmax(m, row[t]);
+    m = warp_max_d(m);
+    double z = 0.0;
+    for (int t = lane; t < nk; t += 32) {
+      const double v = exp(row[t] - m);
+      row[t] = v;
+      z += v;
+    }
+    z = warp_sum_d(z);
+    for (int t = lane; t < nk; t += 32) row[t] /= z;
+  }
+  __syncthreads();
+  for (int idx = threadIdx.x; idx < S * hd; idx += blockDim.x) {
+    const int i = idx / hd, d = idx % hd;
     double acc = 0.0;
-    for (int k = 0; k < D; ++k) acc += att[i * D + k] * Wo[(size_t)j * D + k];
-    h[idx] += acc;
+    for (int t = 0; t < nk; ++t) {
+      const int slot = bt.vis_slot[e][t / S], r = t % S;
+      acc += sc[i * nk + t] * arena[((((size_t)layer * n_slots + slot) * 2 + 1) * S + r) * D + hh * hd + d];
+    }
+    qg[(size_t)i * D + d] = acc;
   }
 }
 
-// x0 = rmsnorm(h) W_head^T (predict_head, 280-281)
+// h += att W_o^T (the tail of layer_attend).  grid (n, D / 32)
+__global__ void toy_oproj(bc_toy_weights w, bc_batch bt, int layer, double* hidden, const double* att) {
+  const int e = blockIdx.x, j0 = blockIdx.y * kCols;
+  const int S = bt.block_size, D = w.dim;
+  const double* a = att + (size_t)e * S * D;
+  double* h = hidden + (size_t)e * S * D;
+  const double* Wo = w.w_o + (size_t)layer * D * D;
+  const int warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int o = warp; o < S * kCols; o += nw) {
+    const int i = o / kCols, j = j0 + o % kCols;
+    if (j >= D) continue;
+    const double acc = warp_dot(a + (size_t)i * D, Wo + (size_t)j * D, D);
+    if ((threadIdx.x & 31) == 0) h[(size_t)i * D + j] += acc;
+  }
+}
+
+// x0 = rmsnorm(h) W_head^T (predict_head, 280-281).  grid (n, D / 32)
 __global__ void toy_head(bc_toy_weights w, bc_batch bt, const double* hidden, ToyPtrs p) {
   extern __shared__ double sm[];
-  const int e = blockIdx.x;
+  const int e = blockIdx.x, j0 = blockIdx.y * kCols;
   const int S = bt.block_size, D = w.dim;
   double* hn = sm;
-  double* red = sm + S * D;
-  const double* h = hidden + (size_t)e * S * D;
-  for (int i = 0; i < S; ++i) {
-    double ss = 0.0;
-    for (int k = threadIdx.x; k < D; k += blockDim.x) ss += h[(size_t)i * D + k] * h[(size_t)i * D + k];
-    const double tot = block_sum(ss, red);
-    const double inv = 1.0 / sqrt(tot / (double)D + kRmsEps);
-    for (int k = threadIdx.x; k < D; k += blockDim.x) hn[i * D + k] = h[(size_t)i * D + k] * inv;
-  }
-  __syncthreads();
+  rms_rows_smem(hidden + (size_t)e * S * D, hn, S, D);
   double* out = p.x0[e];
-  for (int idx = threadIdx.x; idx < S * D; idx += blockDim.x) {
-    const int i = idx / D, j = idx % D;
-    double acc = 0.0;
-    for (int k = 0; k < D; ++k) acc += hn[i * D + k] * w.w_head[(size_t)j * D + k];
-    out[idx] = acc;
+  const int warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int o = warp; o < S * kCols; o += nw) {
+    const int i = o / kCols, j = j0 + o % kCols;
+    if (j >= D) continue;
+    const double acc = warp_dot(hn + i * D, w.w_head + (size_t)j * D, D);
+    if ((threadIdx.x & 31) == 0) out[(size_t)i * D + j] = acc;
   }
 }
 
@@ -273,11 +294,12 @@ extern "C" int bc_toy_forward(const bc_toy_weights* w, const bc_batch* batch,
   cudaStream_t st = (cudaStream_t)stream;
   const int S = b.block_size, D = w->dim, n = b.n_entries;
   double* hidden = workspace;
-  double* qbuf = workspace + (size_t)n * S * D;
-  size_t sm_norm = ((size_t)S * D + 32) * sizeof(double);
+  double* qbuf = workspace + (size_t)n * S * D;   // q, then each head's attention output in place
+  const size_t sm_norm = (size_t)S * D * sizeof(double);
   int max_k = 0;
   for (int e = 0; e < n; ++e) max_k = b.n_vis[e] * S > max_k ? b.n_vis[e] * S : max_k;
-  size_t sm_att = ((size_t)S * D + max_k) * sizeof(double);
+  const int hd = D / w->heads;
+  const size_t sm_att = ((size_t)S * hd + (size_t)S * max_k) * sizeof(double);
   if (sm_norm > 200 * 1024 || sm_att > 200 * 1024)
     return bc_fail(BC_ERR_CONTRACT, "bc_toy_forward: toy dims too large for one CTA");
   static bool attr_done = false;
@@ -287,15 +309,18 @@ extern "C" int bc_toy_forward(const bc_toy_weights* w, const bc_batch* batch,
     BC_CUDA(cudaFuncSetAttribute(toy_head, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     attr_done = true;
   }
-  toy_embed<<<n, kThreads, 0, st>>>(*w, b, p, hidden, status);
+  const int chunks = (D + kCols - 1) / kCols;
+  toy_embed<<<dim3(n, chunks), kThreads, 0, st>>>(*w, b, p, hidden, status);
   BC_LAUNCHED();
   for (int l = 0; l < w->layers; ++l) {
-    toy_qkv<<<dim3(n, 3), kThreads, sm_norm, st>>>(*w, b, l, hidden, qbuf, kv_arena, n_slots);
+    toy_qkv<<<dim3(n, 3, chunks), kThreads, sm_norm, st>>>(*w, b, l, hidden, qbuf, kv_arena, n_slots);
     BC_LAUNCHED();
-    toy_attend<<<n, kThreads, sm_att, st>>>(*w, b, l, hidden, qbuf, kv_arena, n_slots);
+    toy_attend<<<dim3(n, w->heads), kThreads, sm_att, st>>>(*w, b, l, qbuf, kv_arena, n_slots);
+    BC_LAUNCHED();
+    toy_oproj<<<dim3(n, chunks), kThreads, 0, st>>>(*w, b, l, hidden, qbuf);
     BC_LAUNCHED();
   }
-  toy_head<<<n, kThreads, sm_norm, st>>>(*w, b, hidden, p);
+  toy_head<<<dim3(n, chunks), kThreads, sm_norm, st>>>(*w, b, hidden, p);
   BC_LAUNCHED();
   return BC_OK;
 }
