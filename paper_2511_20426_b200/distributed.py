@@ -247,7 +247,7 @@ class _RankWork:
     """Host-side step description of one rank (shared by the real and the
     emulated multi-rank sessions)."""
 
-    def __init__(self, mode, plan, vis_lists, posts, world, rank, slots, slot_epoch, epoch, T):
+    def __init__(self, mode, plan, vis_lists, world, rank, slots, slot_epoch, epoch, T):
         blocks = plan.blocks
         n = len(blocks)
         self.rows = None
@@ -390,7 +390,7 @@ class DistWanSession:
         blocks = plan.blocks
         for b in blocks:
             self.slots.acquire(b)
-        work = _RankWork(self.mode, plan, vis_lists, posts, self.world, self.rank, self.slots,
+        work = _RankWork(self.mode, plan, vis_lists, self.world, self.rank, self.slots,
                          self.slot_epoch, epoch, self.cfg.tokens_per_block)
         if not work.local:
             N.check(N.lib().bc_wan_signal_done(self.state.ctx.handle, epoch, N.stream_ptr()),
@@ -562,7 +562,7 @@ class EmulatedRanks:
         items = []
         init_req, init_dst, eps_req, eps_dst = [], [], [], []
         for r, st in enumerate(self.ranks):
-            work = _RankWork(self.mode, plan, vis_lists, posts, self.world, r, self.slots,
+            work = _RankWork(self.mode, plan, vis_lists, self.world, r, self.slots,
                              self.slot_epoch, epoch, self.cfg.tokens_per_block)
             if not work.local:
                 items.append((st, work, None, None))
