@@ -217,3 +217,28 @@ def test_row_slices_partition_properties():
                 for e, m in enumerate(masks):
                     owners = {r for r, (a, b) in enumerate(sl) if a < (e + 1) * T and b > e * T}
                     assert m == sum(1 << r for r in owners) and m
+
+
+def test_modeled_clock_acceptance_properties(oracle_engine):
+    """Reference acceptance (test_acceptance.py:79-99) through the product
+    engine's modeled clock: B = 40, o = 1, G = 5, uniform pass cost, zero
+    comm/decode -> modeled speedup exactly 200/44 over the sequential
+    rollout; positive comm or decode cost strictly lowers it; the streaming
+    FPS ratio of the 13-block paper config vs sequential is exactly 5."""
+    paper = bc.CascadeConfig(total_frames=39, block_size=3, latent_dim=16, window_blocks=7,
+                             sink_blocks=1, offset=1, workers=1, pass_cost_base=1.0).validate()
+    prompt = "a lighthouse in a storm"
+    cfg = bc.with_fields(paper, total_frames=120, workers=5)
+
+    def speedup(c):
+        seq = bc.run_sequential_reference(c, prompt).trace.total_modeled_time
+        return seq / bc.run_cascade(c, prompt).trace.total_modeled_time
+
+    ideal = 200.0 / 44.0
+    s = speedup(cfg)
+    assert abs(s - ideal) <= 1e-9 and s < 5.0
+    assert speedup(bc.with_fields(cfg, comm_cost_per_frame=1e-4)) < ideal
+    assert speedup(bc.with_fields(cfg, decode_cost=1e-2)) < ideal
+    cascade = bc.run_cascade(bc.with_fields(paper, workers=5), prompt)
+    sequential = bc.run_sequential_reference(paper, prompt)
+    assert bc.streaming_fps(cascade.trace) / bc.streaming_fps(sequential.trace) == 5.0
