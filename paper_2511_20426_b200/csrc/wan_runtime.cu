@@ -61,6 +61,7 @@ struct bc_wan_ctx {
   cudaGraphExec_t graph_exec[BC_MAX_ENTRIES + 1] = {};
   bool width_seen[BC_MAX_ENTRIES + 1] = {};
   cudaStream_t gstream = nullptr;  // capture / launch stream (the caller's may be the legacy stream)
+  bool graphs_broken = false;
   cudaEvent_t gev_in = nullptr, gev_out = nullptr;
   bc_wan_peers peers;
   // BC_KV_PUSH=copy: side-stream push of fresh K/V to the peers' replicas
@@ -656,6 +657,73 @@ int stage_end(bc_wan_ctx* c, cudaStream_t st) {
   return stage_update(c, st);
 }
 
+// Record one step's launches into a CUDA graph on the context's own stream
+// and replay it through the width's executable graph (cudaGraphExecUpdate;
+// re-instantiated when the kernel sequence changed).  The first step of each
+// batch width runs eagerly (per-kernel static setup must not happen inside a
+// capture), as do profiled steps; a failed capture disables graphs for the
+// context and the step runs eagerly.
+template <class F>
+int run_graphed(bc_wan_ctx* c, cudaStream_t& st, int n, F&& run_all) {
+  if (g_graphs < 0) {
+    const char* e = getenv("BC_GRAPHS");
+    g_graphs = e ? atoi(e) != 0 : 1;
+  }
+  // (per-kernel profiling records events between the launches: eager)
+  if (!g_graphs || g_prof || c->graphs_broken || n < 1 || n > BC_MAX_ENTRIES || !c->width_seen[n]) {
+    if (n >= 1 && n <= BC_MAX_ENTRIES) c->width_seen[n] = true;
+    return run_all();
+  }
+  if (!c->gstream) {
+    BC_CUDA(cudaStreamCreateWithFlags(&c->gstream, cudaStreamNonBlocking));
+    BC_CUDA(cudaEventCreateWithFlags(&c->gev_in, cudaEventDisableTiming));
+    BC_CUDA(cudaEventCreateWithFlags(&c->gev_out, cudaEventDisableTiming));
+  }
+  // capture on the context's own stream (the caller's may be the legacy
+  // stream, which cannot be captured); ordered after the caller's earlier
+  // work and before its later work by two events
+  const cudaStream_t caller = st;
+  st = c->gstream;
+  cudaGraph_t graph = nullptr;
+  BC_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+  const int rc = run_all();
+  const cudaError_t ec = cudaStreamEndCapture(st, &graph);
+  st = caller;
+  if (rc || ec != cudaSuccess) {
+    if (graph) cudaGraphDestroy(graph);
+    (void)cudaGetLastError();
+    if (rc) return rc;
+    c->graphs_broken = true;  // something in the step cannot be captured: stay eager
+    return run_all();
+  }
+  cudaGraphExec_t& ex = c->graph_exec[n];
+  if (ex) {
+    cudaGraphExecUpdateResultInfo info;
+    if (cudaGraphExecUpdate(ex, graph, &info) != cudaSuccess) {
+      (void)cudaGetLastError();
+      cudaGraphExecDestroy(ex);
+      ex = nullptr;
+    }
+  }
+  if (!ex) {
+    const cudaError_t ei = cudaGraphInstantiate(&ex, graph, 0);
+    if (ei != cudaSuccess) {
+      cudaGraphDestroy(graph);
+      ex = nullptr;
+      (void)cudaGetLastError();
+      c->graphs_broken = true;
+      return run_all();
+    }
+  }
+  cudaGraphDestroy(graph);
+  BC_CUDA(cudaEventRecord(c->gev_in, caller));
+  BC_CUDA(cudaStreamWaitEvent(c->gstream, c->gev_in, 0));
+  BC_CUDA(cudaGraphLaunch(ex, c->gstream));
+  BC_CUDA(cudaEventRecord(c->gev_out, c->gstream));
+  BC_CUDA(cudaStreamWaitEvent(caller, c->gev_out, 0));
+  return BC_OK;
+}
+
 }  // namespace
 
 extern "C" int bc_wan_step(bc_wan_ctx* c, const bc_batch* batch, const bc_wan_update* upd, int32_t* status,
@@ -676,63 +744,7 @@ extern "C" int bc_wan_step(bc_wan_ctx* c, const bc_batch* batch, const bc_wan_up
     }
     return stage_end(c, st);
   };
-  if (g_graphs < 0) {
-    const char* e = getenv("BC_GRAPHS");
-    g_graphs = e ? atoi(e) != 0 : 1;
-  }
-  const int graphs = g_graphs;
-  // per-kernel profiling needs events between the launches, and the first
-  // step of each batch width initialises per-kernel static state (function
-  // attributes, cluster occupancy of its GEMM tile variants) that must not
-  // happen inside a capture: run those eagerly
-  const int n = batch->n_entries;
-  if (!graphs || g_prof || n < 1 || n > BC_MAX_ENTRIES || !c->width_seen[n]) {
-    if (n >= 1 && n <= BC_MAX_ENTRIES) c->width_seen[n] = true;
-    return run_all();
-  }
-  if (!c->gstream) {
-    BC_CUDA(cudaStreamCreateWithFlags(&c->gstream, cudaStreamNonBlocking));
-    BC_CUDA(cudaEventCreateWithFlags(&c->gev_in, cudaEventDisableTiming));
-    BC_CUDA(cudaEventCreateWithFlags(&c->gev_out, cudaEventDisableTiming));
-  }
-  // capture on the context's own stream; ordered after the caller's stream
-  // work before the launch and before the caller's later work after it
-  const cudaStream_t caller = st;
-  st = c->gstream;
-  cudaGraph_t graph = nullptr;
-  BC_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
-  const int rc = run_all();
-  const cudaError_t ec = cudaStreamEndCapture(st, &graph);
-  if (rc || ec != cudaSuccess) {
-    if (graph) cudaGraphDestroy(graph);
-    (void)cudaGetLastError();
-    if (rc) return rc;
-    return bc_fail(BC_ERR_CUDA, "bc_wan_step: graph capture -> %s", cudaGetErrorString(ec));
-  }
-  cudaGraphExec_t& ex = c->graph_exec[n];
-  if (ex) {
-    cudaGraphExecUpdateResultInfo info;
-    if (cudaGraphExecUpdate(ex, graph, &info) != cudaSuccess) {
-      (void)cudaGetLastError();
-      cudaGraphExecDestroy(ex);
-      ex = nullptr;
-    }
-  }
-  if (!ex) {
-    const cudaError_t ei = cudaGraphInstantiate(&ex, graph, 0);
-    if (ei != cudaSuccess) {
-      cudaGraphDestroy(graph);
-      ex = nullptr;
-      return bc_fail(BC_ERR_CUDA, "bc_wan_step: graph instantiate -> %s", cudaGetErrorString(ei));
-    }
-  }
-  cudaGraphDestroy(graph);
-  BC_CUDA(cudaEventRecord(c->gev_in, caller));
-  BC_CUDA(cudaStreamWaitEvent(st, c->gev_in, 0));
-  BC_CUDA(cudaGraphLaunch(ex, st));
-  BC_CUDA(cudaEventRecord(c->gev_out, st));
-  BC_CUDA(cudaStreamWaitEvent(caller, c->gev_out, 0));
-  return BC_OK;
+  return run_graphed(c, st, batch->n_entries, run_all);
 }
 
 extern "C" int bc_wan_set_peers(bc_wan_ctx* c, const bc_wan_peers* peers) {
@@ -785,6 +797,9 @@ extern "C" int bc_wan_step_dist(bc_wan_ctx* c, const bc_batch* batch, const bc_w
   NvtxScope range(kStageNames[(dist->stage >= -1 && dist->stage <= 4) ? dist->stage + 1 : 0]);
   switch (dist->stage) {
     case -1:
+      // eager: multi-GPU sessions are re-created per run, so per-width graph
+      // instantiation would not amortise (measured slower in the two-process
+      // one-GPU test)
       if (!batch || !upd) return bc_fail(BC_ERR_CONTRACT, "bc_wan_step_dist: null batch");
       RC(stage_begin(c, batch, upd, dist, status, st));
       for (int l = 0; l < c->dims.layers; ++l) {
