@@ -189,6 +189,29 @@ def test_engine_properties_on_oracle(oracle_engine, default_config):
     bc.verify_schedule_consistency(base.trace, cfg)
 
 
+def test_trace_export_import_round_trip(oracle_engine, default_config, tmp_path):
+    """json-lines export is lossless (reference metrics.py:181-205); the CSV
+    carries the instantaneous-FPS series; bad formats and clocks raise."""
+    from paper_2511_20426_b200.metrics import export_trace, import_trace
+    run = bc.run_cascade(bc.with_fields(default_config, total_frames=18), "p")
+    export_trace(run.trace, tmp_path / "t.jsonl")
+    back = import_trace(tmp_path / "t.jsonl")
+    assert [e.to_json() for e in back.events] == [e.to_json() for e in run.trace.events]
+    assert back.total_passes == run.trace.total_passes == 30
+    export_trace(run.trace, tmp_path / "t.csv", format="csv")
+    rows = (tmp_path / "t.csv").read_text().splitlines()
+    series = bc.instantaneous_fps(run.trace)
+    assert rows[0] == "block_index,video_frames,elapsed,fps" and len(rows) == 1 + len(series) == 7
+    assert rows[1].split(",")[0] == str(series[0].block_index) and float(rows[1].split(",")[3]) == series[0].fps
+    assert series.fps_values() == [p.fps for p in series.points]
+    with pytest.raises(bc.InvalidInputError):
+        export_trace(run.trace, tmp_path / "t.x", format="xml")
+    with pytest.raises(bc.InvalidInputError):
+        bc.instantaneous_fps(run.trace, clock="cpu")
+    with pytest.raises(bc.InvalidInputError):
+        bc.streaming_fps(run.trace)  # 6 blocks < 9
+
+
 def test_row_slices_partition_properties():
     """rows partition: contiguous, disjoint, covering slices of the n*T rows,
     balanced to one unit, cut only at query-tile boundaries of an entry, and
