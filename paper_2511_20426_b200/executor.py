@@ -18,40 +18,50 @@ measured one.
 
 from __future__ import annotations
 
+import contextlib
 import time
-from dataclasses import dataclass
+from dataclasses import dataclass, fields
+from typing import NamedTuple
 
 from .errors import ContractViolation, InvalidInputError, IterationError
 
 
+_COST_FROM_CONFIG = (("pass_base", "pass_cost_base"), ("pass_per_frame", "pass_cost_per_frame"),
+                     ("comm_per_frame", "comm_cost_per_frame"), ("decode", "decode_cost"))
+
+
 @dataclass(frozen=True)
 class CostModel:
+    """Modeled clock (reference ``executor.py:27-57``), kept because the trace
+    carries it next to the measured time: a pass costs ``pass_base +
+    pass_per_frame * attended key frames``, a moved KV frame
+    ``comm_per_frame``, an emitted block's decode ``decode``."""
+
     pass_base: float = 1.0
     pass_per_frame: float = 0.0
     comm_per_frame: float = 0.0
     decode: float = 0.0
 
     def __post_init__(self):
-        if min(self.pass_base, self.pass_per_frame, self.comm_per_frame, self.decode) < 0:
-            raise InvalidInputError("cost parameters must be non-negative")
+        negative = [f.name for f in fields(self) if getattr(self, f.name) < 0]
+        if negative:
+            raise InvalidInputError("negative cost parameter(s): " + ", ".join(negative))
+
+    @classmethod
+    def from_config(cls, config) -> "CostModel":
+        return cls(**{mine: getattr(config, theirs) for mine, theirs in _COST_FROM_CONFIG})
 
     def pass_cost(self, visible_frames: int) -> float:
-        return self.pass_base + self.pass_per_frame * visible_frames
+        return self.pass_base + visible_frames * self.pass_per_frame
 
     def comm_cost(self, kv_frames: int) -> float:
-        return self.comm_per_frame * kv_frames
+        return kv_frames * self.comm_per_frame
 
     def decode_cost(self) -> float:
         return self.decode
 
-    @classmethod
-    def from_config(cls, config) -> "CostModel":
-        return cls(pass_base=config.pass_cost_base, pass_per_frame=config.pass_cost_per_frame,
-                   comm_per_frame=config.comm_cost_per_frame, decode=config.decode_cost)
 
-
-@dataclass(frozen=True)
-class EntryTiming:
+class EntryTiming(NamedTuple):
     block_index: int
     pass_index: int
     worker: int
@@ -60,34 +70,30 @@ class EntryTiming:
     wall_seconds: float
 
 
-@dataclass(frozen=True)
-class IterationResult:
+class IterationResult(NamedTuple):
     outputs: list
     timings: list
-    modeled_exec: float
+    modeled_exec: float       # busiest placement, modeled units
     modeled_comm: float
     exchanged_frames: int
-    wall_seconds: float
+    wall_seconds: float       # CUDA-event time of the iteration
 
 
-class WorkerPool:
-    """Placement label set.  In the reference this is a thread pool standing
-    in for GPUs; on B200 the batch runs as one launch sequence per GPU, so
-    the pool only records how many placement slots (GPUs) exist."""
+class WorkerPool(contextlib.AbstractContextManager):
+    """Number of placement slots (GPUs).  The reference's pool is a thread
+    pool standing in for GPUs; here a width-w batch is one launch sequence
+    per GPU, so ``map`` is a plain in-order loop."""
 
     def __init__(self, workers: int):
-        if workers < 1:
-            raise InvalidInputError(f"worker count must be >= 1, got {workers}")
+        if not workers >= 1:
+            raise InvalidInputError(f"need at least one worker (got {workers})")
         self.workers = workers
 
     def map(self, fn, items):
-        return [fn(x) for x in items]
+        return list(map(fn, items))
 
     def close(self):
-        pass
-
-    def __enter__(self):
-        return self
+        return None
 
     def __exit__(self, *exc):
         self.close()
@@ -188,19 +194,21 @@ def execute(plan, entries, visible_kv, mask, weights, pool: WorkerPool,
 # ---------------------------------------------------------------------------
 
 def make_decode_map(pixel_dim: int, latent_dim: int, frames_per_latent: int, seed: int = 0):
+    """Fixed full-column-rank (frames_per_latent * pixel_dim, latent_dim) map,
+    Philox-keyed by ``seed ^ 0xDEC0DE`` (same draws as the reference)."""
     import numpy as np
-    gen = np.random.Generator(np.random.Philox(key=np.uint64(seed ^ 0xDEC0DE)))
-    mat = gen.standard_normal((frames_per_latent * pixel_dim, latent_dim))
-    if np.linalg.matrix_rank(mat) < latent_dim:  # pragma: no cover
-        raise ContractViolation("decode map lost column rank")
+    key = np.uint64(seed ^ 0xDEC0DE)
+    shape = (frames_per_latent * pixel_dim, latent_dim)
+    mat = np.random.Generator(np.random.Philox(key=key)).standard_normal(shape)
+    if np.linalg.matrix_rank(mat) != latent_dim:  # pragma: no cover
+        raise ContractViolation(f"decode map of shape {shape} is rank-deficient")
     return mat
 
 
 def decode_block(latents, decode_map, frames_per_latent: int):
-    s, d = latents.shape
-    if decode_map.ndim != 2 or decode_map.shape[1] != d \
-            or decode_map.shape[0] % frames_per_latent:
+    """(S, D) latents -> (S * frames_per_latent, pixel_dim) frames."""
+    rows, width = decode_map.shape if decode_map.ndim == 2 else (-1, -1)
+    if width != latents.shape[1] or rows < 0 or rows % frames_per_latent:
         raise ContractViolation(
-            f"decode map {decode_map.shape} incompatible with latents {latents.shape}")
-    pix = decode_map.shape[0] // frames_per_latent
-    return (latents @ decode_map.T).reshape(s * frames_per_latent, pix)
+            f"cannot decode latents {latents.shape} with a map of shape {decode_map.shape}")
+    return (latents @ decode_map.T).reshape(latents.shape[0] * frames_per_latent, rows // frames_per_latent)
