@@ -33,150 +33,6 @@ def _readonly(arr) -> np.ndarray:
 
 
 # --------------------------------------------------------------------------
-# Timestep schedule (reference core.py:26-73)
-# --------------------------------------------------------------------------
-
-@dataclass(frozen=True)
-class TimestepSchedule:
-    """Denoise levels (strictly decreasing, in (0, 1000]) followed by one
-    zero-noise cache pass whose KV is what later blocks attend to."""
-
-    denoise_levels: tuple
-    cache_level: float = 0.0
-
-    @property
-    def passes(self) -> int:
-        return len(self.denoise_levels) + 1
-
-    @property
-    def emit_pass(self) -> int:
-        # x0 of the last denoise pass is the block's output
-        return len(self.denoise_levels) - 1
-
-    @property
-    def cache_pass(self) -> int:
-        return len(self.denoise_levels)
-
-    def level_for_pass(self, pass_index: int) -> float:
-        n = len(self.denoise_levels)
-        if 0 <= pass_index < n:
-            return self.denoise_levels[pass_index]
-        if pass_index == n:
-            return self.cache_level
-        raise InvalidInputError(
-            f"pass index {pass_index} out of range for {self.passes} passes")
-
-    def table(self) -> list:
-        """The per-pass level table ``[level(0), ..., level(P-1)]``."""
-        return [self.level_for_pass(p) for p in range(self.passes)]
-
-
-def make_schedule(levels) -> TimestepSchedule:
-    vals = [float(v) for v in levels]
-    if len(vals) == 0:
-        raise InvalidInputError("schedule needs at least one denoise level")
-    if not all(math.isfinite(v) for v in vals):
-        raise InvalidInputError("schedule levels must be finite")
-    if vals[0] > MAX_LEVEL or vals[-1] <= 0.0:
-        raise InvalidInputError(
-            f"denoise levels must lie in (0, {MAX_LEVEL:g}], got {vals}")
-    for hi, lo in zip(vals, vals[1:]):
-        if not lo < hi:
-            raise InvalidInputError(
-                f"denoise levels must be strictly decreasing, got {vals}")
-    return TimestepSchedule(denoise_levels=tuple(vals))
-
-
-# --------------------------------------------------------------------------
-# Latent frames / blocks (reference core.py:76-128)
-# --------------------------------------------------------------------------
-
-@dataclass(frozen=True)
-class LatentFrame:
-    frame_index: int
-    values: np.ndarray
-    noise_level: float
-
-    def __post_init__(self):
-        vals = _readonly(self.values)
-        if not np.isfinite(vals).all():
-            raise InvalidInputError(f"frame {self.frame_index} has non-finite values")
-        object.__setattr__(self, "values", vals)
-
-
-@dataclass(frozen=True)
-class Block:
-    block_index: int
-    frames: tuple
-    pass_index: int = 0
-    conditioning_id: str = ""
-
-    def __post_init__(self):
-        n = len(self.frames)
-        first = self.block_index * n
-        idx = [f.frame_index for f in self.frames]
-        if idx != list(range(first, first + n)):
-            raise InvalidInputError(
-                f"block {self.block_index} frame indices {idx} not contiguous "
-                f"{list(range(first, first + n))}")
-        if len({f.noise_level for f in self.frames}) > 1:
-            raise InvalidInputError(
-                f"block {self.block_index} mixes noise levels "
-                f"{sorted({f.noise_level for f in self.frames})}")
-
-    @property
-    def noise_level(self) -> float:
-        return self.frames[0].noise_level
-
-    @property
-    def latents(self) -> np.ndarray:
-        return np.stack([f.values for f in self.frames])
-
-
-def block_from_latents(block_index, latents, noise_level, conditioning_id="") -> Block:
-    n = latents.shape[0]
-    return Block(block_index,
-                 tuple(LatentFrame(block_index * n + i, latents[i], noise_level)
-                       for i in range(n)),
-                 conditioning_id=conditioning_id)
-
-
-# --------------------------------------------------------------------------
-# Conditioning (reference core.py:131-158)
-# --------------------------------------------------------------------------
-
-@dataclass(frozen=True)
-class Conditioning:
-    """Hash-expanded prompt embedding.  ``id`` is the first 16 hex chars of
-    sha256(prompt); ``digest`` keeps the full hash for derived expansions
-    (the synthetic text-encoder states of the Wan-shaped model)."""
-
-    prompt: str
-    embedding: np.ndarray
-    id: str
-    digest: bytes = field(default=b"", compare=False, repr=False)
-
-    def __post_init__(self):
-        object.__setattr__(self, "embedding", _readonly(self.embedding))
-
-    def key_words(self) -> np.ndarray:
-        return np.frombuffer(self.digest[:16], dtype=np.uint64).copy()
-
-
-def embed_prompt(prompt: str, cond_dim: int) -> Conditioning:
-    if not isinstance(prompt, str) or not prompt:
-        raise InvalidInputError("prompt must be a non-empty string")
-    if cond_dim < 1:
-        raise InvalidInputError(f"conditioning dim must be >= 1, got {cond_dim}")
-    digest = hashlib.sha256(prompt.encode("utf-8")).digest()
-    key = np.frombuffer(digest[:16], dtype=np.uint64)
-    vec = np.random.Generator(np.random.Philox(key=key)).standard_normal(cond_dim)
-    vec = vec / np.linalg.norm(vec)
-    return Conditioning(prompt=prompt, embedding=vec, id=digest.hex()[:16],
-                        digest=digest)
-
-
-# --------------------------------------------------------------------------
 # Counter-keyed noise (reference core.py:161-190)
 # --------------------------------------------------------------------------
 
@@ -226,3 +82,147 @@ class NoiseStream:
 def noise_draw(stream: NoiseStream, block_index: int, pass_index: int,
                frame_index: int) -> np.ndarray:
     return stream.draw(block_index, pass_index, frame_index)
+
+
+# --------------------------------------------------------------------------
+# Conditioning (reference core.py:131-158)
+# --------------------------------------------------------------------------
+
+@dataclass(frozen=True)
+class Conditioning:
+    """Hash-expanded prompt embedding.  ``id`` is the first 16 hex chars of
+    sha256(prompt); ``digest`` keeps the full hash for derived expansions
+    (the synthetic text-encoder states of the Wan-shaped model)."""
+
+    prompt: str
+    embedding: np.ndarray
+    id: str
+    digest: bytes = field(default=b"", compare=False, repr=False)
+
+    def __post_init__(self):
+        object.__setattr__(self, "embedding", _readonly(self.embedding))
+
+    def key_words(self) -> np.ndarray:
+        return np.frombuffer(self.digest[:16], dtype=np.uint64).copy()
+
+
+def embed_prompt(prompt: str, cond_dim: int) -> Conditioning:
+    """sha256(prompt) keys a Philox stream; the embedding is its first
+    ``cond_dim`` normals scaled to unit length."""
+    if not (isinstance(prompt, str) and prompt):
+        raise InvalidInputError("the prompt must be a non-empty str")
+    if cond_dim < 1:
+        raise InvalidInputError(f"cond_dim {cond_dim} < 1")
+    digest = hashlib.sha256(prompt.encode("utf-8")).digest()
+    rng = np.random.Generator(np.random.Philox(key=np.frombuffer(digest[:16], dtype=np.uint64)))
+    raw = rng.standard_normal(cond_dim)
+    return Conditioning(prompt=prompt, embedding=raw / np.linalg.norm(raw), id=digest.hex()[:16], digest=digest)
+
+
+# --------------------------------------------------------------------------
+# Timestep schedule (reference core.py:26-73)
+# --------------------------------------------------------------------------
+
+@dataclass(frozen=True)
+class TimestepSchedule:
+    """Denoise levels (strictly decreasing, in (0, 1000]) followed by one
+    zero-noise cache pass whose KV is what later blocks attend to."""
+
+    denoise_levels: tuple
+    cache_level: float = 0.0
+
+    @property
+    def passes(self) -> int:
+        return len(self.denoise_levels) + 1
+
+    @property
+    def emit_pass(self) -> int:
+        # x0 of the last denoise pass is the block's output
+        return len(self.denoise_levels) - 1
+
+    @property
+    def cache_pass(self) -> int:
+        return len(self.denoise_levels)
+
+    def level_for_pass(self, pass_index: int) -> float:
+        n = len(self.denoise_levels)
+        if 0 <= pass_index < n:
+            return self.denoise_levels[pass_index]
+        if pass_index == n:
+            return self.cache_level
+        raise InvalidInputError(
+            f"pass index {pass_index} out of range for {self.passes} passes")
+
+    def table(self) -> list:
+        """The per-pass level table ``[level(0), ..., level(P-1)]``."""
+        return [self.level_for_pass(p) for p in range(self.passes)]
+
+
+def make_schedule(levels) -> TimestepSchedule:
+    """Validate and freeze a denoise-level list: finite, strictly
+    decreasing, inside (0, MAX_LEVEL]."""
+    vals = tuple(map(float, levels))
+    problems = []
+    if not vals:
+        problems.append("no denoise level given")
+    elif not all(map(math.isfinite, vals)):
+        problems.append("non-finite level")
+    else:
+        if vals[0] > MAX_LEVEL or vals[-1] <= 0.0:
+            problems.append(f"levels outside (0, {MAX_LEVEL:g}]")
+        if any(b >= a for a, b in zip(vals, vals[1:])):
+            problems.append("levels not strictly decreasing")
+    if problems:
+        raise InvalidInputError(f"bad timestep schedule {list(vals)}: " + "; ".join(problems))
+    return TimestepSchedule(denoise_levels=vals)
+
+
+# --------------------------------------------------------------------------
+# Latent frames / blocks (reference core.py:76-128)
+# --------------------------------------------------------------------------
+
+@dataclass(frozen=True)
+class LatentFrame:
+    frame_index: int
+    values: np.ndarray
+    noise_level: float
+
+    def __post_init__(self):
+        vals = _readonly(self.values)
+        if not np.isfinite(vals).all():
+            raise InvalidInputError(f"frame {self.frame_index} has non-finite values")
+        object.__setattr__(self, "values", vals)
+
+
+@dataclass(frozen=True)
+class Block:
+    block_index: int
+    frames: tuple
+    pass_index: int = 0
+    conditioning_id: str = ""
+
+    def __post_init__(self):
+        size = len(self.frames)
+        want = range(self.block_index * size, (self.block_index + 1) * size)
+        got = [fr.frame_index for fr in self.frames]
+        if got != list(want):
+            raise InvalidInputError(f"block {self.block_index}: frame indices {got}, expected {list(want)}")
+        levels = sorted({fr.noise_level for fr in self.frames})
+        if len(levels) > 1:
+            raise InvalidInputError(f"block {self.block_index}: frames at different noise levels {levels}")
+
+    @property
+    def noise_level(self) -> float:
+        return self.frames[0].noise_level
+
+    @property
+    def latents(self) -> np.ndarray:
+        return np.stack([f.values for f in self.frames])
+
+
+def block_from_latents(block_index, latents, noise_level, conditioning_id="") -> Block:
+    n = latents.shape[0]
+    return Block(block_index,
+                 tuple(LatentFrame(block_index * n + i, latents[i], noise_level)
+                       for i in range(n)),
+                 conditioning_id=conditioning_id)
