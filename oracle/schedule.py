@@ -8,26 +8,27 @@ from __future__ import annotations
 
 
 def enumerate_schedule(num_blocks, passes, offset):
-    """Block k runs pass p at iteration k*offset + p (oracles.py:8-21)."""
-    total = (num_blocks - 1) * offset + passes
-    return [[(k, t - k * offset) for k in range(num_blocks) if 0 <= t - k * offset < passes]
-            for t in range(total)]
+    """Block k runs pass p at iteration k*offset + p (oracles.py:8-21):
+    brute force over every (block, pass) pair, bucketed by iteration."""
+    rows = [[] for _ in range((num_blocks - 1) * offset + passes)]
+    for k in range(num_blocks):
+        for p in range(passes):
+            rows[k * offset + p].append((k, p))
+    return rows
 
 
 def replay_pool(inserts, window, sink_blocks):
-    """Keep every inserted block, then drop the smallest non-sink indices
-    while more than ``window`` are held (oracles.py:24-39)."""
-    held, evicted = [], []
+    """Hold every inserted block; while more than ``window`` non-sink blocks
+    are held, evict the smallest (oracles.py:24-39).  Returns (held, evicted)."""
+    held, evicted = set(), []
     for b in inserts:
-        if b not in held:
-            held.append(b)
-        held.sort()
-        regular = [x for x in held if not (sink_blocks and x == 0)]
-        while len(regular) > window:
-            v = regular.pop(0)
-            held.remove(v)
-            evicted.append(v)
-    return held, evicted
+        held.add(b)
+        pinned = {0} & held if sink_blocks else set()
+        regular = sorted(held - pinned)
+        drop = regular[:max(0, len(regular) - window)]
+        held.difference_update(drop)
+        evicted.extend(drop)
+    return sorted(held), evicted
 
 
 def visible_blocks(batch, pool, mode):
