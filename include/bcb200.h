@@ -180,6 +180,7 @@ typedef struct {
  * width) unless disabled; results are identical either way. */
 int bc_wan_step(bc_wan_ctx* ctx, const bc_batch* batch, const bc_wan_update* upd,
                 int32_t* status, void* stream);
+int bc_attention_set_balance(int on); /* 1: balanced persistent self-attention (default, or BC_ATTN_BALANCE env), 0: one CTA per query-tile pair; identical results */
 int bc_wan_set_graphs(int on); /* 1: CUDA graphs (default, or BC_GRAPHS env), 0: eager launches */
 
 /* ---- multi-GPU temporal parallelism (one process per GPU, NVLink P2P) ----

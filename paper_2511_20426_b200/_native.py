@@ -108,6 +108,7 @@ _SIGS = {
                                 C.c_void_p, C.c_int64, C.POINTER(C.c_void_p)]),
     "bc_wan_destroy": (C.c_int, [C.c_void_p]),
     "bc_wan_set_graphs": (C.c_int, [C.c_int]),
+    "bc_attention_set_balance": (C.c_int, [C.c_int]),
     "bc_wan_set_text": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
     "bc_wan_step": (C.c_int, [C.c_void_p, C.POINTER(Batch), C.POINTER(WanUpdate),
                               C.c_void_p, C.c_void_p]),

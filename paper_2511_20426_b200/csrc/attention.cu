@@ -27,6 +27,13 @@
 #include <math.h>
 #include <stdint.h>
 #include <stdlib.h>
+#include <string.h>
+
+#include <algorithm>
+#include <memory>
+#include <queue>
+#include <utility>
+#include <vector>
 
 #include "attention.h"
 #include "bc_common.h"
@@ -182,7 +189,8 @@ struct SoftmaxBars {
 template <int kPoly>
 __device__ __forceinline__ void softmax_tile(const AttnParams& prm, uint32_t tmem_s, uint32_t tmem_o,
                                              uint8_t* sp, SoftmaxBars b, int n_tiles, int tiles_per_slot,
-                                             uint32_t quad, int q_tok0, int e, int head, int tile_x) {
+                                             uint32_t quad, int q_tok0, int e, int head, int tile_x,
+                                             uint32_t jb = 0, uint64_t* o_free = nullptr) {
   const uint32_t row = quad * 32 + lane_id();
   const uint32_t lane_base = (quad * 32) << 16;
   const float c = prm.scale * 1.4426950408889634f;
@@ -191,7 +199,7 @@ __device__ __forceinline__ void softmax_tile(const AttnParams& prm, uint32_t tme
   int t0 = 0;  // first key of tile j within its visible block
   for (int j = 0; j < n_tiles; ++j, t0 = (t0 + kKeys < prm.kv_tokens) ? t0 + kKeys : 0) {
     const int valid = min(kKeys, prm.kv_tokens - t0);
-    mbar_wait(b.s_full, j & 1);
+    mbar_wait(b.s_full, (jb + j) & 1);
     if ((quad) == 0) ATRACE(0 + tile_x * 8, j);
     tc_fence_after();
     float s[128];
@@ -289,7 +297,7 @@ __device__ __forceinline__ void softmax_tile(const AttnParams& prm, uint32_t tme
     if (quad == 0) ATRACE(2 + tile_x * 8, j);
     // PV(j-1) must be complete before O is rescaled or P is overwritten
     if (j > 0) {
-      mbar_wait(b.o_ready, (j - 1) & 1);
+      mbar_wait(b.o_ready, (jb + j - 1) & 1);
       tc_fence_after();
       if (quad == 0) ATRACE(5 + tile_x * 8, j);
       if (__any_sync(0xffffffffu, bump)) {
@@ -324,7 +332,7 @@ __device__ __forceinline__ void softmax_tile(const AttnParams& prm, uint32_t tme
   }
   // epilogue: O / l -> bf16
   if (n_tiles > 0) {
-    mbar_wait(b.o_ready, (n_tiles - 1) & 1);
+    mbar_wait(b.o_ready, (jb + n_tiles - 1) & 1);
     tc_fence_after();
   }
   const int qtok = q_tok0 + (int)row;
@@ -349,6 +357,10 @@ __device__ __forceinline__ void softmax_tile(const AttnParams& prm, uint32_t tme
         dst[q] = v;
       }
     }
+  }
+  if (o_free) {  // O is read out: the next work item's first PV may overwrite it
+    tc_fence_before();
+    mbar_arrive(o_free);
   }
 }
 
@@ -537,6 +549,211 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 1) tmem_dealloc<512>(tmem);
 }
 
+// Balanced persistent variant (single-GPU steps): one CTA per SM runs a
+// host-built list of work items, each either a pair of 128-row query tiles
+// (ping-pong, as attn_kernel) or a single tile.  With one item per CTA the
+// last of ~7.7 waves leaves a third of the SMs idle; here the host assigns
+// whole pairs round by round and splits the last round's pairs into single
+// tiles when its cost model says that ends earlier (longest-processing-time
+// first, build_sched).  The next item's Q load and first QK^T overlap the
+// previous item's epilogue, which is what helps the 4-key-tile text
+// cross-attention most (164 -> 138 ms per run).  Per-row arithmetic and key
+// order are those of attn_kernel: results are bit-identical.
+// Barrier phases run on across items: per-tile barriers of tile x count
+// the tiles x has processed, q_full / q_empty count items, o_free[x] (the
+// epilogue of x has read O_x) counts the items x took part in.
+template <int kPoly>
+__global__ void __launch_bounds__(kThreads, 1)
+    attn_sched_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_kv,
+                      AttnParams prm, const __grid_constant__ AttnSched sch) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Smem::bars);
+  uint64_t* q_full = bars + 0;
+  uint64_t* ring_full = bars + 1;   // [3]
+  uint64_t* ring_empty = bars + 4;  // [3]
+  uint64_t* s_full = bars + 7;      // [2]
+  uint64_t* s_empty = bars + 9;     // [2]
+  uint64_t* p_full = bars + 11;     // [2]
+  uint64_t* o_ready = bars + 13;    // [2]
+  uint64_t* q_empty = bars + 15;
+  uint64_t* o_free = bars + 16;     // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 20);
+
+  const int it0 = sch.start[blockIdx.x], it1 = sch.start[blockIdx.x + 1];
+  if (it0 >= it1) return;
+  const int tiles_per_slot = (prm.kv_tokens + kKeys - 1) / kKeys;
+  const uint32_t warp = warp_id();
+  struct Item {
+    int e, head, q0, n_q, n_tiles;
+  };
+  auto item = [&](int i) {
+    const uint32_t w = sch.items[i];
+    Item r;
+    r.e = (int)(w & 0xffu);
+    r.head = (int)((w >> 8) & 0xffu);
+    r.q0 = prm.q_lo[r.e] + (int)((w >> 16) & 0x7fffu) * kRows;
+    r.n_q = (w >> 31) ? 2 : 1;
+    r.n_tiles = prm.n_vis[r.e] * tiles_per_slot;
+    return r;
+  };
+
+  if (warp == 0 && lane_id() == 0) {
+    tma_prefetch(&map_q);
+    tma_prefetch(&map_kv);
+    mbar_init(q_full, 1);
+    mbar_init(q_empty, 1);
+    for (int i = 0; i < kRing; ++i) {
+      mbar_init(&ring_full[i], 1);
+      mbar_init(&ring_empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&s_full[i], 1);
+      mbar_init(&s_empty[i], 128);
+      mbar_init(&p_full[i], 128);
+      mbar_init(&o_ready[i], 1);
+      mbar_init(&o_free[i], 128);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp < 4) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegsCtl));
+  if (warp == 0) {
+    if (lane_id() == 0) {
+      uint32_t g = 0;  // ring items issued so far
+      for (int i = it0; i < it1; ++i) {
+        const Item w = item(i);
+        if (i > it0) mbar_wait(q_empty, (i - it0 - 1) & 1);  // previous item's QK^T are done with Q
+        const int qrow = prm.q_row[w.e] + (w.q0 - prm.q_lo[w.e]);
+        mbar_arrive_expect_tx(q_full, w.n_q * kTile);
+        for (int x = 0; x < w.n_q; ++x) {
+          tma_load_3d(smem + Smem::qa + x * kTile, &map_q, q_full, 0, w.head, qrow + x * kRows);
+          tma_load_3d(smem + Smem::qa + x * kTile + kHalf, &map_q, q_full, 64, w.head, qrow + x * kRows);
+        }
+        for (int r = 0; r < 2 * w.n_tiles; ++r, ++g) {
+          int j, is_v;
+          ring_item(r, w.n_tiles, j, is_v);
+          const int slot = g % kRing;
+          const uint32_t ph = (g / kRing) & 1;
+          const int kv_slot = prm.vis_slot[w.e][j / tiles_per_slot];
+          const int t0 = (j % tiles_per_slot) * kKeys;
+          const int mat = prm.mat_base + kv_slot * prm.mat_stride + (is_v ? prm.v_offset : 0);
+          mbar_wait(&ring_empty[slot], ph ^ 1);
+          mbar_arrive_expect_tx(&ring_full[slot], kTile);
+          uint8_t* dst = smem + Smem::ring + slot * kTile;
+          tma_load_4d(dst, &map_kv, &ring_full[slot], 0, w.head, t0, mat);
+          tma_load_4d(dst + kHalf, &map_kv, &ring_full[slot], 64, w.head, t0, mat);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    constexpr uint32_t idesc_qk = idesc_bf16(kRows, kKeys);
+    constexpr uint32_t idesc_pv = idesc_bf16(kRows, kHd, 0, 1);  // B (= V) MN-major
+    const uint32_t sq[2] = {smem_u32(smem + Smem::qa), smem_u32(smem + Smem::qb)};
+    const uint32_t sp[2] = {smem_u32(smem + Smem::pa), smem_u32(smem + Smem::pb)};
+    auto slot_of = [&](uint32_t g) { return smem_u32(smem + Smem::ring + (g % kRing) * kTile); };
+    auto ring_wait = [&](uint32_t g) { mbar_wait(&ring_full[g % kRing], (g / kRing) & 1); };
+    auto commit = [&](uint64_t* bar) {
+      if (elect_one()) mma_commit(bar);
+      __syncwarp();
+    };
+    auto issue_qk = [&](int x, uint32_t g) {
+      if (elect_one()) {
+        const uint32_t sk = slot_of(g);
+#pragma unroll
+        for (int k = 0; k < kHd / 16; ++k) {
+          const uint32_t off = (k >> 2) * kHalf + (k & 3) * 32;
+          mma_bf16_ss(tmem + x * 128, desc_sw128(sq[x] + off, 16, 1024), desc_sw128(sk + off, 16, 1024), idesc_qk,
+                      k != 0);
+        }
+        mma_commit(&s_full[x]);
+      }
+      __syncwarp();
+    };
+    auto issue_pv = [&](int x, uint32_t g, bool first) {
+      if (elect_one()) {
+        const uint32_t sv = slot_of(g);
+#pragma unroll
+        for (int k = 0; k < kKeys / 16; ++k) {
+          const uint32_t aoff = (k >> 2) * kHalf + (k & 3) * 32;
+          mma_bf16_ss(tmem + 256 + x * 128, desc_sw128(sp[x] + aoff, 16, 1024),
+                      desc_sw128(sv + k * 2048, kHalf, 1024), idesc_pv, !(first && k == 0));
+        }
+        mma_commit(&o_ready[x]);
+      }
+      __syncwarp();
+    };
+    uint32_t ib = 0;                // ring items consumed before this item
+    uint32_t tb[2] = {0u, 0u};      // tiles processed by x before this item
+    uint32_t nb[2] = {0u, 0u};      // items x took part in before this item
+    for (int i = it0; i < it1; ++i) {
+      const Item w = item(i);
+      const int n = w.n_tiles;
+      mbar_wait(q_full, (i - it0) & 1);
+      if (n > 0) {
+        ring_wait(ib + kpos(0));
+        tc_fence_after();
+        for (int x = 0; x < w.n_q; ++x) {
+          if (tb[x] > 0) mbar_wait(&s_empty[x], (tb[x] - 1) & 1);  // x read its previous S
+          tc_fence_after();
+          issue_qk(x, ib + kpos(0));
+        }
+        commit(&ring_empty[(ib + kpos(0)) % kRing]);
+        if (n == 1) commit(q_empty);
+        for (int j = 0; j < n; ++j) {
+          const bool next = j + 1 < n;
+          for (int x = 0; x < w.n_q; ++x) {
+            if (next) {
+              mbar_wait(&s_empty[x], (tb[x] + j) & 1);
+              if (x == 0) ring_wait(ib + kpos(j + 1));
+              tc_fence_after();
+              issue_qk(x, ib + kpos(j + 1));
+              if (x == w.n_q - 1) {
+                commit(&ring_empty[(ib + kpos(j + 1)) % kRing]);
+                if (j + 1 == n - 1) commit(q_empty);  // the item's last QK^T
+              }
+            }
+            mbar_wait(&p_full[x], (tb[x] + j) & 1);
+            if (x == 0) ring_wait(ib + vpos(j, n));
+            if (j == 0 && nb[x] > 0) mbar_wait(&o_free[x], (nb[x] - 1) & 1);  // previous O read out
+            tc_fence_after();
+            issue_pv(x, ib + vpos(j, n), j == 0);
+          }
+          commit(&ring_empty[(ib + vpos(j, n)) % kRing]);
+        }
+      } else {
+        commit(q_empty);
+      }
+      ib += 2 * n;
+      for (int x = 0; x < w.n_q; ++x) {
+        tb[x] += n;
+        nb[x] += 1;
+      }
+    }
+  } else if (warp >= 4) {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegsSoftmax));
+    const int x = (warp >= 8) ? 1 : 0;
+    SoftmaxBars b{&s_full[x], &s_empty[x], &p_full[x], &o_ready[x]};
+    uint32_t tb = 0;
+    for (int i = it0; i < it1; ++i) {
+      const Item w = item(i);
+      if (x >= w.n_q) continue;
+      softmax_tile<kPoly>(prm, tmem + x * 128, tmem + 256 + x * 128, smem + (x ? Smem::pb : Smem::pa), b,
+                          w.n_tiles, tiles_per_slot, warp & 3, w.q0 + x * kRows, w.e, w.head, x, tb, &o_free[x]);
+      tb += w.n_tiles;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 1) tmem_dealloc<512>(tmem);
+}
+
 PFN_cuTensorMapEncodeTiled_v12000 encoder() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   if (!fn) {
@@ -559,6 +776,147 @@ int encode(CUtensorMap* map, const void* base, int rank, const cuuint64_t* dims,
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return bc_fail(BC_ERR_CUDA, "attention tensor map encode failed (%d)", (int)r);
   return BC_OK;
+}
+
+}  // namespace
+
+int g_attn_balance = -1;  // -1: BC_ATTN_BALANCE env (default on)
+
+namespace {
+
+int sm_count_attn() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+// Cost of a single-tile item per key tile, in units of one tile of a pair
+// (a pair costs 2).  Without a ping-pong partner the tile's softmax latency
+// (MUFU-bound: 128 exps per thread) is exposed every key tile: measured
+// ~0.9 of a whole pair.  BC_ATTN_SINGLE_COST (percent) overrides.
+double single_cost() {
+  static double c = -1.0;
+  if (c < 0.0) {
+    const char* e = getenv("BC_ATTN_SINGLE_COST");
+    c = e ? atof(e) / 100.0 : 1.8;
+  }
+  return c;
+}
+
+struct SchedKey {
+  int n_entries, heads, kv_tokens, ctas;
+  int n_vis[BC_MAX_ENTRIES], q_lo[BC_MAX_ENTRIES], q_hi[BC_MAX_ENTRIES];
+  bool operator==(const SchedKey& o) const { return memcmp(this, &o, sizeof(SchedKey)) == 0; }
+};
+
+struct WorkItem {
+  uint32_t code;
+  double cost;
+  int order;  // tie-break: head-major, so concurrently running items share K/V in L2
+};
+
+// Longest-processing-time-first onto `bins` CTAs; returns the makespan and
+// appends each bin's items (in assignment order) to lists[bin].
+double lpt(std::vector<WorkItem>& items, std::vector<double>& load, std::vector<std::vector<uint32_t>>& lists) {
+  std::stable_sort(items.begin(), items.end(), [](const WorkItem& a, const WorkItem& b) {
+    return a.cost != b.cost ? a.cost > b.cost : a.order < b.order;
+  });
+  using Bin = std::pair<double, int>;
+  std::priority_queue<Bin, std::vector<Bin>, std::greater<Bin>> heap;
+  for (int b = 0; b < (int)load.size(); ++b) heap.push({load[b], b});
+  for (const WorkItem& w : items) {
+    Bin bin = heap.top();
+    heap.pop();
+    load[bin.second] += w.cost;
+    lists[bin.second].push_back(w.code);
+    heap.push({load[bin.second], bin.second});
+  }
+  return *std::max_element(load.begin(), load.end());
+}
+
+// Build the balanced work list (nullptr: does not fit, use attn_kernel).
+// Whole pairs are placed first; the pairs that would form the last,
+// partial round are either kept whole or split into two single-tile items,
+// whichever the cost model says finishes earlier.
+const AttnSched* build_sched(const AttnArgs& a, const AttnParams& p, int* n_ctas) {
+  static std::vector<std::pair<SchedKey, std::unique_ptr<AttnSched>>> cache;
+  SchedKey key;
+  memset(&key, 0, sizeof(key));
+  key.n_entries = a.n_entries;
+  key.heads = a.heads;
+  key.kv_tokens = a.kv_tokens;
+  key.ctas = std::min(sm_count_attn(), kSchedCtas);
+  for (int e = 0; e < a.n_entries; ++e) {
+    key.n_vis[e] = p.n_vis[e];
+    key.q_lo[e] = p.q_lo[e];
+    key.q_hi[e] = p.q_hi[e];
+  }
+  for (auto& c : cache)
+    if (c.first == key) {
+      *n_ctas = key.ctas;
+      return c.second.get();
+    }
+  const int tps = (a.kv_tokens + kKeys - 1) / kKeys;
+  std::vector<WorkItem> pairs, singles;
+  for (int h = 0; h < a.heads; ++h)
+    for (int e = 0; e < a.n_entries; ++e) {
+      const int rows = p.q_hi[e] - p.q_lo[e];
+      const int nq = (rows + kRows - 1) / kRows;
+      const double nt = (double)p.n_vis[e] * tps;
+      for (int t = 0; t < nq; t += 2) {
+        const uint32_t code = (uint32_t)e | ((uint32_t)h << 8) | ((uint32_t)t << 16);
+        const int order = (h * BC_MAX_ENTRIES + e) * 4096 + t;
+        if (t + 1 < nq)
+          pairs.push_back({code | 0x80000000u, 2.0 * nt, order});
+        else
+          singles.push_back({code, single_cost() * nt, order});
+      }
+    }
+  const int G = key.ctas;
+  if (pairs.size() + 2 * singles.size() + pairs.size() > (size_t)kSchedItems || a.heads > 255 ||
+      a.n_entries > 255)
+    return nullptr;
+  std::stable_sort(pairs.begin(), pairs.end(), [](const WorkItem& x, const WorkItem& y) {
+    return x.cost != y.cost ? x.cost > y.cost : x.order < y.order;
+  });
+  const size_t whole = pairs.size() - pairs.size() % G;  // complete rounds of pairs
+  auto plan = [&](bool split, std::vector<std::vector<uint32_t>>& lists) {
+    std::vector<double> load(G, 0.0);
+    lists.assign(G, {});
+    std::vector<WorkItem> first(pairs.begin(), pairs.begin() + (split ? whole : pairs.size()));
+    lpt(first, load, lists);
+    std::vector<WorkItem> rest = singles;
+    if (split)
+      for (size_t i = whole; i < pairs.size(); ++i) {
+        const WorkItem& w = pairs[i];
+        const double c = single_cost() * w.cost / 2.0;
+        const uint32_t base = w.code & 0x7fffffffu;
+        rest.push_back({base, c, w.order});
+        rest.push_back({base + (1u << 16), c, w.order + 1});  // the pair's second tile
+      }
+    return lpt(rest, load, lists);
+  };
+  std::vector<std::vector<uint32_t>> keep, split;
+  const double m_keep = plan(false, keep);
+  const double m_split = plan(true, split);
+  const auto& lists = (m_split < m_keep) ? split : keep;
+  auto sched = std::make_unique<AttnSched>();
+  memset(sched.get(), 0, sizeof(AttnSched));
+  int n = 0;
+  for (int b = 0; b < G; ++b) {
+    sched->start[b] = (uint16_t)n;
+    for (uint32_t c : lists[b]) sched->items[n++] = c;
+  }
+  sched->start[G] = (uint16_t)n;
+  cache.emplace_back(key, std::move(sched));
+  if (cache.size() > 64) cache.erase(cache.begin());
+  *n_ctas = G;
+  return cache.back().second.get();
 }
 
 }  // namespace
@@ -645,6 +1003,25 @@ int attention_run(const AttnArgs& a, cudaStream_t st) {
       return bc_fail(BC_ERR_CUDA, "attention kernel built with %d registers, expected %d", fa.numRegs, kRegsLaunch);
   }
   if (max_pairs == 0) return BC_OK;  // no query rows in this slice
+  if (g_attn_balance < 0) {
+    const char* env = getenv("BC_ATTN_BALANCE");
+    g_attn_balance = env ? atoi(env) : 1;
+  }
+  if (a.balance && g_attn_balance && !a.flags && poly == 0) {
+    static bool attr = false;
+    if (!attr) {
+      BC_CUDA(cudaFuncSetAttribute(attn_sched_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   Smem::total + 1024));
+      attr = true;
+    }
+    int ctas = 0;
+    const AttnSched* sch = build_sched(a, p, &ctas);
+    if (sch) {
+      attn_sched_kernel<0><<<ctas, kThreads, Smem::total + 1024, st>>>(mq, mkv, p, *sch);
+      BC_LAUNCHED();
+      return BC_OK;
+    }
+  }
   dim3 grid(max_pairs, a.n_entries, a.heads);
   switch (poly) {
     case 2: attn_kernel<2><<<grid, kThreads, Smem::total + 1024, st>>>(mq, mkv, p); break;
@@ -658,6 +1035,13 @@ int attention_run(const AttnArgs& a, cudaStream_t st) {
 }
 
 }  // namespace bc
+
+// Select the attention kernel: 1 = balanced persistent work lists (default),
+// 0 = one CTA per (query-tile pair, entry, head).  Results are identical.
+extern "C" int bc_attention_set_balance(int on) {
+  bc::g_attn_balance = on ? 1 : 0;
+  return BC_OK;
+}
 
 // Self-attention over KV-arena slots.  k_arena points at layer 0 of an
 // arena laid out [L][n_slots][2][T][heads*128]; slot_stride_elems is the
@@ -690,5 +1074,6 @@ extern "C" int bc_attention_paged(const void* q, const void* k_arena, const void
   a.n_mats = (max_slot + 1) * a.mat_stride + a.v_offset;
   a.scale = 1.0f / sqrtf(128.0f);
   a.out = out;
+  a.balance = 1;
   return bc::attention_run(a, (cudaStream_t)stream);
 }

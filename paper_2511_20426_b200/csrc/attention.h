@@ -33,6 +33,17 @@ struct AttnParams {
   int q_lo[BC_MAX_ENTRIES], q_hi[BC_MAX_ENTRIES], q_row[BC_MAX_ENTRIES];
 };
 
+// Work list of the balanced persistent kernel (by value, next to
+// AttnParams: the two stay under the 32 KB kernel-parameter limit).  CTA c
+// runs items [start[c], start[c+1]); item = e | head << 8 | tile << 16 |
+// pair << 31 (tile = first 128-row query tile within the entry's range).
+constexpr int kSchedCtas = 256;
+constexpr int kSchedItems = 6144;
+struct AttnSched {
+  uint16_t start[kSchedCtas + 1];
+  uint32_t items[kSchedItems];
+};
+
 struct AttnArgs {
   const void* q;        // bf16 [n_entries*q_tokens][heads*128]
   const void* kv_base;  // bf16 matrices [n_mats][kv_tokens][heads*128]
@@ -51,6 +62,8 @@ struct AttnArgs {
   // ranged = 1: q_lo / q_hi / q_row as in AttnParams, q / out have q_rows rows
   int ranged, q_rows;
   int q_lo[BC_MAX_ENTRIES], q_hi[BC_MAX_ENTRIES], q_row[BC_MAX_ENTRIES];
+  // 1: balanced persistent kernel (single-GPU launches without peer flags)
+  int balance;
 };
 
 int attention_run(const AttnArgs& a, cudaStream_t st);

@@ -75,3 +75,30 @@ def test_attention_deterministic_across_batching():
     full = run_attention(q, arena, vis, T, T, heads)
     solo = run_attention(q[T:2 * T].contiguous(), arena, [vis[1]], T, T, heads)
     assert torch.equal(full[T:2 * T], solo)
+
+
+@pytest.mark.parametrize("q_tokens,kv_tokens,heads,vis", [
+    (4680, 256, 12, [[0, 1, 2], [0, 1, 2, 3], [4, 5, 0, 1, 2]]),   # ~5 items per CTA, mixed lengths
+    (4680, 200, 12, [[0, 1, 2, 3, 4]] * 5),                       # bidirectional-like, ragged key tiles
+    (1000, 384, 7, [[3], [0, 1]]),                                # fewer items than SMs
+    (300, 128, 40, [[0, 1]] * 4),                                 # 14B head count
+])
+def test_attention_balanced_kernel_bit_identical(q_tokens, kv_tokens, heads, vis):
+    """The persistent balanced kernel (work lists of query-tile pairs and
+    single tiles, barrier phases carried across items) gives bit-identical
+    results to one CTA per (pair, entry, head), and matches torch."""
+    g = torch.Generator(device="cuda").manual_seed(q_tokens + heads)
+    arena = torch.randn(6, 2, kv_tokens, heads * 128, device="cuda", generator=g).bfloat16()
+    q = (torch.randn(len(vis) * q_tokens, heads * 128, device="cuda", generator=g) * 2).bfloat16()
+    try:
+        N.lib().bc_attention_set_balance(0)
+        grid = run_attention(q, arena, vis, q_tokens, kv_tokens, heads)
+        N.lib().bc_attention_set_balance(1)
+        bal = run_attention(q, arena, vis, q_tokens, kv_tokens, heads)
+        again = run_attention(q, arena, vis, q_tokens, kv_tokens, heads)   # cached work list
+    finally:
+        N.lib().bc_attention_set_balance(1)
+    assert torch.equal(grid, bal) and torch.equal(bal, again)
+    if heads <= 12:
+        want = reference(q, arena, vis, q_tokens, heads)
+        assert float((bal.float() - want).norm() / want.norm()) < 8e-3
