@@ -549,7 +549,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 1) tmem_dealloc<512>(tmem);
 }
 
-// Balanced persistent variant (single-GPU steps): one CTA per SM runs a
+// Balanced persistent variant: one CTA per SM runs a
 // host-built list of work items, each either a pair of 128-row query tiles
 // (ping-pong, as attn_kernel) or a single tile.  With one item per CTA the
 // last of ~7.7 waves leaves a third of the SMs idle; here the host assigns
@@ -643,6 +643,15 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int kv_slot = prm.vis_slot[w.e][j / tiles_per_slot];
           const int t0 = (j % tiles_per_slot) * kKeys;
           const int mat = prm.mat_base + kv_slot * prm.mat_stride + (is_v ? prm.v_offset : 0);
+          if (!is_v && prm.flags && (j % tiles_per_slot) == 0) {
+            const uint32_t need = prm.need[w.e][j / tiles_per_slot];
+            if (need) {  // K/V rows of this block come from peer GPUs: wait for each producer
+              const uint32_t ep = need >> 8;
+              const uint32_t* f = prm.flags + (size_t)(prm.flag_base + kv_slot) * prm.n_ranks;
+              for (uint32_t m = need & 0xffu; m; m &= m - 1) spin_until_geq(f + (__ffs(m) - 1), ep, 256);
+              asm volatile("fence.proxy.async.global;" ::: "memory");
+            }
+          }
           mbar_wait(&ring_empty[slot], ph ^ 1);
           mbar_arrive_expect_tx(&ring_full[slot], kTile);
           uint8_t* dst = smem + Smem::ring + slot * kTile;
@@ -1007,7 +1016,7 @@ int attention_run(const AttnArgs& a, cudaStream_t st) {
     const char* env = getenv("BC_ATTN_BALANCE");
     g_attn_balance = env ? atoi(env) : 1;
   }
-  if (a.balance && g_attn_balance && !a.flags && poly == 0) {
+  if (a.balance && g_attn_balance && poly == 0) {
     static bool attr = false;
     if (!attr) {
       BC_CUDA(cudaFuncSetAttribute(attn_sched_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,

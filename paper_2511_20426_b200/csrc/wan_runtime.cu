@@ -440,7 +440,7 @@ int stage_begin(bc_wan_ctx* c, const bc_batch* batch, const bc_wan_update* upd, 
   sa.n_ranks = multi ? c->peers.n_ranks : 1;
   sa.ranged = 1;
   sa.q_rows = R;
-  sa.balance = 1;  // persistent balanced kernel unless peer flags are waited on
+  sa.balance = 1;  // persistent balanced kernel (peer-flag waits per item)
   for (int e = 0; e < n; ++e) {
     sa.n_vis[e] = batch->n_vis[e];
     for (int v = 0; v < batch->n_vis[e]; ++v) {
