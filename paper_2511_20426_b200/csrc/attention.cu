@@ -31,6 +31,7 @@
 
 #include <algorithm>
 #include <memory>
+#include <mutex>
 #include <queue>
 #include <utility>
 #include <vector>
@@ -852,8 +853,10 @@ double lpt(std::vector<WorkItem>& items, std::vector<double>& load, std::vector<
 // Whole pairs are placed first; the pairs that would form the last,
 // partial round are either kept whole or split into two single-tile items,
 // whichever the cost model says finishes earlier.
-const AttnSched* build_sched(const AttnArgs& a, const AttnParams& p, int* n_ctas) {
-  static std::vector<std::pair<SchedKey, std::unique_ptr<AttnSched>>> cache;
+std::shared_ptr<const AttnSched> build_sched(const AttnArgs& a, const AttnParams& p, int* n_ctas) {
+  static std::vector<std::pair<SchedKey, std::shared_ptr<const AttnSched>>> cache;
+  static std::mutex mu;  // contexts may step from several host threads
+  std::lock_guard<std::mutex> lock(mu);
   SchedKey key;
   memset(&key, 0, sizeof(key));
   key.n_entries = a.n_entries;
@@ -868,7 +871,7 @@ const AttnSched* build_sched(const AttnArgs& a, const AttnParams& p, int* n_ctas
   for (auto& c : cache)
     if (c.first == key) {
       *n_ctas = key.ctas;
-      return c.second.get();
+      return c.second;
     }
   const int tps = (a.kv_tokens + kKeys - 1) / kKeys;
   std::vector<WorkItem> pairs, singles;
@@ -922,10 +925,10 @@ const AttnSched* build_sched(const AttnArgs& a, const AttnParams& p, int* n_ctas
     for (uint32_t c : lists[b]) sched->items[n++] = c;
   }
   sched->start[G] = (uint16_t)n;
-  cache.emplace_back(key, std::move(sched));
-  if (cache.size() > 64) cache.erase(cache.begin());
+  if (cache.size() >= 64) cache.erase(cache.begin());  // callers hold their own reference
+  cache.emplace_back(key, std::shared_ptr<const AttnSched>(std::move(sched)));
   *n_ctas = G;
-  return cache.back().second.get();
+  return cache.back().second;
 }
 
 }  // namespace
@@ -1024,7 +1027,7 @@ int attention_run(const AttnArgs& a, cudaStream_t st) {
       attr = true;
     }
     int ctas = 0;
-    const AttnSched* sch = build_sched(a, p, &ctas);
+    const std::shared_ptr<const AttnSched> sch = build_sched(a, p, &ctas);
     if (sch) {
       attn_sched_kernel<0><<<ctas, kThreads, Smem::total + 1024, st>>>(mq, mkv, p, *sch);
       BC_LAUNCHED();
