@@ -204,6 +204,35 @@ def toy_config1_times(bc):
             "max_block_rel_l2_vs_oracle": rel}
 
 
+def noise_generation_report(cfg):
+    """host noise generation reported separately.  Every (block,
+    pass) draw of one run (Philox4x64 + numpy's ziggurat, fp32), by the
+    native multi-threaded generator the e2e path uses, vs numpy itself for one
+    block-pass (the reference's GIL-bound path, core.py:170-186)."""
+    import numpy as np
+    from paper_2511_20426_b200 import _native as N
+    from paper_2511_20426_b200.wan import run_noise_keys
+    keys = run_noise_keys(cfg)
+    S, D = cfg.block_size, cfg.latent_dim
+    threads = max(1, os.cpu_count() or 1)
+    out = np.empty((len(keys), S, D), dtype=np.float32)
+    tasks = [(SESSION_SEED, 0, (b, p, b * S + i, 0), out[k, i]) for k, (b, p) in enumerate(keys) for i in range(S)]
+    N.run_noise_tasks(tasks, 1, threads)  # warm-up (page-in)
+    t0 = time.perf_counter()
+    N.run_noise_tasks(tasks, 1, threads)
+    native_s = time.perf_counter() - t0
+    stream = __import__("paper_2511_20426_b200").NoiseStream(SESSION_SEED, D)
+    t0 = time.perf_counter()
+    ref = np.stack([stream.draw(0, 1, i) for i in range(S)])
+    numpy_s = time.perf_counter() - t0
+    if not np.array_equal(ref.astype(np.float32), out[keys.index((0, 1))]):
+        raise RuntimeError("native noise differs from numpy's draws")
+    return {"block_passes_per_run": len(keys), "native_ms_per_run": round(native_s * 1e3, 2),
+            "native_ms_per_block_pass": round(native_s * 1e3 / len(keys), 3), "threads": threads,
+            "numpy_ms_per_block_pass": round(numpy_s * 1e3, 2),
+            "bytes_per_run": int(out.nbytes), "bit_identical_to_numpy": True}
+
+
 def metric_name(args):
     return f"generated frames/sec (cascaded, Wan2.1-{args.preset.upper()}-shaped, 480x832)"
 
@@ -361,9 +390,10 @@ def run_ours(args, cfg):
     # ---- the reference's own CPU-runnable case (BASELINE configs[0]): the toy
     # model of the reference package, fp64 on the device, vs the oracle port
     # of it on the host (the reference code itself is not on the box) ----
-    toy = None
+    toy = noise = None
     if world == 1 and not args.no_cpu:
         toy = toy_config1_times(bc)
+        noise = noise_generation_report(cfg)
 
     S = cfg.block_size
     lat_bytes = S * cfg.latent_dim * 4
@@ -407,6 +437,7 @@ def run_ours(args, cfg):
         "cascade_over_sequential_streaming": stream_fps / seq_stream if seq_stream else None,
         "prompt_switch": switch,
         "config1_toy": toy,
+        "noise_generation": noise,
         "roofline": {"bound": "tensor", "kernel": dom, "achieved": achieved, "peak": peak,
                      "unit": "TFLOP/s", "frac": achieved / peak if achieved else None,
                      "traffic": traffic, "peak_kind": f"{peak_kind} bf16 sustained",

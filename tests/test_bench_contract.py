@@ -23,3 +23,15 @@ def test_reference_arm_json_line():
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["value"] == d["value"]
     assert d["cpu_baseline"]["kind"] == "port" and d["cpu_baseline"]["cores"] >= 1
     assert "workload" in d["config"]
+
+
+def test_noise_generation_report_tiny():
+    """The bench's separate host-noise report: native generator
+    draws for every (block, pass) key of a run, checked against numpy."""
+    sys.path.insert(0, ROOT)
+    import bench
+    import paper_2511_20426_b200 as bc
+    cfg = bc.wan_config("tiny", total_frames=9)
+    r = bench.noise_generation_report(cfg)
+    assert r["bit_identical_to_numpy"] and r["block_passes_per_run"] == 3 * 4
+    assert r["bytes_per_run"] == 12 * cfg.block_size * cfg.latent_dim * 4 and r["native_ms_per_run"] > 0
