@@ -189,11 +189,13 @@ def toy_config1_times(bc):
         return statistics.median(ts) * 1e3
     gpu = bc.run_cascade(cfg1, "a red cube", weights=w)
     gpu_ms = med(lambda: bc.run_cascade(cfg1, "a red cube", weights=w), 5)
+    gpu_seq_ms = med(lambda: bc.run_sequential_reference(cfg1, "a red cube", weights=w), 5)
     orig = engine._runtime_for
     engine._runtime_for = oracle_runtime
     try:
         cpu = bc.run_cascade(cfg1, "a red cube", weights=w)
-        cpu_ms = med(lambda: bc.run_cascade(cfg1, "a red cube", weights=w), 3)
+        cpu_ms = med(lambda: bc.run_cascade(cfg1, "a red cube", weights=w), 5)
+        cpu_seq_ms = med(lambda: bc.run_sequential_reference(cfg1, "a red cube", weights=w), 5)
     finally:
         engine._runtime_for = orig
     import numpy as np
@@ -201,6 +203,8 @@ def toy_config1_times(bc):
               for b in cpu.outputs)
     return {"workload": "reference toy model, L4 D256 2x128 heads, 6 blocks (18 frames), o=1, bidirectional",
             "device_fp64_ms_per_run": round(gpu_ms, 2), "oracle_cpu_ms_per_run": round(cpu_ms, 2),
+            "sequential_device_fp64_ms_per_run": round(gpu_seq_ms, 2),
+            "sequential_oracle_cpu_ms_per_run": round(cpu_seq_ms, 2), "median_of": 5,
             "max_block_rel_l2_vs_oracle": rel}
 
 
