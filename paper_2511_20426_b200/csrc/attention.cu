@@ -585,17 +585,32 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (it0 >= it1) return;
   const int tiles_per_slot = (prm.kv_tokens + kKeys - 1) / kKeys;
   const uint32_t warp = warp_id();
+  // tile x of an item: query rows from token qx of entry ex (x = 0, 1); K/V
+  // from entry e0's visible list (a cross-entry pair's entries have equal
+  // lists).  Scalars, not arrays: a runtime-indexed array would live in
+  // local memory.
   struct Item {
-    int e, head, q0, n_q, n_tiles;
+    int e0, e1, q0, q1, head, n_q, n_tiles;
+    __device__ int e(int x) const { return x ? e1 : e0; }
+    __device__ int q(int x) const { return x ? q1 : q0; }
   };
   auto item = [&](int i) {
     const uint32_t w = sch.items[i];
     Item r;
-    r.e = (int)(w & 0xffu);
+    r.e0 = (int)(w & 0xffu);
     r.head = (int)((w >> 8) & 0xffu);
-    r.q0 = prm.q_lo[r.e] + (int)((w >> 16) & 0x7fffu) * kRows;
-    r.n_q = (w >> 31) ? 2 : 1;
-    r.n_tiles = prm.n_vis[r.e] * tiles_per_slot;
+    if (w & kItemCross) {  // the last query tiles of two entries
+      r.e1 = (int)((w >> 16) & 0xffu);
+      r.q0 = prm.q_lo[r.e0] + ((prm.q_hi[r.e0] - prm.q_lo[r.e0] - 1) / kRows) * kRows;
+      r.q1 = prm.q_lo[r.e1] + ((prm.q_hi[r.e1] - prm.q_lo[r.e1] - 1) / kRows) * kRows;
+      r.n_q = 2;
+    } else {
+      r.e1 = r.e0;
+      r.q0 = prm.q_lo[r.e0] + (int)((w >> 16) & 0x3fffu) * kRows;
+      r.q1 = r.q0 + kRows;
+      r.n_q = (w & kItemPair) ? 2 : 1;
+    }
+    r.n_tiles = prm.n_vis[r.e0] * tiles_per_slot;
     return r;
   };
 
@@ -630,22 +645,22 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int i = it0; i < it1; ++i) {
         const Item w = item(i);
         if (i > it0) mbar_wait(q_empty, (i - it0 - 1) & 1);  // previous item's QK^T are done with Q
-        const int qrow = prm.q_row[w.e] + (w.q0 - prm.q_lo[w.e]);
         mbar_arrive_expect_tx(q_full, w.n_q * kTile);
         for (int x = 0; x < w.n_q; ++x) {
-          tma_load_3d(smem + Smem::qa + x * kTile, &map_q, q_full, 0, w.head, qrow + x * kRows);
-          tma_load_3d(smem + Smem::qa + x * kTile + kHalf, &map_q, q_full, 64, w.head, qrow + x * kRows);
+          const int qrow = prm.q_row[w.e(x)] + (w.q(x) - prm.q_lo[w.e(x)]);
+          tma_load_3d(smem + Smem::qa + x * kTile, &map_q, q_full, 0, w.head, qrow);
+          tma_load_3d(smem + Smem::qa + x * kTile + kHalf, &map_q, q_full, 64, w.head, qrow);
         }
         for (int r = 0; r < 2 * w.n_tiles; ++r, ++g) {
           int j, is_v;
           ring_item(r, w.n_tiles, j, is_v);
           const int slot = g % kRing;
           const uint32_t ph = (g / kRing) & 1;
-          const int kv_slot = prm.vis_slot[w.e][j / tiles_per_slot];
+          const int kv_slot = prm.vis_slot[w.e0][j / tiles_per_slot];
           const int t0 = (j % tiles_per_slot) * kKeys;
           const int mat = prm.mat_base + kv_slot * prm.mat_stride + (is_v ? prm.v_offset : 0);
           if (!is_v && prm.flags && (j % tiles_per_slot) == 0) {
-            const uint32_t need = prm.need[w.e][j / tiles_per_slot];
+            const uint32_t need = prm.need[w.e0][j / tiles_per_slot];
             if (need) {  // K/V rows of this block come from peer GPUs: wait for each producer
               const uint32_t ep = need >> 8;
               const uint32_t* f = prm.flags + (size_t)(prm.flag_base + kv_slot) * prm.n_ranks;
@@ -754,7 +769,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const Item w = item(i);
       if (x >= w.n_q) continue;
       softmax_tile<kPoly>(prm, tmem + x * 128, tmem + 256 + x * 128, smem + (x ? Smem::pb : Smem::pa), b,
-                          w.n_tiles, tiles_per_slot, warp & 3, w.q0 + x * kRows, w.e, w.head, x, tb, &o_free[x]);
+                          w.n_tiles, tiles_per_slot, warp & 3, w.q(x), w.e(x), w.head, x, tb, &o_free[x]);
       tb += w.n_tiles;
     }
   }
@@ -821,6 +836,7 @@ double single_cost() {
 struct SchedKey {
   int n_entries, heads, kv_tokens, ctas;
   int n_vis[BC_MAX_ENTRIES], q_lo[BC_MAX_ENTRIES], q_hi[BC_MAX_ENTRIES];
+  int group[BC_MAX_ENTRIES];  // first entry with an identical visible list
   bool operator==(const SchedKey& o) const { return memcmp(this, &o, sizeof(SchedKey)) == 0; }
 };
 
@@ -867,6 +883,13 @@ std::shared_ptr<const AttnSched> build_sched(const AttnArgs& a, const AttnParams
     key.n_vis[e] = p.n_vis[e];
     key.q_lo[e] = p.q_lo[e];
     key.q_hi[e] = p.q_hi[e];
+    key.group[e] = e;
+    for (int f = 0; f < e; ++f)
+      if (p.n_vis[f] == p.n_vis[e] && !memcmp(p.vis_slot[f], p.vis_slot[e], sizeof(int) * p.n_vis[e]) &&
+          !memcmp(p.need[f], p.need[e], sizeof(uint32_t) * p.n_vis[e])) {
+        key.group[e] = f;
+        break;
+      }
   }
   for (auto& c : cache)
     if (c.first == key) {
@@ -874,21 +897,36 @@ std::shared_ptr<const AttnSched> build_sched(const AttnArgs& a, const AttnParams
       return c.second;
     }
   const int tps = (a.kv_tokens + kKeys - 1) / kKeys;
+  auto n_qtiles = [&](int e) { return (p.q_hi[e] - p.q_lo[e] + kRows - 1) / kRows; };
   std::vector<WorkItem> pairs, singles;
-  for (int h = 0; h < a.heads; ++h)
+  for (int h = 0; h < a.heads; ++h) {
+    int open_single[BC_MAX_ENTRIES];  // per visible-list group: an unpaired last tile (-1: none)
+    for (int e = 0; e < a.n_entries; ++e) open_single[e] = -1;
     for (int e = 0; e < a.n_entries; ++e) {
-      const int rows = p.q_hi[e] - p.q_lo[e];
-      const int nq = (rows + kRows - 1) / kRows;
+      const int nq = n_qtiles(e);
       const double nt = (double)p.n_vis[e] * tps;
       for (int t = 0; t < nq; t += 2) {
         const uint32_t code = (uint32_t)e | ((uint32_t)h << 8) | ((uint32_t)t << 16);
         const int order = (h * BC_MAX_ENTRIES + e) * 4096 + t;
-        if (t + 1 < nq)
-          pairs.push_back({code | 0x80000000u, 2.0 * nt, order});
-        else
-          singles.push_back({code, single_cost() * nt, order});
+        if (t + 1 < nq) {
+          pairs.push_back({code | kItemPair, 2.0 * nt, order});
+        } else if (open_single[key.group[e]] >= 0) {  // pair it with an earlier entry's last tile
+          const int f = open_single[key.group[e]];
+          open_single[key.group[e]] = -1;
+          pairs.push_back({(uint32_t)f | ((uint32_t)h << 8) | ((uint32_t)e << 16) | kItemCross, 2.0 * nt, order});
+        } else {
+          open_single[key.group[e]] = e;
+        }
       }
     }
+    for (int e = 0; e < a.n_entries; ++e)  // last tiles left without a partner
+      if (open_single[e] >= 0) {
+        const int f = open_single[e];
+        const uint32_t t = (uint32_t)(n_qtiles(f) - 1);
+        singles.push_back({(uint32_t)f | ((uint32_t)h << 8) | (t << 16), single_cost() * p.n_vis[f] * tps,
+                           (h * BC_MAX_ENTRIES + f) * 4096 + (int)t});
+      }
+  }
   const int G = key.ctas;
   if (pairs.size() + 2 * singles.size() + pairs.size() > (size_t)kSchedItems || a.heads > 255 ||
       a.n_entries > 255)
@@ -907,9 +945,16 @@ std::shared_ptr<const AttnSched> build_sched(const AttnArgs& a, const AttnParams
       for (size_t i = whole; i < pairs.size(); ++i) {
         const WorkItem& w = pairs[i];
         const double c = single_cost() * w.cost / 2.0;
-        const uint32_t base = w.code & 0x7fffffffu;
-        rest.push_back({base, c, w.order});
-        rest.push_back({base + (1u << 16), c, w.order + 1});  // the pair's second tile
+        const uint32_t h8 = w.code & 0xff00u;
+        if (w.code & kItemCross) {  // the two entries' last tiles
+          const uint32_t e1 = w.code & 0xffu, e2 = (w.code >> 16) & 0xffu;
+          rest.push_back({e1 | h8 | ((uint32_t)(n_qtiles((int)e1) - 1) << 16), c, w.order});
+          rest.push_back({e2 | h8 | ((uint32_t)(n_qtiles((int)e2) - 1) << 16), c, w.order + 1});
+        } else {
+          const uint32_t base = w.code & ~kItemPair;
+          rest.push_back({base, c, w.order});
+          rest.push_back({base + (1u << 16), c, w.order + 1});  // the pair's second tile
+        }
       }
     return lpt(rest, load, lists);
   };

@@ -35,8 +35,15 @@ struct AttnParams {
 
 // Work list of the balanced persistent kernel (by value, next to
 // AttnParams: the two stay under the 32 KB kernel-parameter limit).  CTA c
-// runs items [start[c], start[c+1]); item = e | head << 8 | tile << 16 |
-// pair << 31 (tile = first 128-row query tile within the entry's range).
+// runs items [start[c], start[c+1]).  Item words:
+//   e | head << 8 | tile << 16 [| kItemPair]: query tile `tile` (128 rows,
+//     counted from the entry's q_lo) of entry e, and with kItemPair also
+//     tile + 1 as the ping-pong partner;
+//   e | head << 8 | e2 << 16 | kItemCross: the last query tiles of entries e
+//     and e2, which attend to identical visible lists (bidirectional mode),
+//     as one ping-pong pair.
+constexpr uint32_t kItemPair = 0x80000000u;
+constexpr uint32_t kItemCross = 0x40000000u;
 constexpr int kSchedCtas = 256;
 constexpr int kSchedItems = 6144;
 struct AttnSched {

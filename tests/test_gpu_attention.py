@@ -82,6 +82,7 @@ def test_attention_deterministic_across_batching():
     (4680, 200, 12, [[0, 1, 2, 3, 4]] * 5),                       # bidirectional-like, ragged key tiles
     (1000, 384, 7, [[3], [0, 1]]),                                # fewer items than SMs
     (300, 128, 40, [[0, 1]] * 4),                                 # 14B head count
+    (328, 256, 12, [[0, 1], [2, 3], [0, 1], [2, 3], [0, 1]]),    # last tiles paired across equal lists
 ])
 def test_attention_balanced_kernel_bit_identical(q_tokens, kv_tokens, heads, vis):
     """The persistent balanced kernel (work lists of query-tile pairs and
