@@ -180,6 +180,33 @@ __global__ void ln_rows_kernel(const float* __restrict__ X, __nv_bfloat16* __res
     const int idx = li + 32 * WPR * i;
     v[i] = (active && idx * 4 < d) ? x4[idx] : make_float4(0.f, 0.f, 0.f, 0.f);
   }
+  // Warp-per-row blocks whose 8 rows share one entry stage that entry's
+  // scale / shift sums in shared memory once (all 256 threads, while the row
+  // loads above are in flight), instead of every warp fetching 2 x d floats
+  // from L2 after its reductions.  Same sums, same arithmetic.
+  __shared__ float4 coef[2][WPR == 1 ? 32 * VPL : 1];
+  const int first = blockIdx.x * (8 / WPR);
+  const int last = min(rows - 1, first + 8 / WPR - 1);
+  const int e_blk = (a.row0 + first) / rows_per_entry;
+  const bool staged = WPR == 1 && e_blk == (a.row0 + last) / rows_per_entry;
+  if (staged) {
+    const float4* bsc = reinterpret_cast<const float4*>(a.base_scale);
+    const float4* bsh = reinterpret_cast<const float4*>(a.base_shift);
+    const float4* esc = a.mode == 0 ? reinterpret_cast<const float4*>(a.pe_scale + (size_t)e_blk * a.entry_stride) : nullptr;
+    const float4* esh = a.mode == 0 ? reinterpret_cast<const float4*>(a.pe_shift + (size_t)e_blk * a.entry_stride) : nullptr;
+    for (int idx = threadIdx.x; idx * 4 < d; idx += blockDim.x) {
+      float4 sc = bsc ? __ldg(bsc + idx) : make_float4(0.f, 0.f, 0.f, 0.f);
+      float4 sh = bsh ? __ldg(bsh + idx) : make_float4(0.f, 0.f, 0.f, 0.f);
+      if (esc) {
+        const float4 sc2 = __ldg(esc + idx), sh2 = __ldg(esh + idx);
+        sc = make_float4(sc.x + sc2.x, sc.y + sc2.y, sc.z + sc2.z, sc.w + sc2.w);
+        sh = make_float4(sh.x + sh2.x, sh.y + sh2.y, sh.z + sh2.z, sh.w + sh2.w);
+      }
+      coef[0][idx] = sc;
+      coef[1][idx] = sh;
+    }
+  }
+  if (WPR == 1) __syncthreads();
   float2 s2 = make_float2(0.f, 0.f);
 #pragma unroll
   for (int i = 0; i < VPL; ++i) {
@@ -214,12 +241,18 @@ __global__ void ln_rows_kernel(const float* __restrict__ X, __nv_bfloat16* __res
     const int idx = li + 32 * WPR * i;
     if (idx * 4 >= d) continue;
     // scale = [1 +] base_scale [+ pe_scale[e]], shift = base_shift [+ pe_shift[e]]
-    float4 sc = bsc ? __ldg(bsc + idx) : make_float4(0.f, 0.f, 0.f, 0.f);
-    float4 sh = bsh ? __ldg(bsh + idx) : make_float4(0.f, 0.f, 0.f, 0.f);
-    if (esc) {
-      const float4 sc2 = __ldg(esc + idx), sh2 = __ldg(esh + idx);
-      sc = make_float4(sc.x + sc2.x, sc.y + sc2.y, sc.z + sc2.z, sc.w + sc2.w);
-      sh = make_float4(sh.x + sh2.x, sh.y + sh2.y, sh.z + sh2.z, sh.w + sh2.w);
+    float4 sc, sh;
+    if (staged) {
+      sc = coef[0][idx];
+      sh = coef[1][idx];
+    } else {
+      sc = bsc ? __ldg(bsc + idx) : make_float4(0.f, 0.f, 0.f, 0.f);
+      sh = bsh ? __ldg(bsh + idx) : make_float4(0.f, 0.f, 0.f, 0.f);
+      if (esc) {
+        const float4 sc2 = __ldg(esc + idx), sh2 = __ldg(esh + idx);
+        sc = make_float4(sc.x + sc2.x, sc.y + sc2.y, sc.z + sc2.z, sc.w + sc2.w);
+        sh = make_float4(sh.x + sh2.x, sh.y + sh2.y, sh.z + sh2.z, sh.w + sh2.w);
+      }
     }
     const float2 A01 = __fmul2_rn(__fadd2_rn(make_float2(sc.x, sc.y), make_float2(one, one)), r2);
     const float2 A23 = __fmul2_rn(__fadd2_rn(make_float2(sc.z, sc.w), make_float2(one, one)), r2);
