@@ -429,6 +429,13 @@ __global__ void rms_rows_kernel(__nv_bfloat16* x, int rows, int d, int ld, const
       }
     }
   }
+  // warp-per-row blocks stage the weight vector in shared memory once (as
+  // ln_rows_kernel does its coefficients) while the row loads are in flight
+  __shared__ float4 wsm[WPR == 1 ? 2 * 32 * VPL : 1];
+  if (WPR == 1) {
+    for (int i = threadIdx.x; i * 4 < d; i += blockDim.x) wsm[i] = __ldg(reinterpret_cast<const float4*>(w) + i);
+    __syncthreads();
+  }
   const float inv = rsqrtf(row_reduce<WPR>(ss, red, slot, wir) / d + kEps);
   if (!active) return;
   uint4* d4 = reinterpret_cast<uint4*>(out + (size_t)row * ld_out);
@@ -438,8 +445,8 @@ __global__ void rms_rows_kernel(__nv_bfloat16* x, int rows, int d, int ld, const
     if (idx * 8 >= d) continue;
     // weights as two 16-byte loads (8 scalar loads strided 32 B apart across
     // the warp made this kernel L1-wavefront bound)
-    const float4 w0 = __ldg(reinterpret_cast<const float4*>(w) + 2 * idx);
-    const float4 w1 = __ldg(reinterpret_cast<const float4*>(w) + 2 * idx + 1);
+    const float4 w0 = WPR == 1 ? wsm[2 * idx] : __ldg(reinterpret_cast<const float4*>(w) + 2 * idx);
+    const float4 w1 = WPR == 1 ? wsm[2 * idx + 1] : __ldg(reinterpret_cast<const float4*>(w) + 2 * idx + 1);
     const float wv[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
     uint4 u;
     __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(&u);
