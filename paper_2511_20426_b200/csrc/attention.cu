@@ -341,20 +341,23 @@ __device__ __forceinline__ void softmax_tile(const AttnParams& prm, uint32_t tme
   const float inv = (l_sum > 0.0f) ? 1.0f / l_sum : 0.0f;
   __nv_bfloat16* out = static_cast<__nv_bfloat16*>(prm.out) +
                        ((size_t)(prm.q_row[e] + qtok - prm.q_lo[e]) * prm.heads + head) * kHd;
+  // all four 32-column loads of O in flight, one wait (the epilogue sits
+  // between a work item's last PV and the next item's first P)
+  uint32_t r[4][32];
 #pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    uint32_t r[32];
-    tmem_ld32(tmem_o + lane_base + k * 32, r);
-    tmem_ld_wait();
-    if (live) {
+  for (int k = 0; k < 4; ++k) tmem_ld32(tmem_o + lane_base + k * 32, r[k]);
+  tmem_ld_wait();
+  if (live) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
       uint4* dst = reinterpret_cast<uint4*>(out + k * 32);
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         uint4 v;
-        v.x = pack_bf16(__uint_as_float(r[8 * q + 0]) * inv, __uint_as_float(r[8 * q + 1]) * inv);
-        v.y = pack_bf16(__uint_as_float(r[8 * q + 2]) * inv, __uint_as_float(r[8 * q + 3]) * inv);
-        v.z = pack_bf16(__uint_as_float(r[8 * q + 4]) * inv, __uint_as_float(r[8 * q + 5]) * inv);
-        v.w = pack_bf16(__uint_as_float(r[8 * q + 6]) * inv, __uint_as_float(r[8 * q + 7]) * inv);
+        v.x = pack_bf16(__uint_as_float(r[k][8 * q + 0]) * inv, __uint_as_float(r[k][8 * q + 1]) * inv);
+        v.y = pack_bf16(__uint_as_float(r[k][8 * q + 2]) * inv, __uint_as_float(r[k][8 * q + 3]) * inv);
+        v.z = pack_bf16(__uint_as_float(r[k][8 * q + 4]) * inv, __uint_as_float(r[k][8 * q + 5]) * inv);
+        v.w = pack_bf16(__uint_as_float(r[k][8 * q + 6]) * inv, __uint_as_float(r[k][8 * q + 7]) * inv);
         dst[q] = v;
       }
     }
