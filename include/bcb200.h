@@ -180,6 +180,14 @@ typedef struct {
  * width) unless disabled; results are identical either way. */
 int bc_wan_step(bc_wan_ctx* ctx, const bc_batch* batch, const bc_wan_update* upd,
                 int32_t* status, void* stream);
+/* Work list the balanced kernel would run for bc_attention_paged's arguments
+   (host logic, no device work): item words into items[0..ret), per-CTA
+   offsets into start[0..*n_ctas]; item = e | head << 8 | tile << 16, plus bit
+   31 = pair of tiles (tile, tile + 1), or bit 30 = cross-entry pair (the last
+   tiles of entries e and bits 16-23).  Returns -1 if the grid kernel would
+   run instead. */
+int bc_attention_plan(const bc_batch* batch, int32_t q_per_entry, int32_t kv_tokens, int32_t heads,
+                      uint32_t* items, int32_t items_cap, uint16_t* start, int32_t* n_ctas);
 int bc_attention_set_balance(int on); /* 1: balanced persistent self-attention (default, or BC_ATTN_BALANCE env), 0: one CTA per query-tile pair; identical results */
 int bc_wan_set_graphs(int on); /* 1: CUDA graphs (default, or BC_GRAPHS env), 0: eager launches */
 

@@ -109,6 +109,8 @@ _SIGS = {
     "bc_wan_destroy": (C.c_int, [C.c_void_p]),
     "bc_wan_set_graphs": (C.c_int, [C.c_int]),
     "bc_attention_set_balance": (C.c_int, [C.c_int]),
+    "bc_attention_plan": (C.c_int, [C.POINTER(Batch), C.c_int32, C.c_int32, C.c_int32, C.c_void_p, C.c_int32,
+                                    C.c_void_p, C.POINTER(C.c_int32)]),
     "bc_wan_set_text": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
     "bc_wan_step": (C.c_int, [C.c_void_p, C.POINTER(Batch), C.POINTER(WanUpdate),
                               C.c_void_p, C.c_void_p]),

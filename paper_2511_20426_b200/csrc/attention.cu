@@ -1103,6 +1103,39 @@ extern "C" int bc_attention_set_balance(int on) {
   return BC_OK;
 }
 
+// Host-side view of the balanced kernel's work list for a paged launch (the
+// same arguments as bc_attention_paged, every entry's full q_per_entry rows):
+// items[] / start[] as the kernel receives them (attention.h, AttnSched).
+// Returns the item count, or -1 when the launch would use the grid kernel.
+// Host logic only (no device work), so the CPU tests check coverage and
+// pairing rules with it.
+extern "C" int bc_attention_plan(const bc_batch* batch, int32_t q_per_entry, int32_t kv_tokens, int32_t heads,
+                                 uint32_t* items, int32_t items_cap, uint16_t* start, int32_t* n_ctas) {
+  if (!batch || !items || !start || !n_ctas) return bc_fail(BC_ERR_CONTRACT, "attention plan: null argument");
+  if (batch->n_entries < 1 || batch->n_entries > BC_MAX_ENTRIES)
+    return bc_fail(BC_ERR_CONTRACT, "attention plan: bad entry count");
+  bc::AttnArgs a{};
+  bc::AttnParams p{};
+  a.n_entries = batch->n_entries;
+  a.heads = heads;
+  a.kv_tokens = kv_tokens;
+  for (int e = 0; e < a.n_entries; ++e) {
+    p.n_vis[e] = batch->n_vis[e];
+    for (int v = 0; v < batch->n_vis[e]; ++v) p.vis_slot[e][v] = batch->vis_slot[e][v];
+    p.q_lo[e] = 0;
+    p.q_hi[e] = q_per_entry;
+  }
+  int ctas = 0;
+  const std::shared_ptr<const bc::AttnSched> sch = bc::build_sched(a, p, &ctas);
+  if (!sch) return -1;
+  const int n = sch->start[ctas];
+  if (n > items_cap) return bc_fail(BC_ERR_CONTRACT, "attention plan: %d items exceed the buffer", n);
+  for (int i = 0; i < n; ++i) items[i] = sch->items[i];
+  for (int c = 0; c <= ctas; ++c) start[c] = sch->start[c];
+  *n_ctas = ctas;
+  return n;
+}
+
 // Self-attention over KV-arena slots.  k_arena points at layer 0 of an
 // arena laid out [L][n_slots][2][T][heads*128]; slot_stride_elems is the
 // distance between consecutive slots' K matrices in elements.

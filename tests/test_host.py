@@ -265,3 +265,60 @@ def test_modeled_clock_acceptance_properties(oracle_engine):
     cascade = bc.run_cascade(bc.with_fields(paper, workers=5), prompt)
     sequential = bc.run_sequential_reference(paper, prompt)
     assert bc.streaming_fps(cascade.trace) / bc.streaming_fps(sequential.trace) == 5.0
+
+
+def _attention_plan(vis, q_tokens, kv_tokens, heads):
+    import ctypes as C
+    from paper_2511_20426_b200 import _native as N
+    b = N.make_batch(3, list(range(len(vis))), [0.0] * len(vis), [0] * len(vis), vis)
+    items = np.zeros(6144, np.uint32)
+    start = np.zeros(257, np.uint16)
+    n_ctas = C.c_int32()
+    n = N.lib().bc_attention_plan(C.byref(b), q_tokens, kv_tokens, heads, items.ctypes.data, 6144,
+                                  start.ctypes.data, C.byref(n_ctas))
+    assert n >= 0
+    return items[:n], start[:n_ctas.value + 1]
+
+
+@pytest.mark.parametrize("vis,q_tokens,heads", [
+    ([list(range(13))] * 5, 4680, 12),                    # steady state, bidirectional
+    ([[0, 1, 2], [0, 1, 2, 3], [0, 1, 2, 3, 4]], 4680, 12),  # causal-like: no equal lists
+    ([[0, 1], [2, 3], [0, 1], [2, 3], [0, 1]], 328, 12),     # two groups of equal lists
+    ([[0, 1]] * 2, 4680, 40),                              # 14B head count
+    ([[0]], 300, 2),                                       # fewer items than CTAs
+])
+def test_attention_work_list_covers_every_tile_once(vis, q_tokens, heads):
+    """The balanced attention kernel's work list (built on the host,
+    csrc/attention.cu build_sched): every (entry, head, 128-row query tile)
+    appears in exactly one item; pairs are consecutive tiles of one entry;
+    cross-entry pairs join the last tiles of two entries with identical
+    visible lists; the CTAs' modelled loads differ by at most one item."""
+    items, start = _attention_plan(vis, q_tokens, 256, heads)
+    nq = -(-q_tokens // 128)
+    seen = {}
+    load = []
+    for c in range(len(start) - 1):
+        cost = 0.0
+        for w in items[start[c]:start[c + 1]]:
+            w = int(w)
+            e, h = w & 0xff, (w >> 8) & 0xff
+            if w & 0x40000000:
+                e2 = (w >> 16) & 0xff
+                assert e2 != e and vis[e] == vis[e2]
+                tiles = [(e, h, nq - 1), (e2, h, nq - 1)]
+                cost += 2 * len(vis[e])
+            elif w & 0x80000000:
+                t = (w >> 16) & 0x3fff
+                assert t + 1 < nq
+                tiles = [(e, h, t), (e, h, t + 1)]
+                cost += 2 * len(vis[e])
+            else:
+                tiles = [(e, h, (w >> 16) & 0x3fff)]
+                cost += 1.8 * len(vis[e])
+            for k in tiles:
+                assert k not in seen, k
+                seen[k] = True
+        load.append(cost)
+    assert len(seen) == len(vis) * heads * nq
+    biggest = 2 * max(len(v) for v in vis)
+    assert max(load) - min(load) <= biggest + 1e-9
