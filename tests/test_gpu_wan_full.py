@@ -1,0 +1,219 @@
+"""Full-depth Wan parity at the configurations the bench runs.
+
+The product (bf16 tcgen05 kernels) against the torch fp32 restatement of
+the oracle (oracle/wan_torch.py, pinned to oracle/wan.py by
+tests/test_oracle_wan_torch.py), TF32 off, on the same GPU:
+
+* teacher-forced steady-state iteration of the 13-block Wan2.1-1.3B bench
+  run (30 layers, 480x832, 512x4096 text, width 5 over an 8-block pool:
+  iteration 12, blocks 8..12 at levels 0/250/500/750/1000, block 12 seeing
+  39 latent frames): the product runs the free-running session up to that
+  iteration; there the SAME inputs (its latents, its pool KV slots, its text
+  states) go through both sides; x0 rel-L2 <= 2e-3 per entry (north star
+  per-step tolerance), v = (x_t - x0)/sigma reported beside it;
+* free-running 13-block runs, o=1 (bidirectional cascade) and o=5 (the
+  sequential rollout), final latents rel-L2 <= 1e-2 per block;
+* Wan2.1-14B geometry at its full 40 layers on a reduced latent grid.
+
+Margins go to $BC_PARITY_REPORT (JSON) when set (profiles/r2_wan_parity_full.json).
+"""
+
+import json
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+STEP_TOL = 2e-3
+RUN_TOL = 1e-2
+REPORT = {}
+
+
+def rel(a, b):
+    import torch
+    a = torch.as_tensor(a).double().flatten()
+    b = torch.as_tensor(b).double().flatten().to(a.device)
+    return float((a - b).norm() / b.norm())
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _report():
+    yield
+    path = os.environ.get("BC_PARITY_REPORT")
+    if path and REPORT:
+        os.makedirs(os.path.dirname(os.path.abspath(path)), exist_ok=True)
+        with open(path, "w") as fh:
+            json.dump(REPORT, fh, indent=1, sort_keys=True)
+
+
+def _free():
+    import gc
+    import torch
+    gc.collect()
+    torch.cuda.empty_cache()
+
+
+class _TapRuntime:
+    """engine._runtime_for replacement: the product WanSession, except that at
+    iteration ``tap`` the step's exact inputs are also run through the
+    product with post = x0 and through the fp32 oracle."""
+
+    def __init__(self, weights, tap, oracle, sink):
+        self.weights, self.tap, self.oracle, self.sink = weights, tap, oracle, sink
+
+    def __call__(self, weights, config):
+        return self
+
+    def open_session(self, config, cond, session_seed, noise_feed=None):
+        from paper_2511_20426_b200 import _native as N
+        from paper_2511_20426_b200.wan import POST_X0, WanSession, _make_update, text_states
+        tap, oracle, sink = self.tap, self.oracle, self.sink
+
+        class Tap(WanSession):
+            def step(self, plan, mask, pool, vis_lists, posts):
+                if plan.iteration == tap:
+                    self._tap(plan, mask, vis_lists)
+                super().step(plan, mask, pool, vis_lists, posts)
+
+            def _tap(self, plan, mask, vis_lists):
+                torch = self.torch
+                req, dst = [], []
+                for e in plan.entries:             # what step() would do first
+                    self.slots.acquire(e.block_index)
+                    if e.pass_index == 0 and e.block_index not in self.latents:
+                        t = torch.empty(self.shape, dtype=torch.float32, device="cuda")
+                        self.latents[e.block_index] = t
+                        req.append((e.block_index, 0))
+                        dst.append(t)
+                if req:
+                    self.noise.fetch(req, dst)
+                blocks = plan.blocks
+                n = len(blocks)
+                lat = [self.latents[b].clone() for b in blocks]
+                x_in = [x.clone() for x in lat]
+                outs = [torch.empty_like(x) for x in lat]
+                levels = [e.noise_level for e in plan.entries]
+                vis = [[self.slots.slot_of(v) for v in lst] for lst in vis_lists]
+                bt = N.make_batch(self.cfg.block_size, blocks, levels,
+                                  [self.slots.slot_of(b) for b in blocks], vis)
+                self.ctx.step(bt, _make_update([POST_X0] * n, lat, [None] * n, outs, [None] * n))
+                torch.cuda.synchronize()
+                self.ctx.check_status()
+                arena = self.ctx.arena
+                pool_kv = {b: (lambda l, s=self.slots.slot_of(b): (arena[l, s, 0], arena[l, s, 1]))
+                           for b in mask.pool_blocks}
+                text_kv = oracle.context(text_states(self.cond, self.cfg.text_len, self.cfg.text_dim))
+                ref = oracle.forward([(b, x, lv) for b, x, lv in zip(blocks, x_in, levels)], pool_kv,
+                                     dict(zip(blocks, vis_lists)), text_kv=text_kv)
+                rows = []
+                for b, x, o, lv, (x0r, kvr, vr) in zip(blocks, x_in, outs, levels, ref):
+                    s = self.slots.slot_of(b)
+                    row = {"block": b, "level": lv, "visible_frames": mask.visible_frames(b),
+                           "x0_rel": rel(o, x0r)}
+                    if lv > 0:
+                        row["v_rel"] = rel((x - o) / (lv / 1000.0), vr)
+                    kk = [rel(arena[l, s, 0].float(), kvr[l][0]) for l in range(self.cfg.layers)]
+                    vv = [rel(arena[l, s, 1].float(), kvr[l][1]) for l in range(self.cfg.layers)]
+                    row["k_rel_max"], row["v_cache_rel_max"] = max(kk), max(vv)
+                    row["k_rel_last_layer"], row["v_cache_rel_last_layer"] = kk[-1], vv[-1]
+                    rows.append(row)
+                sink.extend(rows)
+                del ref, text_kv
+
+        return Tap(self.weights.runtime(), config, cond, session_seed, noise_feed)
+
+
+def _teacher_forced(monkeypatch, cfg, weights, tap):
+    import paper_2511_20426_b200 as bc
+    from paper_2511_20426_b200 import engine
+    from oracle.wan_torch import WanTorchOracle
+    rows = []
+    with monkeypatch.context() as m:
+        m.setattr(engine, "_runtime_for", _TapRuntime(weights, tap, WanTorchOracle(weights.t, cfg), rows))
+        bc.run_cascade(cfg, "a lighthouse in a storm", weights=weights)
+    assert len(rows) == min(cfg.cascade_width, cfg.num_blocks)
+    return rows
+
+
+def _free_running(monkeypatch, cfg, weights):
+    import paper_2511_20426_b200 as bc
+    from paper_2511_20426_b200 import engine
+    from oracle.loop import wan_torch_oracle_runtime
+    gpu = bc.run_cascade(cfg, "a lighthouse in a storm", weights=weights)
+    weights.runtime().release_cached()
+    _free()
+    with monkeypatch.context() as m:
+        m.setattr(engine, "_runtime_for", wan_torch_oracle_runtime(weights.t))
+        cpu = bc.run_cascade(cfg, "a lighthouse in a storm", weights=weights)
+    assert gpu.emitted_order == cpu.emitted_order
+    assert [e.pool_state for e in gpu.trace.events] == [e.pool_state for e in cpu.trace.events]
+    errs = [rel(gpu.outputs[b], cpu.outputs[b]) for b in range(cfg.num_blocks)]
+    del cpu
+    _free()
+    return errs
+
+
+@pytest.fixture(scope="module")
+def w13():
+    import paper_2511_20426_b200 as bc
+    from paper_2511_20426_b200.wan import WanWeights
+    cfg = bc.wan_config("1.3b", total_frames=39, offset=1, attention_mode="bidirectional",
+                        window_blocks=7, sink_blocks=1)
+    w = WanWeights.random(cfg, 7)
+    yield cfg, w
+    w.runtime().release_cached()
+    del w
+    _free()
+
+
+@pytest.mark.parametrize("mode", ["bidirectional", "causal"])
+def test_13b_full_depth_steady_state_step(w13, monkeypatch, mode):
+    import paper_2511_20426_b200 as bc
+    cfg, w = w13
+    cfg = bc.with_fields(cfg, attention_mode=mode)
+    rows = _teacher_forced(monkeypatch, cfg, w, tap=12)
+    REPORT[f"1.3b_L30_step_it12_{mode}"] = rows
+    assert [r["block"] for r in rows] == [8, 9, 10, 11, 12]
+    assert rows[-1]["visible_frames"] == (39 if mode == "bidirectional" else 39)
+    for r in rows:
+        assert r["x0_rel"] <= STEP_TOL, r
+
+
+@pytest.mark.parametrize("offset", [1, 5])
+def test_13b_full_depth_free_running(w13, monkeypatch, offset):
+    import paper_2511_20426_b200 as bc
+    cfg, w = w13
+    errs = _free_running(monkeypatch, bc.with_fields(cfg, offset=offset), w)
+    REPORT[f"1.3b_L30_run_o{offset}_bidirectional"] = errs
+    assert max(errs) <= RUN_TOL, errs
+
+
+@pytest.fixture(scope="module")
+def w14():
+    import paper_2511_20426_b200 as bc
+    from paper_2511_20426_b200.wan import WanWeights
+    _free()
+    cfg = bc.wan_config("14b", latent_height=16, latent_width=32, total_frames=39, offset=1,
+                        attention_mode="bidirectional", window_blocks=7, sink_blocks=1)
+    w = WanWeights.random(cfg, 7)
+    yield cfg, w
+    w.runtime().release_cached()
+    del w
+    _free()
+
+
+def test_14b_full_depth_steady_state_step(w14, monkeypatch):
+    cfg, w = w14
+    rows = _teacher_forced(monkeypatch, cfg, w, tap=12)
+    REPORT["14b_L40_16x32_step_it12_bidirectional"] = rows
+    for r in rows:
+        assert r["x0_rel"] <= STEP_TOL, r
+
+
+def test_14b_full_depth_free_running(w14, monkeypatch):
+    cfg, w = w14
+    errs = _free_running(monkeypatch, cfg, w)
+    REPORT["14b_L40_16x32_run_o1_bidirectional"] = errs
+    assert max(errs) <= RUN_TOL, errs
