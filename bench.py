@@ -105,63 +105,140 @@ def dist_env():
 # CPU reference / baseline (oracle port of the path, numpy fp32)
 # ---------------------------------------------------------------------------
 
-def cpu_sample_seconds(cfg, reps=1):
-    """Time one bounded sample of the workload on the host cores: ONE of the
-    `layers` transformer layers for ONE of the 5 entries of a steady-state
-    cascade iteration (13 visible blocks = 60,840 keys, 4,680 query tokens,
-    512 text tokens), numpy fp32 oracle (oracle/wan.py)."""
-    import numpy as np
-    from oracle import wan as wo
-    d, T = cfg.model_dim, cfg.tokens_per_block
-    rng = np.random.default_rng(0)
+def blas_threads():
+    """Threads numpy's BLAS runs with (threadpoolctl), else the core count."""
+    try:
+        from threadpoolctl import threadpool_info
+        n = [i.get("num_threads") for i in threadpool_info() if i.get("user_api") == "blas"]
+        if n and n[0]:
+            return int(n[0])
+    except Exception:
+        pass
+    return os.cpu_count() or 1
 
-    def w(*shape, fan):
-        return (rng.standard_normal(shape, dtype=np.float32) / np.sqrt(fan)).astype(np.float32)
 
-    p = {"qkv_w": w(3 * d, d, fan=d), "qkv_b": w(3 * d, fan=50), "o_w": w(d, d, fan=d),
-         "o_b": w(d, fan=50), "cq_w": w(d, d, fan=d), "cq_b": w(d, fan=50),
-         "co_w": w(d, d, fan=d), "co_b": w(d, fan=50), "ffn1_w": w(cfg.ffn_dim, d, fan=d),
-         "ffn1_b": w(cfg.ffn_dim, fan=50), "ffn2_w": w(d, cfg.ffn_dim, fan=cfg.ffn_dim),
-         "ffn2_b": w(d, fan=50), "nq": 1 + w(d, fan=400), "nk": 1 + w(d, fan=400),
-         "n3w": 1 + w(d, fan=400), "n3b": w(d, fan=50), "cnq": 1 + w(d, fan=400),
-         "mod": w(6, d, fan=d)}
-    X = rng.standard_normal((T, d), dtype=np.float32)
-    pool_k = rng.standard_normal((12 * T, d), dtype=np.float32)
-    pool_v = rng.standard_normal((12 * T, d), dtype=np.float32)
-    tk = rng.standard_normal((cfg.text_len, d), dtype=np.float32)
-    tv = rng.standard_normal((cfg.text_len, d), dtype=np.float32)
-    cos, sin = wo.rope_tables(27, cfg.block_size, cfg.latent_height // 2, cfg.latent_width // 2)
-    H = cfg.heads
-    times = []
-    for _ in range(reps):
+class CpuLayerSample:
+    """One transformer layer of ONE entry with ``vis_frames`` visible latent
+    frames (4,680 query tokens at 480x832; pool + own keys; 512 text
+    tokens), numpy fp32 oracle (oracle/wan.py), timed on the host cores.
+    Random activations / weights of the layer's shapes (built once)."""
+
+    def __init__(self, cfg, max_vis_frames=39):
+        import numpy as np
+        self.cfg = cfg
+        d, T = cfg.model_dim, cfg.tokens_per_block
+        rng = np.random.default_rng(0)
+
+        def w(*shape, fan):
+            return (rng.standard_normal(shape, dtype=np.float32) / np.sqrt(fan)).astype(np.float32)
+
+        self.p = {"qkv_w": w(3 * d, d, fan=d), "qkv_b": w(3 * d, fan=50), "o_w": w(d, d, fan=d),
+                  "o_b": w(d, fan=50), "cq_w": w(d, d, fan=d), "cq_b": w(d, fan=50),
+                  "co_w": w(d, d, fan=d), "co_b": w(d, fan=50), "ffn1_w": w(cfg.ffn_dim, d, fan=d),
+                  "ffn1_b": w(cfg.ffn_dim, fan=50), "ffn2_w": w(d, cfg.ffn_dim, fan=cfg.ffn_dim),
+                  "ffn2_b": w(d, fan=50), "nq": 1 + w(d, fan=400), "nk": 1 + w(d, fan=400),
+                  "n3w": 1 + w(d, fan=400), "n3b": w(d, fan=50), "cnq": 1 + w(d, fan=400),
+                  "mod": w(6, d, fan=d)}
+        self.X = rng.standard_normal((T, d), dtype=np.float32)
+        pool_tokens = max(0, max_vis_frames // cfg.block_size - 1) * T
+        self.pool_k = rng.standard_normal((pool_tokens, d), dtype=np.float32)
+        self.pool_v = rng.standard_normal((pool_tokens, d), dtype=np.float32)
+        self.tk = rng.standard_normal((cfg.text_len, d), dtype=np.float32)
+        self.tv = rng.standard_normal((cfg.text_len, d), dtype=np.float32)
+
+    def seconds(self, vis_frames):
+        import numpy as np
+        from oracle import wan as wo
+        cfg, p = self.cfg, self.p
+        d, T, H = cfg.model_dim, cfg.tokens_per_block, cfg.heads
+        npool = (vis_frames // cfg.block_size - 1) * T
+        cos, sin = wo.rope_tables(27, cfg.block_size, cfg.latent_height // 2, cfg.latent_width // 2)
+        X = self.X
         t0 = time.perf_counter()
         m = p["mod"]
         xn = wo.layer_norm(X) * (1 + m[1]) + m[0]
         qkv = xn @ p["qkv_w"].T + p["qkv_b"]
         q = wo.apply_rope(wo.rms_norm(qkv[:, :d], p["nq"]).reshape(T, H, 128), cos, sin).reshape(T, d)
         k = wo.apply_rope(wo.rms_norm(qkv[:, d:2 * d], p["nk"]).reshape(T, H, 128), cos, sin).reshape(T, d)
-        att = wo.attention(q, np.concatenate([pool_k, k]), np.concatenate([pool_v, qkv[:, 2 * d:]]), H)
+        att = wo.attention(q, np.concatenate([self.pool_k[:npool], k]),
+                           np.concatenate([self.pool_v[:npool], qkv[:, 2 * d:]]), H)
         Xo = X + m[2] * (att @ p["o_w"].T + p["o_b"])
         xc = wo.layer_norm(Xo) * p["n3w"] + p["n3b"]
         qc = wo.rms_norm(xc @ p["cq_w"].T + p["cq_b"], p["cnq"])
-        Xo = Xo + wo.attention(qc, tk, tv, H) @ p["co_w"].T + p["co_b"]
+        Xo = Xo + wo.attention(qc, self.tk, self.tv, H) @ p["co_w"].T + p["co_b"]
         xm = wo.layer_norm(Xo) * (1 + m[4]) + m[3]
         Xo = Xo + m[5] * (wo.gelu_tanh(xm @ p["ffn1_w"].T + p["ffn1_b"]) @ p["ffn2_w"].T + p["ffn2_b"])
-        times.append(time.perf_counter() - t0)
-    return times
+        return time.perf_counter() - t0
 
 
-def cpu_fps_from_sample(cfg, sample_s):
-    width = min(cfg.cascade_width, cfg.num_blocks)
-    iter_s = sample_s * cfg.layers * width     # one steady-state iteration emits one block
-    return FRAMES_PER_BLOCK / iter_s
+def trace_visible_frames(cfg):
+    """Visible latent frames of every entry of the run, from the closed-form
+    schedule and pool replay (oracle/schedule.py, restating the reference's
+    tests/oracles.py:8-39): block k runs pass p at iteration k*o + p and
+    enters the pool after its cache pass."""
+    from oracle.schedule import enumerate_schedule, replay_pool, visible_blocks
+    P, o, S = cfg.passes, cfg.offset, cfg.block_size
+    rows = enumerate_schedule(cfg.num_blocks, P, o)
+    out = []
+    for i, row in enumerate(rows):
+        inserted = [k for k in range(cfg.num_blocks) if k * o + P - 1 < i]
+        pool, _ = replay_pool(inserted, cfg.window_blocks, cfg.sink_blocks)
+        vis = visible_blocks([k for k, _ in row], pool, cfg.attention_mode)
+        out += [len(v) * S for v in vis.values()]
+    return out
 
 
-def cpu_sample_desc(cfg):
-    return (f"1 of {cfg.layers} layers x 1 of {min(cfg.cascade_width, cfg.num_blocks)} entries of a "
-            f"steady-state cascade iteration ({cfg.tokens_per_block} query tokens, 13 visible blocks = "
-            f"{13 * cfg.tokens_per_block} keys, {cfg.text_len} text tokens), numpy fp32 oracle; "
-            f"fps = 12 frames / (sample x {cfg.layers * min(cfg.cascade_width, cfg.num_blocks)})")
+def fit_line(points):
+    """Least-squares t = a + b * frames over (frames, seconds) samples (per
+    layer and entry, attention is linear in the visible keys, the rest is
+    constant)."""
+    xs = [float(x) for x, _ in points]
+    ys = [float(y) for _, y in points]
+    n = len(xs)
+    mx, my = sum(xs) / n, sum(ys) / n
+    sxx = sum((x - mx) ** 2 for x in xs)
+    b = sum((x - mx) * (y - my) for x, y in zip(xs, ys)) / sxx if sxx > 0 else 0.0
+    return my - b * mx, b
+
+
+def cpu_run_seconds(cfg, points):
+    """Host seconds of the whole run: layers x sum over the run's entries of
+    the fitted per-layer time at that entry's visible-frame count."""
+    a, b = fit_line(points)
+    vis = trace_visible_frames(cfg)
+    return cfg.layers * sum(a + b * v for v in vis), len(vis), (a, b)
+
+
+def cpu_sample_frames(cfg):
+    top = min(cfg.num_blocks, cfg.window_blocks + cfg.sink_blocks + cfg.cascade_width) * cfg.block_size
+    return sorted({cfg.block_size, (cfg.block_size + top) // 2 // cfg.block_size * cfg.block_size, top})
+
+
+def cpu_baseline(cfg, frames=None, pts=None):
+    """cpu_baseline object for one config (rank 0, N=1): one timed layer
+    sample at each of 2-3 distinct visible-frame counts, line fit, summed
+    over the run's real entry list.  ``pts`` reuses another config's samples
+    of the same model (same layer shapes; only the entry list differs)."""
+    if pts is None:
+        frames = frames or cpu_sample_frames(cfg)
+        samp = CpuLayerSample(cfg, max(frames))
+        samp.seconds(frames[0])                                # page-in
+        pts = [(f, samp.seconds(f)) for f in frames]
+    frames = [f for f, _ in pts]
+    run_s, entries, (a, b) = cpu_run_seconds(cfg, pts)
+    return {"value": cfg.num_blocks * FRAMES_PER_BLOCK / run_s, "unit": "frames/s",
+            "cores": blas_threads(), "kind": "port",
+            "sample": cpu_sample_desc(cfg, frames, entries),
+            "sample_seconds": {str(f): round(t, 3) for f, t in pts},
+            "fit_s_per_layer": [round(a, 4), round(b, 5)],
+            "run_seconds_estimate": round(run_s, 1), "points": pts}
+
+
+def cpu_sample_desc(cfg, frames, entries):
+    return (f"numpy fp32 oracle (oracle/wan.py), BLAS threads {blas_threads()}: one layer of one entry "
+            f"({cfg.tokens_per_block} query tokens, {cfg.text_len} text tokens) timed at visible frames "
+            f"{frames}; t(frames) fitted linear and summed over the run's {entries} entries x "
+            f"{cfg.layers} layers (embed/head/noise excluded)")
 
 
 TOY_CFG1 = dict(layers=4, latent_dim=256, heads=2, head_dim=128, cond_dim=256, total_frames=18,
@@ -241,35 +318,60 @@ def metric_name(args):
     return f"generated frames/sec (cascaded, Wan2.1-{args.preset.upper()}-shaped, 480x832)"
 
 
-def workload_config(args, cfg, parallelism):
+def parallelism(world):
+    if world == 1:
+        return "temporal1"
+    from paper_2511_20426_b200.distributed import shard_mode
+    push = "copy-engine side stream" if os.environ.get("BC_KV_PUSH") == "copy" else "q/k-kernel P2P stores"
+    return f"temporal{world} (shard={shard_mode()}, kv_push={push}, IPC peer memory over NVLink)"
+
+
+def workload_config(args, cfg, par):
     return {"workload": f"wan2.1-{args.preset} cascade o=1, {cfg.num_blocks} blocks "
                         f"({cfg.num_blocks * FRAMES_PER_BLOCK} frames), 480x832, 4-step, "
-                        f"3 latent frames/block, bidirectional, W=7 sink={args.sink}"
+                        f"3 latent frames/block, {cfg.attention_mode}, W={cfg.window_blocks} "
+                        f"sink={cfg.sink_blocks}"
                         + (f", cascade prompt switch every {args.switch_every} blocks"
                            if args.switch_every else ""),
             "model": f"wan2.1-{args.preset}-shaped", "global_batch": 1,
-            "seq_len": cfg.tokens_per_block, "parallelism": parallelism,
+            "seq_len": cfg.tokens_per_block, "parallelism": par,
             "l2": "working set (weights + KV arena) >> 126 MB L2; no flush"}
 
 
 def run_reference(args, cfg):
+    """The reference arm: the oracle port of the path on the host cores.
+    Each step times ONE layer of one entry at one visible-frame count
+    (rotating over the counts the run has); value = the run's frames over
+    the line fit summed across the run's real entry list x layers."""
     world, rank, _ = dist_env()
     if rank != 0:
         return
-    cores = os.cpu_count()
-    for _ in range(args.warmup):
-        cpu_sample_seconds(cfg)
-    times = [cpu_sample_seconds(cfg)[0] for _ in range(args.steps)]
-    per = statistics.mean(times)
-    fps = cpu_fps_from_sample(cfg, per)
+    vis = sorted(set(trace_visible_frames(cfg)))
+    order = []
+    lo, hi = 0, len(vis) - 1
+    while lo <= hi:                       # extremes first: the fit is anchored early
+        order.append(vis[hi])
+        if lo != hi:
+            order.append(vis[lo])
+        lo, hi = lo + 1, hi - 1
+    samp = CpuLayerSample(cfg, max(vis))
+    for i in range(args.warmup):
+        samp.seconds(order[i % len(order)])
+    pts = [(order[i % len(order)], samp.seconds(order[i % len(order)])) for i in range(args.steps)]
+    if len({f for f, _ in pts}) < 2:      # a line needs two distinct counts
+        pts.append((order[1 % len(order)], samp.seconds(order[1 % len(order)])))
+    run_s, entries, (a, b) = cpu_run_seconds(cfg, pts)
+    fps = cfg.num_blocks * FRAMES_PER_BLOCK / run_s
+    per = statistics.mean(t for _, t in pts)
     line = {
         "impl": "reference", "metric": metric_name(args),
-        "value": fps, "unit": "frames/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": per * 1e3, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-        "dtype": "f32", "data": "synthetic (random-init weights, N(0,1) activations)",
-        "config": workload_config(args, cfg, f"temporal{world}"),
-        "cpu_baseline": {"value": fps, "unit": "frames/s", "cores": cores, "kind": "port",
-                         "sample": cpu_sample_desc(cfg)},
+        "value": fps, "unit": "frames/s", "n_gpus": max(world, args.gpus), "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": per * 1e3, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic (random-init weights, N(0,1) activations)",
+        "config": workload_config(args, cfg, "host cores (reference CPU path)"),
+        "cpu_baseline": {"value": fps, "unit": "frames/s", "cores": blas_threads(), "kind": "port",
+                         "sample": cpu_sample_desc(cfg, sorted({f for f, _ in pts}), entries),
+                         "fit_s_per_layer": [a, b], "run_seconds_estimate": run_s},
         "e2e": {"value": fps, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -279,96 +381,201 @@ def run_reference(args, cfg):
 # our arm
 # ---------------------------------------------------------------------------
 
+class Ctx:
+    """Per-process measurement plumbing (ranks, barrier, max over ranks)."""
+
+    def __init__(self):
+        import torch
+        self.torch = torch
+        self.world, self.rank, local = dist_env()
+        # BC_FORCE_DEVICE / BC_DIST_BACKEND: test hooks to run the multi-rank
+        # bench with several ranks on one GPU over gloo (NCCL refuses duplicate
+        # GPUs); the driver's runs use one GPU per rank and NCCL
+        self.dev = int(os.environ.get("BC_FORCE_DEVICE", local))
+        self.backend = os.environ.get("BC_DIST_BACKEND", "nccl")
+        torch.cuda.set_device(self.dev)
+        if self.world > 1:
+            import torch.distributed as dist
+            dist.init_process_group(self.backend)
+
+    def barrier(self):
+        if self.world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+
+    def max(self, x):
+        if self.world == 1:
+            return x
+        import torch.distributed as dist
+        t = self.torch.tensor([x], dtype=self.torch.float64,
+                              device="cuda" if self.backend == "nccl" else "cpu")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def device_timed(self, fn, steps, clocks_index=None):
+        """K calls bracketed by barrier + synchronize, CUDA events on the
+        launching stream; returns (max-over-ranks ms, results, clocks)."""
+        torch = self.torch
+        self.barrier()
+        torch.cuda.synchronize()
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with ClockSampler(self.dev if clocks_index is None else clocks_index) as clocks:
+            ev0.record()
+            out = [fn() for _ in range(steps)]
+            ev1.record()
+            torch.cuda.synchronize()
+        self.barrier()
+        return self.max(ev0.elapsed_time(ev1)), out, clocks.summary()
+
+    def host_timed(self, fn, steps):
+        """End to end: host clock around K calls (host buffers in, results
+        out), synchronize on both sides, max over ranks."""
+        torch = self.torch
+        self.barrier()
+        torch.cuda.synchronize()
+        with ClockSampler(self.dev) as clocks:
+            t0 = time.perf_counter()
+            out = [fn() for _ in range(steps)]
+            torch.cuda.synchronize()
+            s = time.perf_counter() - t0
+        self.barrier()
+        return self.max(s) * 1e3, out, clocks.summary()
+
+
+def measure_config(C, bc, cfg, weights, steps, warmup, switches=(), seq=True, feed=None):
+    """value (device-resident noise, graphs, no per-kernel events) and e2e
+    (public run_cascade, host noise H2D, blocks D2H) for the cascade and, if
+    asked, the sequential rollout of the same model -- both arms measured the
+    same way (same K, W, clock and noise path)."""
+    from paper_2511_20426_b200.metrics import streaming_fps
+    from paper_2511_20426_b200.wan import ResidentNoiseFeed, run_noise_keys
+    feed = feed or ResidentNoiseFeed(SESSION_SEED, cfg, run_noise_keys(cfg))
+    frames = cfg.num_blocks * FRAMES_PER_BLOCK
+    out = {}
+    arms = [("cascade", cfg, bc.run_cascade)]
+    if seq:
+        arms.append(("sequential", bc.with_fields(cfg, offset=cfg.passes), None))
+    for name, c, _ in arms:
+        if name == "cascade":
+            def dev_run(c=c):
+                return bc.run_cascade(c, PROMPT, session_seed=SESSION_SEED, weights=weights,
+                                      noise_feed=feed, switches=list(switches))
+
+            def host_run(c=c):
+                return bc.run_cascade(c, PROMPT, session_seed=SESSION_SEED, weights=weights,
+                                      switches=list(switches))
+        else:
+            def dev_run(c=c):
+                return bc.run_sequential_reference(c, PROMPT, session_seed=SESSION_SEED,
+                                                   weights=weights, noise_feed=feed)
+
+            def host_run(c=c):
+                return bc.run_sequential_reference(c, PROMPT, session_seed=SESSION_SEED, weights=weights)
+        for _ in range(warmup):
+            dev_run()
+        l0 = __import__("paper_2511_20426_b200._native", fromlist=["x"]).launch_count()
+        ms, runs, clocks = C.device_timed(dev_run, steps)
+        launches = __import__("paper_2511_20426_b200._native", fromlist=["x"]).launch_count() - l0
+        host_run()                       # pinned staging / first-touch warm-up of the host path
+        e2e_ms, _, clocks_e2e = C.host_timed(host_run, steps)
+        out[name] = {"value": frames * steps / (ms / 1e3), "ms_per_step": ms / steps,
+                     "streaming_fps": statistics.mean(streaming_fps(r.trace, clock="wall") for r in runs),
+                     "e2e": frames * steps / (e2e_ms / 1e3), "e2e_ms_per_step": e2e_ms / steps,
+                     "launches": launches, "clocks": clocks, "clocks_e2e": clocks_e2e,
+                     "last_run": runs[-1]}
+    return out, feed
+
+
+def kernel_profile(bc, N, cfg, weights, feed):
+    """Per-kernel-class breakdown in a SEPARATE pass: one generation launched
+    eagerly with CUDA events around every launch on its stream
+    (bc_profile_enable); the timed value above runs as CUDA graphs without
+    events.  Returns ({class: (ms, flops, bytes, launches)}, run ms)."""
+    import torch
+    N.profile_collect()
+    N.profile_enable(True)
+    try:
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        bc.run_cascade(cfg, PROMPT, session_seed=SESSION_SEED, weights=weights, noise_feed=feed)
+        torch.cuda.synchronize()
+        wall = (time.perf_counter() - t0) * 1e3
+    finally:
+        prof = N.profile_collect()
+        N.profile_enable(False)
+    return prof, wall
+
+
+def kernels_and_roofline(prof, peaks, peak_kind):
+    total = sum(v[0] for v in prof.values())
+    kernels = {k: {"ms": round(v[0], 3), "launches": v[3],
+                   "tflops": round(v[1] / (v[0] / 1e3) / 1e12, 1) if v[0] > 0 and v[1] > 0 else None,
+                   "gbs": round(v[2] / (v[0] / 1e3) / 1e9, 1) if v[0] > 0 and v[2] > 0 else None,
+                   "share": round(v[0] / total, 4) if total else None}
+               for k, v in prof.items()}
+    dom = max(("self_attention", "cross_attention", "gemm"), key=lambda k: prof[k][0])
+    dom_ms, dom_flops, _, dom_n = prof[dom]
+    achieved = dom_flops / (dom_ms / 1e3) / 1e12 if dom_ms > 0 else None
+    peak = peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops"))
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tpath):
+        with open(tpath) as fh:
+            traffic = json.load(fh).get(dom)
+    roof = {"bound": "tensor", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+            "frac": achieved / peak if achieved else None, "traffic": traffic,
+            "peak_kind": f"{peak_kind} bf16 sustained", "launches": dom_n,
+            "share_of_step": kernels[dom]["share"],
+            "launch_mode": "separate profiled generation: eager launches, CUDA events around each "
+                           "launch on its stream"}
+    return kernels, roof
+
+
+def sub_line(C, bc, name, cfg, weights, args, switches=(), seq=False, cpu_pts=None, feed=None,
+             frames=None):
+    """A secondary configuration (14B, LongLive-style, causal cascade): value
+    and e2e measured like the headline with W = 1, K = 1 (a generation is
+    2.4-20 s), plus its CPU baseline on rank 0 at N = 1 (same-model configs
+    reuse the headline's layer samples, summed over their own entry list)."""
+    steps = 1
+    res, _ = measure_config(C, bc, cfg, weights, steps, 1, switches=switches, seq=seq, feed=feed)
+    cas = res["cascade"]
+    line = {"workload": name, "value": cas["value"], "unit": "frames/s", "steps": steps, "warmup": 1,
+            "ms_per_step": cas["ms_per_step"], "streaming_fps": cas["streaming_fps"],
+            "e2e": {"value": cas["e2e"], "unit": "frames/s"}, "gpu_launches": cas["launches"],
+            "clocks": cas["clocks"]}
+    if seq:
+        s = res["sequential"]
+        line["sequential"] = {"value": s["value"], "e2e": s["e2e"], "streaming_fps": s["streaming_fps"]}
+    if C.world == 1 and C.rank == 0 and not args.no_cpu:
+        line["cpu_baseline"] = cpu_baseline(cfg, frames=frames, pts=cpu_pts)
+    return line
+
+
 def run_ours(args, cfg):
     import torch
     import paper_2511_20426_b200 as bc
     from paper_2511_20426_b200 import _native as N
-    from paper_2511_20426_b200.metrics import end_to_end_fps, streaming_fps
-    from paper_2511_20426_b200.wan import ResidentNoiseFeed, WanWeights, run_noise_keys
+    from paper_2511_20426_b200.metrics import end_to_end_fps
+    from paper_2511_20426_b200.wan import WanWeights, run_noise_keys
 
-    world, rank, local = dist_env()
-    # BC_FORCE_DEVICE / BC_DIST_BACKEND: test hooks to run the multi-rank
-    # bench with several ranks on one GPU over gloo (NCCL refuses duplicate
-    # GPUs); the driver's runs use one GPU per rank and NCCL
-    dev = int(os.environ.get("BC_FORCE_DEVICE", local))
-    backend = os.environ.get("BC_DIST_BACKEND", "nccl")
-    torch.cuda.set_device(dev)
-    if world > 1:
-        import torch.distributed as dist
-        dist.init_process_group(backend)
-
-    def max_over_ranks(x):
-        if world == 1:
-            return x
-        import torch.distributed as dist
-        t = torch.tensor([x], dtype=torch.float64, device="cuda" if backend == "nccl" else "cpu")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
+    C = Ctx()
+    world, rank = C.world, C.rank
     weights = WanWeights.random(cfg, WEIGHT_SEED)
-    seq_cfg = bc.with_fields(cfg, offset=cfg.passes)
-    feed = ResidentNoiseFeed(SESSION_SEED, cfg, run_noise_keys(cfg))
-
-    def barrier():
-        if world > 1:
-            import torch.distributed as dist
-            dist.barrier()
-
     switches = [bc.SwitchSpec(f"{PROMPT}, scene {k}", "cascade", at_block=k)
                 for k in range(args.switch_every, cfg.num_blocks, args.switch_every)] \
         if args.switch_every else []
-
-    def one_run(c=cfg, noise=feed):
-        return bc.run_cascade(c, PROMPT, session_seed=SESSION_SEED, weights=weights, noise_feed=noise,
-                              switches=switches)
-
-    for _ in range(args.warmup):
-        one_run()
-    N.profile_collect()
-    # ---- timed region: device-resident inputs ----
-    N.profile_enable(True)
-    launches0 = N.launch_count()
-    barrier()
-    torch.cuda.synchronize()
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(dev) as clocks:
-        ev0.record()
-        runs = [one_run() for _ in range(args.steps)]
-        ev1.record()
-        torch.cuda.synchronize()
-    barrier()
-    launches = N.launch_count() - launches0
-    prof = N.profile_collect()
-    N.profile_enable(False)
-    ms = max_over_ranks(ev0.elapsed_time(ev1))
-    # temporal parallelism: all ranks cooperate on ONE video (strong scaling)
     frames = cfg.num_blocks * FRAMES_PER_BLOCK
-    value = frames * args.steps / (ms / 1e3)
-    stream_fps = statistics.mean(streaming_fps(r.trace, clock="wall") for r in runs)
 
-    # ---- e2e through the public API with host buffers (noise H2D, outputs D2H) ----
-    # (measured right after the device-resident runs, under the same thermal /
-    # power state; its own clock samples are reported as clocks_e2e)
-    # one untimed end-to-end run first: the host-noise path's pinned staging
-    # buffers and first-touch costs are warm-up, not steady state
-    bc.run_cascade(cfg, PROMPT, session_seed=SESSION_SEED, weights=weights, switches=switches)
-    barrier()
-    torch.cuda.synchronize()
-    with ClockSampler(dev) as clocks_e2e:
-        t0 = time.perf_counter()
-        e2e_runs = [bc.run_cascade(cfg, PROMPT, session_seed=SESSION_SEED, weights=weights,
-                                   switches=switches) for _ in range(args.steps)]
-        torch.cuda.synchronize()
-        e2e_s = time.perf_counter() - t0
-    e2e_s = max_over_ranks(e2e_s)
-    e2e_value = frames * args.steps / e2e_s
-    # ---- sequential block-causal rollout, same weights / inputs ----
-    seq_e2e = seq_stream = None
-    if not args.no_seq:
-        for _ in range(2):
-            seq = bc.run_sequential_reference(seq_cfg, PROMPT, session_seed=SESSION_SEED,
-                                              weights=weights, noise_feed=feed)
-        seq_e2e = end_to_end_fps(seq.trace)
-        seq_stream = streaming_fps(seq.trace, clock="wall")
+    # ---- headline: cascade + sequential, value (resident noise, graphs,
+    # no per-kernel events) and e2e (public API, host noise in, blocks out) ----
+    res, feed = measure_config(C, bc, cfg, weights, args.steps, args.warmup, switches=switches,
+                               seq=not args.no_seq)
+    cas = res["cascade"]
+    seq = res.get("sequential")
+
+    # ---- per-kernel-class profile: separate eager pass ----
+    prof, prof_ms = kernel_profile(bc, N, cfg, weights, feed)
 
     # ---- prompt switch at block 8: cascade mode (product: text K/V swap only)
     # vs the KV-recache baseline (SURVEY 8f rank 4; paper: ~200 ms stall) ----
@@ -391,70 +598,99 @@ def run_ours(args, cfg):
                                                     (nxt.wall_clock - prev), 2),
                             "e2e_fps": end_to_end_fps(r.trace)}
 
-    # ---- the reference's own CPU-runnable case (BASELINE configs[0]): the toy
-    # model of the reference package, fp64 on the device, vs the oracle port
-    # of it on the host (the reference code itself is not on the box) ----
-    toy = noise = None
-    if world == 1 and not args.no_cpu:
+    # ---- the reference's own CPU-runnable case (BASELINE configs[0]) ----
+    toy = noise = cpu = None
+    if world == 1 and rank == 0 and not args.no_cpu:
         toy = toy_config1_times(bc)
         noise = noise_generation_report(cfg)
+        cpu = cpu_baseline(cfg)
+
+    # ---- secondary configurations (BASELINE configs[3], [4]; causal cascade) ----
+    subs = {}
+    if not args.no_sub and args.preset == "1.3b":
+        subs["causal_cascade_1.3b"] = sub_line(
+            C, bc, "wan2.1-1.3b cascade o=1, 13 blocks, CAUSAL attention among cascaded blocks",
+            bc.with_fields(cfg, attention_mode="causal"), weights, args, seq=False,
+            cpu_pts=cpu and cpu["points"])
+        ll_cfg = bc.with_fields(cfg, total_frames=240, sink_blocks=0)
+        ll_sw = [bc.SwitchSpec(f"{PROMPT}, scene {k}", "cascade", at_block=k) for k in (20, 40, 60)]
+        subs["longlive_1.3b"] = sub_line(
+            C, bc, "LongLive-style: wan2.1-1.3b cascade o=1, 80 blocks (240 latent / 960 video frames), "
+                   "rolling W=7, no sink, cascade prompt switches at blocks 20/40/60, no KV recache",
+            ll_cfg, weights, args, switches=ll_sw, seq=False, cpu_pts=cpu and cpu["points"])
+        weights.runtime().release_cached()
+        del weights
+        import gc
+        gc.collect()
+        torch.cuda.empty_cache()
+        from paper_2511_20426_b200 import wan_config
+        c14 = wan_config("14b", total_frames=cfg.total_frames, offset=1, attention_mode="bidirectional",
+                         window_blocks=7, sink_blocks=cfg.sink_blocks)
+        w14 = WanWeights.random(c14, WEIGHT_SEED)
+        subs["wan14b"] = sub_line(
+            C, bc, "wan2.1-14b-shaped cascade o=1, 13 blocks, 480x832, bidirectional, W=7 sink=1",
+            c14, w14, args, seq=False, feed=feed, frames=[3, 39])
+        w14.runtime().release_cached()
+        del w14
 
     S = cfg.block_size
     lat_bytes = S * cfg.latent_dim * 4
     h2d = len(run_noise_keys(cfg)) * lat_bytes + cfg.text_len * cfg.text_dim * 4
     d2h = cfg.num_blocks * lat_bytes
-
     if rank != 0:
         return
     peaks, peak_kind = _peaks()
-    dom = max(("self_attention", "cross_attention", "gemm"), key=lambda k: prof[k][0])
-    dom_ms, dom_flops, _, dom_n = prof[dom]
-    achieved = dom_flops / (dom_ms / 1e3) / 1e12 if dom_ms > 0 else None
-    peak = peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops"))
-    traffic = None
-    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if os.path.exists(tpath):
-        with open(tpath) as fh:
-            traffic = json.load(fh).get(dom)
-    total_prof_ms = sum(v[0] for v in prof.values())
-    kernels = {k: {"ms": round(v[0], 3), "launches": v[3],
-                   "tflops": round(v[1] / (v[0] / 1e3) / 1e12, 1) if v[0] > 0 and v[1] > 0 else None,
-                   "gbs": round(v[2] / (v[0] / 1e3) / 1e9, 1) if v[0] > 0 and v[2] > 0 else None,
-                   "share": round(v[0] / total_prof_ms, 4) if total_prof_ms else None}
-               for k, v in prof.items()}
-    # CPU baseline on a bounded sample (rank 0, N=1 only)
-    cpu = None
-    if world == 1 and not args.no_cpu:
-        samp = cpu_sample_seconds(cfg, reps=1)[0]
-        cpu = {"value": cpu_fps_from_sample(cfg, samp), "unit": "frames/s", "cores": os.cpu_count(),
-               "kind": "port", "sample": cpu_sample_desc(cfg), "sample_seconds": samp}
+    kernels, roof = kernels_and_roofline(prof, peaks, peak_kind)
     line = {
         "metric": metric_name(args),
-        "value": value, "unit": "frames/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+        "value": cas["value"], "unit": "frames/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": cas["ms_per_step"], "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
         "data": f"synthetic (random-init Wan2.1-{args.preset.upper()}-shaped weights, counter-keyed N(0,1) "
                 "noise, hash-expanded 512x4096 text states)",
-        "config": workload_config(args, cfg, f"temporal{world}"),
-        "streaming_fps": stream_fps,
-        "sequential": {"e2e_fps": seq_e2e, "streaming_fps": seq_stream},
-        "cascade_over_sequential_streaming": stream_fps / seq_stream if seq_stream else None,
+        "config": workload_config(args, cfg, parallelism(world)),
+        "launch_mode": {"value": "CUDA graphs (one per batch width), no per-kernel events, noise "
+                                 "pre-resident in HBM" if world == 1 else
+                                 "eager multi-rank steps, noise pre-resident in HBM",
+                        "e2e": "public run_cascade, host noise generated + copied H2D per iteration, "
+                               "emitted blocks copied D2H, host clock",
+                        "kernels": "separate eager generation with per-launch CUDA events"},
+        "streaming_fps": cas["streaming_fps"],
+        "sequential": ({"value": seq["value"], "e2e": seq["e2e"], "streaming_fps": seq["streaming_fps"],
+                        "ms_per_step": seq["ms_per_step"], "steps": args.steps, "warmup": args.warmup,
+                        "method": "same as the cascade: K timed generations after W warm-ups, device "
+                                  "events with resident noise (value) and host clock with H2D noise (e2e)"}
+                       if seq else None),
+        "cascade_over_sequential": ({"value": cas["value"] / seq["value"], "e2e": cas["e2e"] / seq["e2e"],
+                                     "streaming": cas["streaming_fps"] / seq["streaming_fps"]}
+                                    if seq else None),
         "prompt_switch": switch,
         "config1_toy": toy,
         "noise_generation": noise,
-        "roofline": {"bound": "tensor", "kernel": dom, "achieved": achieved, "peak": peak,
-                     "unit": "TFLOP/s", "frac": achieved / peak if achieved else None,
-                     "traffic": traffic, "peak_kind": f"{peak_kind} bf16 sustained",
-                     "launches": dom_n, "share_of_step": kernels[dom]["share"]},
+        "roofline": roof,
         "kernels": kernels,
-        "e2e": {"value": e2e_value, "unit": "frames/s", "h2d_bytes_per_step": h2d,
+        "kernel_profile_run_ms": round(prof_ms, 1),
+        "e2e": {"value": cas["e2e"], "unit": "frames/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h},
-        "gpu_launches": launches,
-        "clocks": clocks.summary(),
-        "clocks_e2e": clocks_e2e.summary(),
+        "gpu_launches": cas["launches"],
+        "clocks": cas["clocks"],
+        "clocks_e2e": cas["clocks_e2e"],
         "cpu_baseline": cpu,
+        "configs": subs or None,
     }
     print(json.dumps(line), flush=True)
+
+
+def relaunch_under_torchrun(args):
+    """--gpus N>1 outside torchrun: one process per GPU under
+    torch.distributed.run (127.0.0.1 rendezvous); rank 0 prints the line."""
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.run(cmd).returncode
 
 
 def main():
@@ -465,14 +701,18 @@ def main():
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--preset", default="1.3b")
     ap.add_argument("--blocks", type=int, default=13)
-    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline sample")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline samples")
     ap.add_argument("--sink", type=int, default=1, help="sink blocks (LongLive-style: 0)")
     ap.add_argument("--switch-every", type=int, default=0,
-                    help="cascade-mode prompt switch every N blocks (LongLive-style config 5)")
+                    help="cascade-mode prompt switch every N blocks")
     ap.add_argument("--no-seq", action="store_true", help="skip the sequential rollout")
     ap.add_argument("--no-switch", action="store_true",
                     help="skip the cascade-vs-recache prompt-switch measurement")
+    ap.add_argument("--no-sub", action="store_true",
+                    help="skip the 14B / LongLive / causal secondary configurations")
     args = ap.parse_args()
+    if args.impl == "ours" and args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(relaunch_under_torchrun(args))
     from paper_2511_20426_b200 import wan_config
     cfg = wan_config(args.preset, total_frames=3 * args.blocks, offset=1,
                      attention_mode="bidirectional", window_blocks=7, sink_blocks=args.sink)

@@ -783,14 +783,14 @@ __global__ void __launch_bounds__(kThreads, 1)
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 encoder() {
-  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-  if (!fn) {
+  static const PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
     cudaDriverEntryPointQueryResult q;
     void* p = nullptr;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
-        q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
-  }
+    return (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+               ? reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p)
+               : nullptr;
+  }();
   return fn;
 }
 
@@ -812,27 +812,17 @@ int g_attn_balance = -1;  // -1: BC_ATTN_BALANCE env (default on)
 
 namespace {
 
-int sm_count_attn() {
-  static int n = 0;
-  if (!n) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    if (n <= 0) n = 148;
-  }
-  return n;
-}
+int sm_count_attn() { return current_sm_count(); }
 
 // Cost of a single-tile item per key tile, in units of one tile of a pair
 // (a pair costs 2).  Without a ping-pong partner the tile's softmax latency
 // (MUFU-bound: 128 exps per thread) is exposed every key tile: measured
 // ~0.9 of a whole pair.  BC_ATTN_SINGLE_COST (percent) overrides.
 double single_cost() {
-  static double c = -1.0;
-  if (c < 0.0) {
+  static const double c = [] {
     const char* e = getenv("BC_ATTN_SINGLE_COST");
-    c = e ? atof(e) / 100.0 : 1.8;
-  }
+    return e ? atof(e) / 100.0 : 1.8;
+  }();
   return c;
 }
 
@@ -931,7 +921,9 @@ std::shared_ptr<const AttnSched> build_sched(const AttnArgs& a, const AttnParams
       }
   }
   const int G = key.ctas;
-  if (pairs.size() + 2 * singles.size() + pairs.size() > (size_t)kSchedItems || a.heads > 255 ||
+  // items emitted: every pair once, plus at most one extra per pair of the
+  // last partial round when it is split into single tiles, plus the singles
+  if (pairs.size() + pairs.size() % G + singles.size() > (size_t)kSchedItems || a.heads > 255 ||
       a.n_entries > 255)
     return nullptr;
   std::stable_sort(pairs.begin(), pairs.end(), [](const WorkItem& x, const WorkItem& y) {
@@ -967,6 +959,9 @@ std::shared_ptr<const AttnSched> build_sched(const AttnArgs& a, const AttnParams
   const auto& lists = (m_split < m_keep) ? split : keep;
   auto sched = std::make_unique<AttnSched>();
   memset(sched.get(), 0, sizeof(AttnSched));
+  size_t total = 0;
+  for (const auto& l : lists) total += l.size();
+  if (total > (size_t)kSchedItems) return nullptr;  // (cannot happen given the bound above)
   int n = 0;
   for (int b = 0; b < G; ++b) {
     sched->start[b] = (uint16_t)n;
@@ -1045,13 +1040,15 @@ int attention_run(const AttnArgs& a, cudaStream_t st) {
     bc_attn_trace_ptr = buf;
   }
 #endif
-  static int poly = -1;
-  if (poly < 0) {
-    // tuning knob: pairs of exponentials (of every 8) evaluated by the FMA-pipe
-    // polynomial instead of MUFU.EX2
+  // tuning knob: pairs of exponentials (of every 8) evaluated by the FMA-pipe
+  // polynomial instead of MUFU.EX2
+  static const int poly = [] {
     const char* env = getenv("BC_ATTN_POLY");
-    poly = env ? atoi(env) : kDefaultPoly;
-    if (poly != 0 && poly != 2 && poly != 3 && poly != 4 && poly != 8) poly = kDefaultPoly;
+    const int v = env ? atoi(env) : kDefaultPoly;
+    return (v != 0 && v != 2 && v != 3 && v != 4 && v != 8) ? kDefaultPoly : v;
+  }();
+  static PerDeviceOnce grid_attrs;
+  BC_RC(per_device_once(grid_attrs, [&]() -> int {
     BC_CUDA(cudaFuncSetAttribute(attn_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, Smem::total + 1024));
     BC_CUDA(cudaFuncSetAttribute(attn_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, Smem::total + 1024));
     BC_CUDA(cudaFuncSetAttribute(attn_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, Smem::total + 1024));
@@ -1061,19 +1058,20 @@ int attention_run(const AttnArgs& a, cudaStream_t st) {
     BC_CUDA(cudaFuncGetAttributes(&fa, attn_kernel<0>));
     if (fa.numRegs != kRegsLaunch)  // the setmaxnreg split assumes this allocation (else: deadlock)
       return bc_fail(BC_ERR_CUDA, "attention kernel built with %d registers, expected %d", fa.numRegs, kRegsLaunch);
-  }
+    return BC_OK;
+  }));
   if (max_pairs == 0) return BC_OK;  // no query rows in this slice
   if (g_attn_balance < 0) {
     const char* env = getenv("BC_ATTN_BALANCE");
     g_attn_balance = env ? atoi(env) : 1;
   }
   if (a.balance && g_attn_balance && poly == 0) {
-    static bool attr = false;
-    if (!attr) {
+    static PerDeviceOnce sched_attrs;
+    BC_RC(per_device_once(sched_attrs, [&]() -> int {
       BC_CUDA(cudaFuncSetAttribute(attn_sched_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    Smem::total + 1024));
-      attr = true;
-    }
+      return BC_OK;
+    }));
     int ctas = 0;
     const std::shared_ptr<const AttnSched> sch = build_sched(a, p, &ctas);
     if (sch) {
@@ -1114,6 +1112,11 @@ extern "C" int bc_attention_plan(const bc_batch* batch, int32_t q_per_entry, int
   if (!batch || !items || !start || !n_ctas) return bc_fail(BC_ERR_CONTRACT, "attention plan: null argument");
   if (batch->n_entries < 1 || batch->n_entries > BC_MAX_ENTRIES)
     return bc_fail(BC_ERR_CONTRACT, "attention plan: bad entry count");
+  if (heads < 1 || heads > 255 || kv_tokens < 1 || q_per_entry < 1 || items_cap < 0)
+    return bc_fail(BC_ERR_CONTRACT, "attention plan: bad heads / kv_tokens / q_per_entry / items_cap");
+  for (int e = 0; e < batch->n_entries; ++e)
+    if (batch->n_vis[e] < 0 || batch->n_vis[e] > BC_MAX_VIS)
+      return bc_fail(BC_ERR_CONTRACT, "attention plan: bad visible count %d (entry %d)", batch->n_vis[e], e);
   bc::AttnArgs a{};
   bc::AttnParams p{};
   a.n_entries = batch->n_entries;

@@ -69,7 +69,10 @@ struct AttnArgs {
   // ranged = 1: q_lo / q_hi / q_row as in AttnParams, q / out have q_rows rows
   int ranged, q_rows;
   int q_lo[BC_MAX_ENTRIES], q_hi[BC_MAX_ENTRIES], q_row[BC_MAX_ENTRIES];
-  // 1: balanced persistent kernel (single-GPU launches without peer flags)
+  // 1: balanced persistent kernel (work list of query-tile items per CTA).
+  // Used by single-GPU and multi-GPU steps alike; with peer flags each item
+  // waits (bounded, %globaltimer) before its first key tile of a visible
+  // slot until every producer rank of that slot published the slot's epoch
   int balance;
 };
 

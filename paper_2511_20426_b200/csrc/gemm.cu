@@ -403,39 +403,30 @@ teardown:
 
 // ---------------------------------------------------------------- host side
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
-  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-  if (!fn) {
+  static const PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
     cudaDriverEntryPointQueryResult q;
     void* p = nullptr;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
-        q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
-  }
+    return (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+               ? reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p)
+               : nullptr;
+  }();
   return fn;
 }
 
-int sm_count() {
-  static int n = 0;
-  if (!n) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    if (n <= 0) n = 148;
-  }
-  return n;
-}
+int sm_count() { return current_sm_count(); }
 
 template <int BN, int MODE, int CG>
 int launch(const CUtensorMap& ma, const CUtensorMap& mb, void* C, int M, int N, int K,
            const float* bias, const float* gate, int gate_stride, int rows_per_gate, int gate_row0,
            cudaStream_t st) {
   using Cfg = GemmCfg<BN, CG>;
-  static bool attr = false;
-  if (!attr) {
+  static PerDeviceOnce attrs_once;
+  BC_RC(per_device_once(attrs_once, [&]() -> int {
     BC_CUDA(cudaFuncSetAttribute(gemm_kernel<BN, MODE, CG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)Cfg::kSmem));
-    attr = true;
-  }
+    return BC_OK;
+  }));
   const int tiles = ((M + BM * CG - 1) / (BM * CG)) * (N / BN);
   cudaLaunchConfig_t cfg{};
   cfg.blockDim = dim3(kThreads);
@@ -452,9 +443,13 @@ int launch(const CUtensorMap& ma, const CUtensorMap& mb, void* C, int M, int N, 
   // per unit, so a unit that only starts when another finishes doubles the
   // kernel time.  Pairs need both CTAs on one TPC, and not every TPC of the
   // part is whole, so ask the occupancy calculator how many clusters fit.
-  static int units = 0;
-  if (!units) {
-    units = sm_count() / CG;
+  static PerDeviceOnce units_once;
+  static int units_of[PerDeviceOnce::kMaxDevices];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const int slot = (dev >= 0 && dev < PerDeviceOnce::kMaxDevices) ? dev : 0;
+  per_device_once(units_once, [&]() -> int {
+    int units = sm_count() / CG;
     if (CG > 1) {
       cfg.gridDim = dim3(units * CG);
       int n = 0;
@@ -463,7 +458,10 @@ int launch(const CUtensorMap& ma, const CUtensorMap& mb, void* C, int M, int N, 
         units = n;
       (void)cudaGetLastError();
     }
-  }
+    units_of[slot] = units;
+    return BC_OK;
+  });
+  const int units = units_of[slot] > 0 ? units_of[slot] : sm_count() / CG;
   const int grid = (tiles < units ? tiles : units) * CG;
   cfg.gridDim = dim3(grid);
   BC_CUDA(cudaLaunchKernelEx(&cfg, gemm_kernel<BN, MODE, CG>, ma, mb, C, M, N, K, bias, gate, gate_stride,
@@ -531,11 +529,10 @@ int gemm_run(const GemmArgs& g, cudaStream_t st) {
   const int bn = g.bn ? g.bn : gemm_plan_bn(g.M, g.N);
   // CTA pairs for wide tiles when they still fill the machine (tuning knob
   // BC_GEMM_PAIR=0/1 overrides)
-  static int pair_env = -2;
-  if (pair_env == -2) {
+  static const int pair_env = [] {
     const char* e = getenv("BC_GEMM_PAIR");
-    pair_env = e ? atoi(e) : -1;
-  }
+    return e ? atoi(e) : -1;
+  }();
   const int pair_tiles = ((g.M + 2 * BM - 1) / (2 * BM)) * (g.N / (bn ? bn : 1));
   const bool pair = (bn == 256 || bn == 192) && g.cg != 1 &&
                     (g.cg == 2 || bn == 192 || (pair_env >= 0 ? pair_env == 1 : pair_tiles >= sm_count() / 2));

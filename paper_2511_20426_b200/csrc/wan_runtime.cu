@@ -190,26 +190,26 @@ int timed(int cls, double flops, double bytes, cudaStream_t st, F&& f) {
 }
 
 PFN_cuStreamWaitValue32_v11070 wait_value32() {
-  static PFN_cuStreamWaitValue32_v11070 fn = nullptr;
-  if (!fn) {
+  static const PFN_cuStreamWaitValue32_v11070 fn = [] {
     cudaDriverEntryPointQueryResult q;
     void* p = nullptr;
-    if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &p, cudaEnableDefault, &q) == cudaSuccess &&
-        q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<PFN_cuStreamWaitValue32_v11070>(p);
-  }
+    return (cudaGetDriverEntryPoint("cuStreamWaitValue32", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+               ? reinterpret_cast<PFN_cuStreamWaitValue32_v11070>(p)
+               : nullptr;
+  }();
   return fn;
 }
 
 PFN_cuStreamWriteValue32_v11070 write_value32() {
-  static PFN_cuStreamWriteValue32_v11070 fn = nullptr;
-  if (!fn) {
+  static const PFN_cuStreamWriteValue32_v11070 fn = [] {
     cudaDriverEntryPointQueryResult q;
     void* p = nullptr;
-    if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &p, cudaEnableDefault, &q) == cudaSuccess &&
-        q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<PFN_cuStreamWriteValue32_v11070>(p);
-  }
+    return (cudaGetDriverEntryPoint("cuStreamWriteValue32", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+               ? reinterpret_cast<PFN_cuStreamWriteValue32_v11070>(p)
+               : nullptr;
+  }();
   return fn;
 }
 

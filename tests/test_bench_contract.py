@@ -35,3 +35,25 @@ def test_noise_generation_report_tiny():
     r = bench.noise_generation_report(cfg)
     assert r["bit_identical_to_numpy"] and r["block_passes_per_run"] == 3 * 4
     assert r["bytes_per_run"] == 12 * cfg.block_size * cfg.latent_dim * 4 and r["native_ms_per_run"] > 0
+
+
+def test_trace_visible_frames_matches_engine_trace(oracle_engine):
+    """The CPU arm sums its fitted per-layer time over the run's entries;
+    the entry list (visible frames per entry, from the closed-form schedule
+    and pool replay) equals what the product engine's trace records."""
+    sys.path.insert(0, ROOT)
+    import bench
+    import paper_2511_20426_b200 as bc
+    for kw in (dict(offset=1), dict(offset=5), dict(offset=2, attention_mode="causal"),
+               dict(offset=1, sink_blocks=0, window_blocks=5)):
+        cfg = bc.CascadeConfig(total_frames=39, pass_cost_base=1.0, **kw).validate()
+        run = bc.run_cascade(cfg, "a red cube")
+        want = [e["visible_frames"] for ev in run.trace.events for e in ev.entries]
+        assert bench.trace_visible_frames(cfg) == want, kw
+
+
+def test_fit_line_exact():
+    sys.path.insert(0, ROOT)
+    import bench
+    a, b = bench.fit_line([(3, 1.0 + 0.5 * 3), (21, 1.0 + 0.5 * 21), (39, 1.0 + 0.5 * 39)])
+    assert abs(a - 1.0) < 1e-12 and abs(b - 0.5) < 1e-12

@@ -285,6 +285,7 @@ def _attention_plan(vis, q_tokens, kv_tokens, heads):
     ([[0, 1, 2], [0, 1, 2, 3], [0, 1, 2, 3, 4]], 4680, 12),  # causal-like: no equal lists
     ([[0, 1], [2, 3], [0, 1], [2, 3], [0, 1]], 328, 12),     # two groups of equal lists
     ([[0, 1]] * 2, 4680, 40),                              # 14B head count
+    ([list(range(13))] * 5, 4680, 40),                    # 14B steady state (must not fall back)
     ([[0]], 300, 2),                                       # fewer items than CTAs
 ])
 def test_attention_work_list_covers_every_tile_once(vis, q_tokens, heads):
@@ -322,3 +323,22 @@ def test_attention_work_list_covers_every_tile_once(vis, q_tokens, heads):
     assert len(seen) == len(vis) * heads * nq
     biggest = 2 * max(len(v) for v in vis)
     assert max(load) - min(load) <= biggest + 1e-9
+
+
+def test_attention_plan_rejects_malformed_batches():
+    """bc_attention_plan is a public entry point: visible counts beyond
+    BC_MAX_VIS, bad head / token counts are contract errors, not stack
+    overwrites."""
+    import ctypes as C
+    from paper_2511_20426_b200 import _native as N
+    b = N.make_batch(3, [0], [0.0], [0], [[0]])
+    items = np.zeros(64, np.uint32)
+    start = np.zeros(257, np.uint16)
+    n_ctas = C.c_int32()
+    b.n_vis[0] = 10_000
+    assert N.lib().bc_attention_plan(C.byref(b), 128, 256, 2, items.ctypes.data, 64, start.ctypes.data,
+                                     C.byref(n_ctas)) == 1
+    b.n_vis[0] = 1
+    for q, kv, h in ((0, 256, 2), (128, 0, 2), (128, 256, 0), (128, 256, 256)):
+        assert N.lib().bc_attention_plan(C.byref(b), q, kv, h, items.ctypes.data, 64, start.ctypes.data,
+                                         C.byref(n_ctas)) == 1
