@@ -51,3 +51,26 @@ def oracle_engine(monkeypatch):
     from oracle.loop import oracle_runtime
     monkeypatch.setattr(engine, "_runtime_for", oracle_runtime)
     return engine
+
+
+def wan_oracle_outputs(cfg, weights, prompt, device_oracle=False, switches=()):
+    """Outputs of the product engine driven by the Wan oracle (numpy fp32 on
+    the host, or its torch fp32 restatement on the GPU for big geometry)
+    instead of the device runtime -- the checker for multi-rank runs."""
+    import paper_2511_20426_b200 as bc
+    from paper_2511_20426_b200 import engine
+    from oracle.loop import wan_oracle_runtime, wan_torch_oracle_runtime
+    rt = wan_torch_oracle_runtime(weights.t) if device_oracle else wan_oracle_runtime(weights.host_params())
+    orig = engine._runtime_for
+    engine._runtime_for = rt
+    try:
+        run = bc.run_cascade(bc.with_fields(cfg, workers=1), prompt, weights=weights, switches=list(switches))
+    finally:
+        engine._runtime_for = orig
+    return run.outputs
+
+
+def rel_l2(a, b):
+    a = np.asarray(a, dtype=np.float64)
+    b = np.asarray(b, dtype=np.float64)
+    return float(np.linalg.norm(a - b) / np.linalg.norm(b))

@@ -81,6 +81,13 @@ def main():
     arrays["default_cascade_causal"] = run_outputs(bc.with_fields(dflt, attention_mode="causal"), "a red cube")
     arrays["default_sequential"] = seq_outputs(dflt, "a red cube")
     arrays["default_cascade_o2"] = run_outputs(bc.with_fields(dflt, offset=2), "a red cube")
+    # every offset the reference sweeps (test_acceptance.py:42-55): batch widths 3/2/2
+    for o in (2, 3, 4):
+        if o != 2:
+            arrays[f"default_cascade_o{o}"] = run_outputs(bc.with_fields(dflt, offset=o), "a red cube")
+        arrays[f"default_causal_o{o}"] = run_outputs(bc.with_fields(dflt, offset=o, attention_mode="causal"),
+                                                     "a red cube")
+        arrays[f"tiny_cascade_o{o}"] = run_outputs(bc.with_fields(tiny, offset=o), "a red cube")
     sw = [bc.SwitchSpec("a calm meadow after the storm", "cascade", at_block=8)]
     arrays["default_cascade_switch8"] = run_outputs(dflt, "a lighthouse in a storm", switches=sw)
     # KV-recache comparison baseline and the sink refresh (both rebuild pool KV)

@@ -47,8 +47,11 @@ def test_two_processes_one_gpu(mode, shard):
     import torch.multiprocessing as mp
     import paper_2511_20426_b200 as bc
     from paper_2511_20426_b200.wan import WanWeights
+    from conftest import rel_l2, wan_oracle_outputs
     cfg = bc.wan_config("tiny", total_frames=15, attention_mode=mode)
-    base = bc.run_cascade(cfg, "a lighthouse in a storm", weights=WanWeights.random(cfg, 7))
+    w = WanWeights.random(cfg, 7)
+    base = bc.run_cascade(cfg, "a lighthouse in a storm", weights=w)
+    ref = wan_oracle_outputs(cfg, w, "a lighthouse in a storm")
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
@@ -62,3 +65,4 @@ def test_two_processes_one_gpu(mode, shard):
     assert sorted(got) == sorted(base.outputs)
     for b in base.outputs:
         assert np.array_equal(got[b], base.outputs[b]), b
+        assert rel_l2(got[b], ref[b]) < 1e-2, b   # and the two-rank run vs the fp32 oracle

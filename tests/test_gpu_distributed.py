@@ -10,7 +10,15 @@ import numpy as np
 import pytest
 import torch
 
+from conftest import rel_l2, wan_oracle_outputs
+
 pytestmark = pytest.mark.gpu
+RUN_TOL = 1e-2   # north star: final latents vs the fp32 oracle
+
+
+def _vs_oracle(run, ref):
+    for b in ref:
+        assert rel_l2(run.outputs[b], ref[b]) < RUN_TOL, b
 
 
 @pytest.fixture(scope="module")
@@ -42,11 +50,13 @@ def test_emulated_ranks_bit_identical(tiny, monkeypatch, shard, mode, push):
     cfg, w = tiny
     cfg = bc.with_fields(cfg, attention_mode=mode)
     base = bc.run_cascade(cfg, "a lighthouse in a storm", weights=w)
+    ref = wan_oracle_outputs(cfg, w, "a lighthouse in a storm")
     monkeypatch.setattr(distributed, "EMULATE", True)
     for g in (2, 3, 5, 8):
         run = bc.run_cascade(bc.with_fields(cfg, workers=g), "a lighthouse in a storm", weights=w)
         assert np.array_equal(_stack(run), _stack(base)), g
         assert run.pool.state_dump() == base.pool.state_dump()
+        _vs_oracle(run, ref)
 
 
 @pytest.mark.parametrize("shard", ["rows", "blocks"])
@@ -100,6 +110,7 @@ def test_emulated_prompt_switch(tiny, monkeypatch, shard):
     monkeypatch.setattr(distributed, "EMULATE", True)
     run = bc.run_cascade(bc.with_fields(cfg, workers=2), "first", weights=w, switches=sw)
     assert np.array_equal(_stack(run), _stack(base))
+    _vs_oracle(run, wan_oracle_outputs(cfg, w, "first", switches=sw))
 
 
 def test_emulated_rows_ragged_slices(monkeypatch):
@@ -120,6 +131,7 @@ def test_emulated_rows_ragged_slices(monkeypatch):
     assert sum(a == b for a, b in distributed.row_slices(2, 192, 7)) == 5   # 5 of 7 ranks idle
     run = bc.run_cascade(bc.with_fields(cfg, workers=7), "ragged", weights=w)
     assert np.array_equal(_stack(run), _stack(base))
+    _vs_oracle(run, wan_oracle_outputs(cfg, w, "ragged"))
 
 
 @pytest.mark.parametrize("shard", ["rows", "blocks"])
@@ -135,8 +147,11 @@ def test_emulated_full_geometry(monkeypatch, shard):
     cfg = bc.wan_config("1.3b", total_frames=15, layers=2)
     w = WanWeights.random(cfg, 5)
     base = bc.run_cascade(cfg, "full geometry", weights=w)
+    w.runtime().release_cached()
+    ref = wan_oracle_outputs(cfg, w, "full geometry", device_oracle=True)
     monkeypatch.setenv("BC_TEMPORAL_SHARD", shard)
     monkeypatch.setattr(distributed, "EMULATE", True)
     for g in (2, 8):
         run = bc.run_cascade(bc.with_fields(cfg, workers=g), "full geometry", weights=w)
         assert np.array_equal(_stack(run), _stack(base)), g
+        _vs_oracle(run, ref)

@@ -77,6 +77,20 @@ def test_toy_runs_match_reference(golden, tiny_config, default_config):
                 golden["default_cascade_switch8"]) < REL
 
 
+@pytest.mark.parametrize("o", [2, 3, 4])
+def test_toy_runs_every_offset_match_reference(golden, tiny_config, default_config, o):
+    """Device runs at offsets 2..4 (batch widths 3/2/2 -- their own graph
+    executables and attention work lists) vs the reference's outputs."""
+    import paper_2511_20426_b200 as bc
+    d = default_config
+    assert _rel(_stack(bc.run_cascade(bc.with_fields(d, offset=o), "a red cube")),
+                golden[f"default_cascade_o{o}"]) < REL
+    assert _rel(_stack(bc.run_cascade(bc.with_fields(d, offset=o, attention_mode="causal"), "a red cube")),
+                golden[f"default_causal_o{o}"]) < REL
+    assert _rel(_stack(bc.run_cascade(bc.with_fields(tiny_config, offset=o), "a red cube")),
+                golden[f"tiny_cascade_o{o}"]) < REL
+
+
 def test_toy_recache_baseline_matches_reference(golden, default_config):
     """KV-recache comparison baseline on the device (fp64) vs the
     reference's own outputs, plus the sink refresh."""

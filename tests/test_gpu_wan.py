@@ -73,7 +73,9 @@ def _stack(run):
     return np.stack([run.outputs[k] for k in sorted(run.outputs)])
 
 
-@pytest.mark.parametrize("offset,mode", [(1, "bidirectional"), (1, "causal"), (5, "bidirectional")])
+@pytest.mark.parametrize("offset,mode", [(1, "bidirectional"), (1, "causal"), (5, "bidirectional"),
+                                         (2, "bidirectional"), (3, "causal"), (4, "bidirectional"),
+                                         (2, "causal"), (3, "bidirectional"), (4, "causal")])
 def test_wan_full_run_vs_oracle(tiny, monkeypatch, offset, mode):
     import paper_2511_20426_b200 as bc
     from paper_2511_20426_b200 import engine

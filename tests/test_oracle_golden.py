@@ -136,6 +136,19 @@ def _stack(run):
     return np.stack([run.outputs[k] for k in sorted(run.outputs)])
 
 
+@pytest.mark.parametrize("o", [2, 3, 4])
+def test_engine_runs_every_offset_match_reference(oracle_engine, golden, tiny_config, default_config, o):
+    """Offsets 2..4 (batch widths 3/2/2; reference test_acceptance.py:42-55)."""
+    from paper_2511_20426_b200 import run_cascade, with_fields
+    d = default_config
+    assert np.array_equal(_stack(run_cascade(with_fields(d, offset=o), "a red cube")),
+                          golden[f"default_cascade_o{o}"])
+    assert np.array_equal(_stack(run_cascade(with_fields(d, offset=o, attention_mode="causal"), "a red cube")),
+                          golden[f"default_causal_o{o}"])
+    assert np.array_equal(_stack(run_cascade(with_fields(tiny_config, offset=o), "a red cube")),
+                          golden[f"tiny_cascade_o{o}"])
+
+
 def test_engine_runs_match_reference(oracle_engine, golden, tiny_config, default_config):
     from paper_2511_20426_b200 import SwitchSpec, run_cascade, run_sequential_reference, with_fields
     assert np.array_equal(_stack(run_cascade(tiny_config, "a red cube")), golden["tiny_cascade_bidir"])
