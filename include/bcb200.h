@@ -267,6 +267,74 @@ int bc_attention_paged(const void* q, const void* k_arena, const void* v_arena,
                        const bc_batch* batch, int32_t q_per_entry, int32_t heads,
                        void* out, void* stream);
 
+
+/* ---------------------------------------------------------------------------
+ * VAE decode.  Replaces the reference's decode lane
+ * (engine.py:151-158, a cost-model charge) and its linear stand-in
+ * decode_block / make_decode_map (executor.py:189-212) with the public
+ * Wan2.1 causal 3-D VAE decoder.  Activations are "padded frames":
+ * channels-last [n_frames][H+2][W+2][C] with a zero border; frames 0-1 of a
+ * causal conv input hold its history (the previous block's last two input
+ * frames, zeros before the first block).  Host orchestration:
+ * paper_2511_20426_b200/vae.py.
+ * ------------------------------------------------------------------------- */
+#define BC_VAE_MAX_FRAMES 16
+
+typedef struct {
+  const void* in;      /* bf16 padded frames [n_frames][H+2][W+2][cin]          */
+  const void* w;       /* bf16 [cout][kt*kh*kw][cin] (tap-major, K-contiguous)  */
+  const float* bias;   /* fp32 [cout]                                           */
+  int32_t H, W;        /* valid extent                                          */
+  int32_t n_frames;    /* frames in the input / output buffers                  */
+  int32_t frame0;      /* first output frame (>= kt-1: causal taps read frame0-2..frame0) */
+  int32_t n_out_frames;
+  int32_t cin, cout;   /* cin % 32 == 0, cout % 16 == 0                         */
+  int32_t kt, kh, kw;  /* 3x3x3, 1x3x3, 3x1x1 or 1x1x1                           */
+  const float* res;    /* optional fp32 residual, same layout as out32          */
+  float* out32;        /* optional fp32 y = conv + bias (+ res), padded frames  */
+  void* out16;         /* optional bf16 y                                       */
+  void* act;           /* optional bf16 silu?(RMS_norm(y) * gamma): the next conv's input */
+  const float* gamma;  /* fp32 [cout] for act                                   */
+  int32_t act_silu;    /* 1: silu(norm), 0: norm only (attention block input)   */
+  float* video;        /* optional fp32 [frames][video_channels][H][W], clamped to [-1,1] */
+  int32_t video_channels, video_frame0;
+} bc_vae_conv_args;
+
+/* Output frame j of an upsample reads source (src[j] ? b : a) frame frame[j]
+ * at channel offset chan[j] (b has 2C channels: the time conv's two halves). */
+typedef struct {
+  int32_t src[BC_VAE_MAX_FRAMES];
+  int32_t frame[BC_VAE_MAX_FRAMES];
+  int32_t chan[BC_VAE_MAX_FRAMES];
+} bc_vae_frame_map;
+
+/* Causal conv as a tcgen05 implicit GEMM with fused bias / residual / RMS
+ * norm + SiLU / clamp epilogues (CausalConv3d, Conv2d of Resample, the 1x1
+ * shortcut and to_qkv of the Wan2.1 decoder). */
+int bc_vae_conv(const bc_vae_conv_args* args /*[host]*/, void* stream);
+/* z [T][zc][H][W] fp32 -> z*std+mean -> 1x1x1 conv (WanVAE_.conv2) -> bf16
+ * padded frames [frame0+t] with cpad channels (zc..cpad-1 left as they are). */
+int bc_vae_prep(const float* z, const float* w2, const float* b2, const float* mean, const float* stdv,
+                void* out, int32_t T, int32_t zc, int32_t H, int32_t W, int32_t frame0, int32_t cpad,
+                void* stream);
+/* nearest-exact x2 (Resample) of fp32 padded frames into bf16 padded frames
+ * [out_frame0 + j] of the next level (2H x 2W). */
+int bc_vae_upsample(const float* a, const float* b, const bc_vae_frame_map* map /*[host]*/, int32_t C,
+                    int32_t H, int32_t W, void* out, int32_t out_frame0, int32_t n_out, void* stream);
+/* AttentionBlock helpers (one frame): q, k [np][C], v^T [C][np] from the
+ * padded qkv rows; row softmax of S [rows][np] over n_valid columns; and the
+ * residual x += proj followed by the next conv's silu(RMS_norm(x) * gamma). */
+int bc_vae_attn_gather(const void* qkv, int32_t frame, int32_t H, int32_t W, int32_t C, int32_t np,
+                       void* q, void* k, void* vt, void* stream);
+int bc_vae_softmax(const float* S, void* P, int32_t rows, int32_t np, int32_t n_valid, float scale,
+                   void* stream);
+/* silu?(RMS_norm(x) * gamma) of fp32 padded frames [frame0, frame0+n) into
+ * bf16 -- the next conv's input when a conv's rows do not fit one unit. */
+int bc_vae_norm_act(const float* x, const float* gamma, void* act, int32_t frame0, int32_t n_frames,
+                    int32_t H, int32_t W, int32_t C, int32_t use_silu, void* stream);
+int bc_vae_attn_out(float* x, const float* proj, const float* gamma, void* act, int32_t frame, int32_t H,
+                    int32_t W, int32_t C, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

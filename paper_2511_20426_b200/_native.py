@@ -89,6 +89,23 @@ class WanDist(C.Structure):
                 ("stage", C.c_int32), ("layer", C.c_int32), ("row0", C.c_int32), ("row1", C.c_int32)]
 
 
+class VaeConvArgs(C.Structure):
+    _fields_ = [("in_", C.c_void_p), ("w", C.c_void_p), ("bias", C.c_void_p)] + \
+               [(n, C.c_int32) for n in ("H", "W", "n_frames", "frame0", "n_out_frames", "cin", "cout",
+                                         "kt", "kh", "kw")] + \
+               [(n, C.c_void_p) for n in ("res", "out32", "out16", "act", "gamma")] + \
+               [("act_silu", C.c_int32), ("video", C.c_void_p), ("video_channels", C.c_int32),
+                ("video_frame0", C.c_int32)]
+
+
+VAE_MAX_FRAMES = 16
+
+
+class VaeFrameMap(C.Structure):
+    _fields_ = [("src", C.c_int32 * VAE_MAX_FRAMES), ("frame", C.c_int32 * VAE_MAX_FRAMES),
+                ("chan", C.c_int32 * VAE_MAX_FRAMES)]
+
+
 _SIGS = {
     "bc_last_error": (C.c_char_p, []),
     "bc_version": (C.c_char_p, []),
@@ -130,6 +147,17 @@ _SIGS = {
     "bc_ipc_close": (C.c_int, [C.c_void_p]),
     "bc_free": (C.c_int, [C.c_void_p]),
     "bc_memset_async": (C.c_int, [C.c_void_p, C.c_int, C.c_int64, C.c_void_p]),
+    "bc_vae_conv": (C.c_int, [C.POINTER(VaeConvArgs), C.c_void_p]),
+    "bc_vae_prep": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+                    + [C.c_int32] * 6 + [C.c_void_p]),
+    "bc_vae_upsample": (C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(VaeFrameMap), C.c_int32, C.c_int32,
+                                  C.c_int32, C.c_void_p, C.c_int32, C.c_int32, C.c_void_p]),
+    "bc_vae_attn_gather": (C.c_int, [C.c_void_p] + [C.c_int32] * 5 + [C.c_void_p] * 4),
+    "bc_vae_softmax": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_float,
+                                 C.c_void_p]),
+    "bc_vae_norm_act": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p] + [C.c_int32] * 6 + [C.c_void_p]),
+    "bc_vae_attn_out": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p] + [C.c_int32] * 4
+                        + [C.c_void_p]),
     "bc_profile_enable": (C.c_int, [C.c_int]),
     "bc_profile_collect": (C.c_int, [C.POINTER(C.c_double), C.POINTER(C.c_double),
                                      C.POINTER(C.c_double), C.POINTER(C.c_int64), C.c_int]),

@@ -31,6 +31,9 @@ struct GemmArgs {
 int gemm_run(const GemmArgs& g, cudaStream_t st);
 int make_tmap_2d(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer,
                  uint64_t row_stride_bytes, uint32_t box_inner, uint32_t box_outer);
+// the same with a 128 / 64 / 32-byte (or 0 = no) swizzle
+int make_tmap_2d_swz(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer,
+                     uint64_t row_stride_bytes, uint32_t box_inner, uint32_t box_outer, int swizzle_bytes);
 int num_sms();
 
 }  // namespace bc
