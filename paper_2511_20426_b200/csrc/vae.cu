@@ -35,6 +35,7 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "bc_common.h"
 #include "gemm.h"
@@ -43,7 +44,7 @@
 namespace bc {
 namespace {
 
-constexpr int kConvThreads = 192;  // TMA warp, MMA warp, 4 epilogue warps
+constexpr int kConvThreads = 320;  // TMA warp, MMA warp, 8 epilogue warps
 
 template <int CK, int R, int NMAX>
 struct ConvCfg {
@@ -56,9 +57,10 @@ struct ConvCfg {
   static constexpr int kSB = kSB0 < 2 ? 2 : kSB0 > 8 ? 8 : kSB0;
   static constexpr int kSA0 = (kBudget - kSB * kBBytes) / kABytes;
   static constexpr int kSA = kSA0 < 2 ? 2 : kSA0 > 4 ? 4 : kSA0;
-  static constexpr int kCols = R * NMAX;
+  static constexpr int kAcc = 2 * R * NMAX <= 512 ? 2 : 1;  // double-buffered accumulators when they fit
+  static constexpr int kCols = kAcc * R * NMAX;
   static constexpr int kTmemCols = kCols <= 32 ? 32 : kCols <= 64 ? 64 : kCols <= 128 ? 128 : kCols <= 256 ? 256 : 512;
-  static constexpr size_t kSmem = 1024 + (size_t)kSA * kABytes + (size_t)kSB * kBBytes + 512;
+  static constexpr size_t kSmem = 1024 + (size_t)kSA * kABytes + (size_t)kSB * kBBytes + 512 + 1024;
   static_assert(kCols <= 512, "TMEM holds 512 fp32 columns");
   static_assert(kSmem <= 227 * 1024, "shared memory");
 };
@@ -99,7 +101,28 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16
       : "memory");
 }
 
-__device__ __forceinline__ float silu(float a) { return a / (1.0f + __expf(-a)); }
+__device__ __forceinline__ float silu(float a) { return a * __frcp_rn(1.0f + __expf(-a)); }
+// 256-bit global accesses (sm_100: one full 32-byte sector per lane)
+__device__ __forceinline__ void ld8f(const float* p, float (&r)[8]) {
+  asm volatile("ld.global.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=f"(r[0]), "=f"(r[1]), "=f"(r[2]), "=f"(r[3]), "=f"(r[4]), "=f"(r[5]), "=f"(r[6]), "=f"(r[7])
+               : "l"(p));
+}
+__device__ __forceinline__ void st8f(float* p, const float* r) {
+  asm volatile("st.global.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "f"(r[0]), "f"(r[1]), "f"(r[2]),
+               "f"(r[3]), "f"(r[4]), "f"(r[5]), "f"(r[6]), "f"(r[7])
+               : "memory");
+}
+__device__ __forceinline__ void st8bf16x2(void* p, const float* r) {  // 16 floats -> 16 bf16 (32 B)
+  asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(pack_bf16(r[0], r[1])),
+               "r"(pack_bf16(r[2], r[3])), "r"(pack_bf16(r[4], r[5])), "r"(pack_bf16(r[6], r[7])),
+               "r"(pack_bf16(r[8], r[9])), "r"(pack_bf16(r[10], r[11])), "r"(pack_bf16(r[12], r[13])),
+               "r"(pack_bf16(r[14], r[15]))
+               : "memory");
+}
+__device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t threads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
+}
 
 template <int CK, int R, int NMAX>
 __global__ void __launch_bounds__(kConvThreads, 1)
@@ -116,8 +139,9 @@ __global__ void __launch_bounds__(kConvThreads, 1)
   uint64_t* bfull = aempty + SA;
   uint64_t* bempty = bfull + SB;
   uint64_t* tfull = bempty + SB;
-  uint64_t* tempty = tfull + 1;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 1);
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  float* ss_part = reinterpret_cast<float*>(smem + SA * Cfg::kABytes + SB * Cfg::kBBytes + 512);  // [4][2][32]
 
   const uint32_t warp = warp_id();
   const int n_units = p.num_mg * p.num_ng;
@@ -133,8 +157,10 @@ __global__ void __launch_bounds__(kConvThreads, 1)
       mbar_init(&bfull[i], 1);
       mbar_init(&bempty[i], 1);
     }
-    mbar_init(tfull, 1);
-    mbar_init(tempty, 128);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&tfull[i], 1);
+      mbar_init(&tempty[i], 256);
+    }
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc<Cfg::kTmemCols>(tmem_slot);
@@ -184,7 +210,10 @@ __global__ void __launch_bounds__(kConvThreads, 1)
     int ia = 0, ib = 0, it = 0;
     uint32_t pa = 0, pb = 0;
     for (int unit = blockIdx.x; unit < n_units; unit += gridDim.x, ++it) {
-      mbar_wait(tempty, (it & 1) ^ 1);
+      const int acc = Cfg::kAcc == 2 ? (it & 1) : 0;
+      const uint32_t acc_phase = Cfg::kAcc == 2 ? ((it >> 1) & 1) : (it & 1);
+      const uint32_t d_base = tmem_base + acc * (R * NMAX);
+      mbar_wait(&tempty[acc], acc_phase ^ 1);
       tc_fence_after();
       for (int s = 0; s < stages; ++s) {
         mbar_wait(&afull[ia], pa);
@@ -199,11 +228,11 @@ __global__ void __launch_bounds__(kConvThreads, 1)
             for (int r = 0; r < R; ++r)
 #pragma unroll
               for (int k = 0; k < CK / 16; ++k)
-                mma_bf16_ss(tmem_base + r * NMAX, desc_swz(a0 + (r * 128 + kw) * RB + k * 32, RB),
+                mma_bf16_ss(d_base + r * NMAX, desc_swz(a0 + (r * 128 + kw) * RB + k * 32, RB),
                             desc_swz(b0 + k * 32, RB), idesc, (s | kw | k) != 0);
             mma_commit(&bempty[ib]);
             if (kw == p.kw - 1) mma_commit(&aempty[ia]);
-            if (kw == p.kw - 1 && s == stages - 1) mma_commit(tfull);
+            if (kw == p.kw - 1 && s == stages - 1) mma_commit(&tfull[acc]);
           }
           __syncwarp();
           if (++ib == SB) {
@@ -218,14 +247,26 @@ __global__ void __launch_bounds__(kConvThreads, 1)
       }
     }
   } else {
+    // 8 epilogue warps: two per TMEM lane quadrant, interleaved 16-column
+    // chunks (even chunks to the first, odd to the second).  A row's
+    // residual loads are all issued before its first TMEM load; the fused
+    // norm's sum of squares is combined across the pair through shared
+    // memory and a 64-thread named barrier per quadrant.
+    constexpr int kMaxMine = (NMAX / 16 + 1) / 2;  // chunks per warp of the pair
     const uint32_t quad = warp & 3;
+    const int half = ((int)warp - 2) >> 2;
+    const int n_chunks = p.ncol / 16;
+    const int mine = (n_chunks - half + 1) / 2;
     const int row_end = p.row0 + p.rows;
     const float norm_scale = sqrtf((float)p.cout);
+    float* ssx = ss_part + quad * 64;
     int it = 0;
     for (int unit = blockIdx.x; unit < n_units; unit += gridDim.x, ++it) {
       const int mg = unit / p.num_ng, ng = unit - mg * p.num_ng;
       const int o0 = p.row0 + mg * R * 128, n0 = ng * p.ncol;
-      mbar_wait(tfull, it & 1);
+      const int acc = Cfg::kAcc == 2 ? (it & 1) : 0;
+      const uint32_t acc_phase = Cfg::kAcc == 2 ? ((it >> 1) & 1) : (it & 1);
+      mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
 #pragma unroll 1
       for (int r = 0; r < R; ++r) {
@@ -234,90 +275,86 @@ __global__ void __launch_bounds__(kConvThreads, 1)
         const int rem = row - f * p.F;
         const int yy = rem / p.Wp, xx = rem - (rem / p.Wp) * p.Wp;
         const bool valid = row < row_end && yy >= 1 && yy <= p.H && xx >= 1 && xx <= p.W;
-        const uint32_t taddr = tmem_base + ((quad * 32) << 16) + r * NMAX;
-        float ss = 0.f;
-#pragma unroll 1
-        for (int c = 0; c < p.ncol; c += 16) {
-          uint32_t v[16];
-          tmem_ld16(taddr + c, v);
-          tmem_ld_wait();
-          float y[16];
+        const uint32_t taddr = tmem_base + ((quad * 32) << 16) + (acc * R + r) * NMAX;
+        // residual loads run kPre chunks ahead of their use (rolling buffer)
+        constexpr int kPre = kMaxMine <= 3 ? kMaxMine : 2;
+        float rq[kPre][16];
+        const bool do_res = p.res && valid;
+        auto load_res = [&](int i) {
+          const float* src = p.res + (size_t)row * p.cout + n0 + (2 * i + half) * 16;
+          float t0[8], t1[8];
+          ld8f(src, t0);
+          ld8f(src + 8, t1);
 #pragma unroll
-          for (int j = 0; j < 16; ++j) y[j] = __uint_as_float(v[j]) + __ldg(p.bias + n0 + c + j);
-          const size_t off = (size_t)row * p.cout + n0 + c;
-          if (valid) {
-            if (p.res) {
-#pragma unroll
-              for (int j = 0; j < 16; j += 4) {
-                const float4 q = *reinterpret_cast<const float4*>(p.res + off + j);
-                y[j] += q.x;
-                y[j + 1] += q.y;
-                y[j + 2] += q.z;
-                y[j + 3] += q.w;
-              }
-            }
-            if (p.out32) {
-#pragma unroll
-              for (int j = 0; j < 16; j += 4)
-                *reinterpret_cast<float4*>(p.out32 + off + j) = make_float4(y[j], y[j + 1], y[j + 2], y[j + 3]);
-            }
-            if (p.out16) {
-              uint4 a, b;
-              a.x = pack_bf16(y[0], y[1]); a.y = pack_bf16(y[2], y[3]);
-              a.z = pack_bf16(y[4], y[5]); a.w = pack_bf16(y[6], y[7]);
-              b.x = pack_bf16(y[8], y[9]); b.y = pack_bf16(y[10], y[11]);
-              b.z = pack_bf16(y[12], y[13]); b.w = pack_bf16(y[14], y[15]);
-              *reinterpret_cast<uint4*>(p.out16 + off) = a;
-              *reinterpret_cast<uint4*>(p.out16 + off + 8) = b;
-            }
-            if (p.video && c == 0) {
-              const int vf = f - p.row0 / p.F + p.video_frame0;
-#pragma unroll
-              for (int j = 0; j < 16; ++j)
-                if (j < p.video_ch)
-                  p.video[(((size_t)vf * p.video_ch + j) * p.H + (yy - 1)) * p.W + (xx - 1)] =
-                      fminf(1.0f, fmaxf(-1.0f, y[j]));
-            }
+          for (int j = 0; j < 8; ++j) {
+            rq[i % kPre][j] = t0[j];
+            rq[i % kPre][8 + j] = t1[j];
           }
-          if (p.act) {
-            uint32_t w[16];
+        };
+        if (do_res) {
 #pragma unroll
-            for (int j = 0; j < 16; ++j) {
-              ss = fmaf(y[j], y[j], ss);
-              w[j] = __float_as_uint(y[j]);
-            }
-            tmem_st16(taddr + c, w);
-          }
+          for (int i = 0; i < kPre; ++i)
+            if (i < mine) load_res(i);
         }
-        if (p.act) {
-          tmem_st_wait();
-          const float inv = norm_scale / fmaxf(sqrtf(ss), 1e-12f);
-#pragma unroll 1
-          for (int c = 0; c < p.ncol; c += 16) {
+        float y[kMaxMine][16];
+        float ss = 0.f;
+#pragma unroll
+        for (int i = 0; i < kMaxMine; ++i) {
+          if (i < mine) {
+            const int c = (2 * i + half) * 16;
             uint32_t v[16];
             tmem_ld16(taddr + c, v);
             tmem_ld_wait();
-            float a[16];
 #pragma unroll
-            for (int j = 0; j < 16; ++j) {
-              a[j] = __uint_as_float(v[j]) * inv * __ldg(p.gamma + n0 + c + j);
-              if (p.act_silu) a[j] = silu(a[j]);
+            for (int j = 0; j < 16; ++j) y[i][j] = __uint_as_float(v[j]) + __ldg(p.bias + n0 + c + j);
+            const size_t off = (size_t)row * p.cout + n0 + c;
+            if (do_res) {
+#pragma unroll
+              for (int j = 0; j < 16; ++j) y[i][j] += rq[i % kPre][j];
+              if (i + kPre < mine) load_res(i + kPre);
             }
             if (valid) {
-              const size_t off = (size_t)row * p.cout + n0 + c;
-              uint4 u, w;
-              u.x = pack_bf16(a[0], a[1]); u.y = pack_bf16(a[2], a[3]);
-              u.z = pack_bf16(a[4], a[5]); u.w = pack_bf16(a[6], a[7]);
-              w.x = pack_bf16(a[8], a[9]); w.y = pack_bf16(a[10], a[11]);
-              w.z = pack_bf16(a[12], a[13]); w.w = pack_bf16(a[14], a[15]);
-              *reinterpret_cast<uint4*>(p.act + off) = u;
-              *reinterpret_cast<uint4*>(p.act + off + 8) = w;
+              if (p.out32) {
+                st8f(p.out32 + off, &y[i][0]);
+                st8f(p.out32 + off + 8, &y[i][8]);
+              }
+              if (p.out16) st8bf16x2(p.out16 + off, &y[i][0]);
+              if (p.video && c == 0) {
+                const int vf = f - p.row0 / p.F + p.video_frame0;
+#pragma unroll
+                for (int j = 0; j < 16; ++j)
+                  if (j < p.video_ch)
+                    p.video[(((size_t)vf * p.video_ch + j) * p.H + (yy - 1)) * p.W + (xx - 1)] =
+                        fminf(1.0f, fmaxf(-1.0f, y[i][j]));
+              }
+            }
+#pragma unroll
+            for (int j = 0; j < 16; ++j) ss = fmaf(y[i][j], y[i][j], ss);
+          }
+        }
+        if (p.act) {
+          ssx[half * 32 + lane_id()] = ss;
+          named_bar_sync(1 + quad, 64);
+          const float tot = ssx[lane_id()] + ssx[32 + lane_id()];
+          named_bar_sync(1 + quad, 64);       // both read before the next row writes
+          const float inv = norm_scale / fmaxf(sqrtf(tot), 1e-12f);
+#pragma unroll
+          for (int i = 0; i < kMaxMine; ++i) {
+            if (i < mine) {
+              const int c = (2 * i + half) * 16;
+              float a[16];
+#pragma unroll
+              for (int j = 0; j < 16; ++j) {
+                a[j] = y[i][j] * inv * __ldg(p.gamma + n0 + c + j);
+                if (p.act_silu) a[j] = silu(a[j]);
+              }
+              if (valid) st8bf16x2(p.act + (size_t)row * p.cout + n0 + c, a);
             }
           }
         }
       }
       tc_fence_before();
-      mbar_arrive(tempty);
+      mbar_arrive(&tempty[acc]);
     }
   }
   tc_fence_before();
@@ -578,9 +615,21 @@ extern "C" int bc_vae_conv(const bc_vae_conv_args* a, void* stream) {
     if (a->cout % ncol) return bc_fail(BC_ERR_CONTRACT, "vae_conv: cout %d has no tile width", a->cout);
     if ((a->act || a->video) && ncol != a->cout)
       return bc_fail(BC_ERR_CONTRACT, "vae_conv: fused norm needs the whole row in one unit (cout %d)", a->cout);
+    // a unit holding a whole 192-channel row with a fused norm: one row tile,
+    // double-buffered accumulators (the epilogue overlaps the next mainloop)
+    static const int r1 = [] {
+      const char* e = getenv("BC_VAE_R1");
+      return e ? atoi(e) : 1;
+    }();
+    if (r1 && a->cin % 64 == 0 && ncol == a->cout && a->act) return conv_launch<64, 1, 192>(*a, ncol, st);
     return a->cin % 64 == 0 ? conv_launch<64, 2, 192>(*a, ncol, st) : conv_launch<32, 2, 192>(*a, ncol, st);
   }
-  return conv_launch<32, 4, 96>(*a, a->cout, st);
+  static const int r4 = [] {
+    const char* e = getenv("BC_VAE_R4");
+    return e ? atoi(e) : 0;
+  }();
+  if (r4) return conv_launch<32, 4, 96>(*a, a->cout, st);
+  return conv_launch<32, 2, 96>(*a, a->cout, st);
 }
 
 extern "C" int bc_vae_prep(const float* z, const float* w2, const float* b2, const float* mean, const float* stdv,
