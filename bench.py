@@ -552,6 +552,57 @@ def sub_line(C, bc, name, cfg, weights, args, switches=(), seq=False, cpu_pts=No
     return line
 
 
+def vae_report(C, bc, cfg, weights, feed, peaks):
+    """VAE decode, timed separately as the north star asks:
+    (a) the decoder alone on steady-state blocks (3 latent -> 12 video frames
+    at 480x832), CUDA events on its stream; (b) the cascade and the sequential
+    rollout with the decode lane on (each emitted block decoded on a side
+    stream of the same GPU, overlapping the following iterations): frames
+    over the time the LAST block finished decoding, and the paper's
+    decode-inclusive streaming FPS."""
+    import torch
+    from paper_2511_20426_b200.metrics import end_to_end_fps, streaming_fps
+    from paper_2511_20426_b200.vae import VaeDecoder, VaeWeights, vae_config
+    vcfg = vae_config("wan2.1", latent_h=cfg.latent_height, latent_w=cfg.latent_width,
+                      block_size=cfg.block_size)
+    dec = VaeDecoder(VaeWeights.random(vcfg, 11))
+    g = torch.Generator(device="cuda")
+    g.manual_seed(5)
+    zs = [torch.randn((cfg.block_size, 16, cfg.latent_height, cfg.latent_width), generator=g, device="cuda")
+          for _ in range(6)]
+    dec.reset()
+    dec.decode_block(zs[0])
+    dec.decode_block(zs[1])
+    torch.cuda.synchronize()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    ev[0].record(dec.stream)
+    for z in zs[2:]:
+        dec.decode_block(z)
+    ev[1].record(dec.stream)
+    torch.cuda.synchronize()
+    ms = ev[0].elapsed_time(ev[1]) / (len(zs) - 2)
+    fl = dec.flops_per_block(False)
+    peak = peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops"))
+    out = {"decoder": "Wan2.1 causal 3-D VAE decoder (random init), 16 latent ch -> RGB, x8 space, x4 time",
+           "ms_per_block": round(ms, 3), "video_frames_per_block": vcfg.frames_out(cfg.block_size, False),
+           "decode_fps_alone": round(vcfg.frames_out(cfg.block_size, False) / ms * 1e3, 2),
+           "tflop_per_block": round(fl / 1e12, 3), "tflops": round(fl / ms / 1e9, 1),
+           "roofline_frac": round(fl / ms / 1e9 / peak, 4) if peak else None,
+           "buffers_gb": round(dec.nbytes() / 1e9, 2)}
+    for name, fn in (("cascade", bc.run_cascade), ("sequential", bc.run_sequential_reference)):
+        c = cfg if name == "cascade" else bc.with_fields(cfg, offset=cfg.passes)
+        fn(c, PROMPT, session_seed=SESSION_SEED, weights=weights, noise_feed=feed, decoder=dec)
+        r = fn(c, PROMPT, session_seed=SESSION_SEED, weights=weights, noise_feed=feed, decoder=dec)
+        out[f"{name}_with_decode"] = {
+            "e2e_fps_decoded": round(end_to_end_fps(r.trace, clock="decoded"), 3),
+            "streaming_fps_decoded": round(streaming_fps(r.trace, clock="decoded"), 3),
+            "e2e_fps_generation_same_run": round(end_to_end_fps(r.trace), 3),
+            "decode_lane": "same GPU, side stream, overlapped with the following iterations"}
+    del dec
+    torch.cuda.empty_cache()
+    return out
+
+
 def run_ours(args, cfg):
     import torch
     import paper_2511_20426_b200 as bc
@@ -597,6 +648,11 @@ def run_ours(args, cfg):
                             "fps_next_block": round(nxt.emitted_video_frames /
                                                     (nxt.wall_clock - prev), 2),
                             "e2e_fps": end_to_end_fps(r.trace)}
+
+    # ---- VAE decode, timed separately ----
+    vae = None
+    if world == 1 and not args.no_vae:
+        vae = vae_report(C, bc, cfg, weights, feed, _peaks()[0])
 
     # ---- the reference's own CPU-runnable case (BASELINE configs[0]) ----
     toy = noise = cpu = None
@@ -665,6 +721,7 @@ def run_ours(args, cfg):
                                      "streaming": cas["streaming_fps"] / seq["streaming_fps"]}
                                     if seq else None),
         "prompt_switch": switch,
+        "vae_decode": vae,
         "config1_toy": toy,
         "noise_generation": noise,
         "roofline": roof,
@@ -706,6 +763,7 @@ def main():
     ap.add_argument("--switch-every", type=int, default=0,
                     help="cascade-mode prompt switch every N blocks")
     ap.add_argument("--no-seq", action="store_true", help="skip the sequential rollout")
+    ap.add_argument("--no-vae", action="store_true", help="skip the VAE decode measurements")
     ap.add_argument("--no-switch", action="store_true",
                     help="skip the cascade-vs-recache prompt-switch measurement")
     ap.add_argument("--no-sub", action="store_true",

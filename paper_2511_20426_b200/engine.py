@@ -49,6 +49,7 @@ class RunResult:
     pool: KVPool
     emitted_order: list
     switch_events: list = field(default_factory=list)
+    videos: dict = field(default_factory=dict)     # block -> decoded frames (device), with a decoder
 
     @property
     def iterations(self) -> int:
@@ -101,6 +102,52 @@ class _Session:
         self.session.close()
 
 
+class _DecodeLane:
+    """The reference's decode lane (``engine.py:151-158``: a cost-model charge,
+    overlapped on a second worker with ``decode_overlap``) made real: every
+    emitted block's x0 is decoded to video frames by a device VAE
+    (:class:`~paper_2511_20426_b200.vae.VaeDecoder`) on its own stream, so
+    decoding block b overlaps the denoising iterations that follow.  The
+    trace's ``decode_start`` / ``decode_done`` get CUDA-event times on the
+    same origin as ``wall_clock`` (``metrics.streaming_fps(trace,
+    clock="decoded")`` is the paper's decode-inclusive streaming FPS,
+    ``PAPER.md:246``)."""
+
+    def __init__(self, decoder, dev, config):
+        if config.model != "wan":
+            raise InvalidInputError("VAE decode needs the Wan-shaped model (latents (S, 16, h, w))",
+                                    fields=["model"])
+        dc = decoder.cfg
+        if (dc.block_size, dc.z_dim, dc.latent_h, dc.latent_w) != (
+                config.block_size, config.latent_channels, config.latent_height, config.latent_width):
+            raise InvalidInputError("VAE geometry does not match the run's latents", fields=["decoder"])
+        import torch
+        self.torch = torch
+        self.decoder, self.dev = decoder, dev
+        self.videos, self.marks = {}, []
+        decoder.reset()
+
+    def emit(self, block, event):
+        torch = self.torch
+        z = self.dev.emitted_device(block)
+        st = self.decoder.stream
+        st.wait_stream(torch.cuda.current_stream())
+        z.record_stream(st)                     # the session may free it before the decode ran
+        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s0.record(st)
+        self.videos[block] = self.decoder.decode_block(z)
+        s1.record(st)
+        self.marks.append((event, s0, s1))
+
+    def finish(self):
+        self.decoder.stream.synchronize()
+        origin = self.dev.events[0]
+        for ev, s0, s1 in self.marks:
+            ev.decode_start = origin.elapsed_time(s0) / 1e3
+            ev.decode_done = origin.elapsed_time(s1) / 1e3
+        self.marks.clear()
+
+
 def _collect_outputs(dev, blocks) -> dict:
     """Emitted blocks as host arrays; multi-GPU sessions gather them from
     their owner ranks."""
@@ -134,8 +181,10 @@ def run_cascade(config: CascadeConfig, prompt: str,
                 weight_seed: int = DEFAULT_WEIGHT_SEED,
                 switches=(), command_queue: CommandQueue | None = None,
                 event_sink=None, weights=None, pace_seconds: float = 0.0,
-                noise_feed=None) -> RunResult:
-    """Plan / execute / apply until every block has retired (Alg. 1)."""
+                noise_feed=None, decoder=None) -> RunResult:
+    """Plan / execute / apply until every block has retired (Alg. 1).
+    ``decoder`` (a :class:`~paper_2511_20426_b200.vae.VaeDecoder`, optional):
+    decode each emitted block on the device, overlapped (``_DecodeLane``)."""
     config.validate()
     if config.decode_overlap and config.workers < 2:
         raise InvalidInputError("decode overlap needs at least 2 workers",
@@ -153,6 +202,7 @@ def run_cascade(config: CascadeConfig, prompt: str,
                         "weight_seed": weight_seed, "config": config.to_dict()})
     sess = _Session(config, weights, cond, session_seed, noise_feed)
     dev = sess.session
+    lane = _DecodeLane(decoder, dev, config) if decoder is not None else None
     switch_events = []
     modeled = 0.0
     decode_done_at = 0.0
@@ -254,6 +304,8 @@ def run_cascade(config: CascadeConfig, prompt: str,
                 decode_start=dec_start, decode_done=dec_done, switch=record)
             trace.append(event)
             pending.append(event)
+            if lane is not None and emitted_block is not None:
+                lane.emit(emitted_block, event)
             if event_sink is not None:
                 dev.fill_wall_times(pending)
                 pending.clear()
@@ -262,6 +314,8 @@ def run_cascade(config: CascadeConfig, prompt: str,
             if pace_seconds > 0.0:
                 time.sleep(pace_seconds)
         dev.fill_wall_times(pending)
+        if lane is not None:
+            lane.finish()
         outputs = _collect_outputs(dev, state.emitted)
     finally:
         sess.close()
@@ -272,13 +326,14 @@ def run_cascade(config: CascadeConfig, prompt: str,
             f"run finished with outputs for {sorted(outputs)}; expected all of "
             f"0..{config.num_blocks - 1}")
     return RunResult(outputs=outputs, trace=trace, pool=pool,
-                     emitted_order=list(state.emitted), switch_events=switch_events)
+                     emitted_order=list(state.emitted), switch_events=switch_events,
+                     videos=lane.videos if lane is not None else {})
 
 
 def run_sequential_reference(config: CascadeConfig, prompt: str,
                              session_seed: int = DEFAULT_SESSION_SEED,
                              weight_seed: int = DEFAULT_WEIGHT_SEED,
-                             weights=None, noise_feed=None) -> RunResult:
+                             weights=None, noise_feed=None, decoder=None) -> RunResult:
     """Plain block-causal rollout: every block runs all its passes against
     its predecessors' cached KV before the next block starts.  Written as
     nested loops over (block, pass), independent of the state machine, so
@@ -296,6 +351,7 @@ def run_sequential_reference(config: CascadeConfig, prompt: str,
                         "config": config.to_dict()})
     sess = _Session(config, weights, cond, session_seed, noise_feed)
     dev = sess.session
+    lane = _DecodeLane(decoder, dev, config) if decoder is not None else None
     emitted_order = []
     modeled = 0.0
     it = 0
@@ -338,9 +394,14 @@ def run_sequential_reference(config: CascadeConfig, prompt: str,
                     emitted_block=emitted_block,
                     emitted_video_frames=(S * config.video_frames_per_latent
                                           if emitted_block is not None else None)))
+                if lane is not None and emitted_block is not None:
+                    lane.emit(emitted_block, trace.events[-1])
                 it += 1
         dev.fill_wall_times(trace.events)
+        if lane is not None:
+            lane.finish()
         outputs = _collect_outputs(dev, emitted_order)
     finally:
         sess.close()
-    return RunResult(outputs=outputs, trace=trace, pool=pool, emitted_order=emitted_order)
+    return RunResult(outputs=outputs, trace=trace, pool=pool, emitted_order=emitted_order,
+                     videos=lane.videos if lane is not None else {})

@@ -30,3 +30,6 @@ def test_bench_line(gpus):
     assert d["sequential"]["value"] > 0
     if gpus > 1:
         assert "shard=" in d["config"]["parallelism"]
+    else:
+        v = d["vae_decode"]
+        assert v["ms_per_block"] > 0 and v["cascade_with_decode"]["e2e_fps_decoded"] > 0

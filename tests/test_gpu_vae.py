@@ -199,3 +199,45 @@ def test_vae_decode_reset_restarts_stream():
 def test_vae_decode_wan_geometry():
     from paper_2511_20426_b200.vae import vae_config
     _decode_vs_oracle(vae_config("wan2.1"), 2, 33, VIDEO_TOL, "decode_wan2.1_480x832_rel_l2_per_block")
+
+
+def test_vae_decode_lane_in_run_cascade():
+    """run_cascade(decoder=...) decodes every emitted block on the decoder's
+    stream (the reference's decode lane, engine.py:151-158, made real): the
+    videos equal an independent decode of the run's outputs in emission
+    order, decode stamps follow emissions, and the decode-inclusive
+    streaming FPS is defined."""
+    import numpy as np
+    import torch
+    import paper_2511_20426_b200 as bc
+    from paper_2511_20426_b200 import metrics
+    from paper_2511_20426_b200.vae import VaeDecoder, VaeWeights, vae_config
+    from paper_2511_20426_b200.wan import WanWeights
+
+    cfg = bc.wan_config("tiny", total_frames=27)
+    vcfg = vae_config("tiny", latent_h=cfg.latent_height, latent_w=cfg.latent_width)
+    vw = VaeWeights.random(vcfg, 3)
+    res = bc.run_cascade(cfg, "a lighthouse", weights=WanWeights.random(cfg, 7), decoder=VaeDecoder(vw))
+    assert sorted(res.videos) == list(range(cfg.num_blocks))
+    ref = VaeDecoder(vw)
+    ref.reset()
+    for k, b in enumerate(res.emitted_order):
+        z = torch.from_numpy(res.outputs[b].astype(np.float32).reshape(
+            cfg.block_size, cfg.latent_channels, cfg.latent_height, cfg.latent_width)).cuda()
+        want = ref.decode_block(z)
+        ref.wait()
+        got = res.videos[b]
+        assert got.shape == (vcfg.frames_out(cfg.block_size, k == 0), 3, vcfg.video_h, vcfg.video_w)
+        assert torch.equal(got, want), b
+    ems = res.trace.emissions
+    for ev in ems:
+        assert ev.decode_start is not None and ev.decode_done >= ev.decode_start >= 0.0
+        assert ev.decode_done >= ev.wall_clock - 1e-6
+    done = [ev.decode_done for ev in ems]
+    assert done == sorted(done)
+    assert metrics.streaming_fps(res.trace, clock="decoded") > 0.0
+    # a block cannot be decoded before it was emitted: decoded e2e FPS is at
+    # most the frames over the last EMISSION time (the run's wall clock also
+    # holds the trailing cache passes, so it can end after the last decode)
+    frames = sum(ev.emitted_video_frames for ev in ems)
+    assert metrics.end_to_end_fps(res.trace, clock="decoded") <= frames / ems[-1].wall_clock + 1e-9
