@@ -7,9 +7,14 @@ batch is one batched device forward per GPU:
 * single process / single GPU: ``execute`` calls ``forward`` once for every
   entry of the plan (the width-w batch is one set of kernel launches) and
   times it with CUDA events on the launching stream (``wall_seconds``);
-* multi-GPU: :mod:`paper_2511_20426_b200.distributed` shards the plan's
-  entries round-robin over ranks (``worker = position % G``, the reference's
-  assignment) and exchanges each layer's fresh K/V over NCCL.
+* multi-GPU: :mod:`paper_2511_20426_b200.distributed` splits the batch's
+  query rows evenly over the ranks (``rows``, default) or gives whole entries
+  to ranks round-robin (``blocks``: ``worker = position % G``, the
+  reference's assignment), and hands each layer's fresh K/V to the peers
+  with NVLink P2P stores into their IPC-mapped KV arenas plus per-slot
+  ready flags, issued by the q/k-norm kernel that produces them (or by a
+  side-stream copy, ``BC_KV_PUSH=copy``); torch.distributed (NCCL / gloo)
+  carries only the host-side rendezvous and IPC handle exchange.
 
 ``CostModel`` and ``exchanged_kv_frames`` are kept with the reference's
 arithmetic because the trace schema carries the modeled clock next to the
