@@ -6,8 +6,8 @@ one ``metrics`` line per iteration, one ``block`` line per emission (with
 the block decoded to pixels by the fixed linear stand-in decoder,
 executor.py:189-212), and a final ``done`` line.  The projection carries no
 wall-clock fields, so a live stream and a replayed one are identical.  The
-HTTP/SSE service itself is out of scope; this is the
-payload it would serve, fed by the device engine's ``event_sink``.
+session service that serves these lines over SSE, fed by the device
+engine's ``event_sink``, is :mod:`paper_2511_20426_b200.service`.
 """
 
 from __future__ import annotations
