@@ -322,7 +322,9 @@ def parallelism(world):
     if world == 1:
         return "temporal1"
     from paper_2511_20426_b200.distributed import shard_mode
-    push = "copy-engine side stream" if os.environ.get("BC_KV_PUSH") == "copy" else "q/k-kernel P2P stores"
+    how = os.environ.get("BC_KV_PUSH")
+    push = ("copy-engine side stream" if how == "copy" else "q/k-kernel P2P stores" if how == "kernel" else
+            "auto: copy engines between distinct GPUs, q/k-kernel P2P stores for ranks sharing a GPU")
     return f"temporal{world} (shard={shard_mode()}, kv_push={push}, IPC peer memory over NVLink)"
 
 

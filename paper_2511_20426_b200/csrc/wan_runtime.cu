@@ -775,8 +775,28 @@ extern "C" int bc_wan_set_peers(bc_wan_ctx* c, const bc_wan_peers* peers) {
   // engine -- a same-device copy (one-GPU emulation of the ranks) is an SM
   // kernel that a spinning attention can starve (measured: hangs at full
   // Wan-1.3B geometry, scripts/emulated_full.py).
+  // Default by device identity: when every peer replica lives on ANOTHER
+  // GPU the copies run on copy engines (DMA over NVLink, no SMs), so the
+  // transfer overlaps the producer's own attention instead of lengthening
+  // its q/k kernel by the NVLink store time; peers on this device (the
+  // one-GPU emulation, two processes on one GPU) keep the kernel stores.
+  // BC_KV_PUSH=copy / kernel overrides.
   const char* how = getenv("BC_KV_PUSH");
-  c->push_by_copy = how && std::strcmp(how, "copy") == 0;
+  if (how && std::strcmp(how, "copy") == 0) {
+    c->push_by_copy = true;
+  } else if (how && std::strcmp(how, "kernel") == 0) {
+    c->push_by_copy = false;
+  } else {
+    int me = -1;
+    cudaGetDevice(&me);
+    bool all_remote = peers->n_peers > 0;
+    for (int p = 0; p < peers->n_peers && all_remote; ++p) {
+      cudaPointerAttributes at{};
+      if (cudaPointerGetAttributes(&at, peers->peer_arena[p]) != cudaSuccess || at.device == me) all_remote = false;
+    }
+    (void)cudaGetLastError();
+    c->push_by_copy = all_remote;
+  }
   if (peers->n_peers > 0 && !c->side) {
     BC_CUDA(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
     BC_CUDA(cudaEventCreateWithFlags(&c->ev_qk, cudaEventDisableTiming));
