@@ -256,7 +256,11 @@ __device__ __forceinline__ void softmax_tile(const AttnParams& prm, uint32_t tme
     float alpha = 1.0f;
     bool bump;
     {
+#ifdef BC_ABL_MAX  // timing ablation only: no row max
+      const float mt = s[0] * c;
+#else
       const float mt = row_max() * c;
+#endif
       bump = (j == 0) || (mt > m_used + kRescaleThresh);
       if (bump) {
         const float m_new = fmaxf(m_used, mt);
@@ -281,8 +285,14 @@ __device__ __forceinline__ void softmax_tile(const AttnParams& prm, uint32_t tme
           p1 = ex2(x1);
         }
         const uint64_t pp = f2(p0, p1);
+#ifndef BC_ABL_SUM  // timing ablation only: no row sum
         sum2[t & 1] = fadd2(sum2[t & 1], pp);
+#endif
+#ifdef BC_ABL_PACK  // timing ablation only: no bf16 conversion
+        pk[t] = __float_as_uint(p0) ^ __float_as_uint(p1);
+#else
         pk[t] = pack_bf16(p0, p1);
+#endif
       }
     } else {
 #pragma unroll
@@ -297,7 +307,11 @@ __device__ __forceinline__ void softmax_tile(const AttnParams& prm, uint32_t tme
     }
     if (quad == 0) ATRACE(2 + tile_x * 8, j);
     // PV(j-1) must be complete before O is rescaled or P is overwritten
+#ifdef BC_ABL_OWAIT  // timing ablation only (races): no wait for PV(j-1)
+    if (false) {
+#else
     if (j > 0) {
+#endif
       mbar_wait(b.o_ready, (jb + j - 1) & 1);
       tc_fence_after();
       if (quad == 0) ATRACE(5 + tile_x * 8, j);
@@ -316,12 +330,16 @@ __device__ __forceinline__ void softmax_tile(const AttnParams& prm, uint32_t tme
     }
     // P -> smem in the UMMA K-major SW128 layout: half h holds keys
     // [64h, 64h+64); 16-byte chunk q of row r sits at chunk (q ^ (r & 7)).
+#ifndef BC_ABL_STS  // timing ablation only: no P stores
 #pragma unroll
     for (int q = 0; q < 16; ++q) {
       const int half = q >> 3, ch = q & 7;
       sts128(sp_u32 + half * kHalf + row * 128 + ((ch ^ (row & 7)) << 4), pk[4 * q], pk[4 * q + 1], pk[4 * q + 2],
              pk[4 * q + 3]);
     }
+#else
+    if (pk[5] == 0x12345u) sts128(sp_u32 + row * 16, pk[0], pk[1], pk[2], pk[3]);
+#endif
     float sa, sb, sc, sd;
     f2_split(sum2[0], sa, sb);
     f2_split(sum2[1], sc, sd);
