@@ -53,10 +53,16 @@ struct ConvCfg {
   static constexpr int kABytes = ((kStripRows * kRowBytes + 1023) / 1024) * 1024;
   static constexpr int kBBytes = ((NMAX * kRowBytes + 1023) / 1024) * 1024;
   static constexpr int kBudget = 200 * 1024;
+#ifndef BC_VAE_SA_MAX
+#define BC_VAE_SA_MAX 4
+#endif
+#ifndef BC_VAE_SB_MAX
+#define BC_VAE_SB_MAX 8
+#endif
   static constexpr int kSB0 = (96 * 1024) / kBBytes;
-  static constexpr int kSB = kSB0 < 2 ? 2 : kSB0 > 8 ? 8 : kSB0;
+  static constexpr int kSB = kSB0 < 2 ? 2 : kSB0 > BC_VAE_SB_MAX ? BC_VAE_SB_MAX : kSB0;
   static constexpr int kSA0 = (kBudget - kSB * kBBytes) / kABytes;
-  static constexpr int kSA = kSA0 < 2 ? 2 : kSA0 > 4 ? 4 : kSA0;
+  static constexpr int kSA = kSA0 < 2 ? 2 : kSA0 > BC_VAE_SA_MAX ? BC_VAE_SA_MAX : kSA0;
   static constexpr int kAcc = 2 * R * NMAX <= 512 ? 2 : 1;  // double-buffered accumulators when they fit
   static constexpr int kCols = kAcc * R * NMAX;
   static constexpr int kTmemCols = kCols <= 32 ? 32 : kCols <= 64 ? 64 : kCols <= 128 ? 128 : kCols <= 256 ? 256 : 512;
