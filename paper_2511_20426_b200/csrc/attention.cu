@@ -45,7 +45,7 @@ unsigned long long* bc_attn_trace_ptr = nullptr;
 extern "C" int bc_attn_trace_read(unsigned long long* host) {
   if (!bc_attn_trace_ptr) return 1;
   cudaDeviceSynchronize();
-  cudaMemcpy(host, bc_attn_trace_ptr, 32 * 64 * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+  cudaMemcpy(host, bc_attn_trace_ptr, (32 * 64 + 256 * 8) * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
   return 0;
 }
 #endif
@@ -734,6 +734,19 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       __syncwarp();
     };
+#ifdef BC_ATTN_TRACE
+    // per-CTA summary (scripts/attn_trace.sh): cycles, key steps, and where
+    // the issuer spent them
+    const long long trc0 = clock64();
+    unsigned long long trg0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(trg0));
+    long long tr_wait = 0, tr_kv = 0, tr_se = 0, tr_iqk = 0, tr_ipv = 0;
+#define TR_T(v) const long long v = clock64()
+#define TR_ADD(acc, v) acc += clock64() - v
+#else
+#define TR_T(v)
+#define TR_ADD(acc, v)
+#endif
     uint32_t ib = 0;                // ring items consumed before this item
     uint32_t tb[2] = {0u, 0u};      // tiles processed by x before this item
     uint32_t nb[2] = {0u, 0u};      // items x took part in before this item
@@ -755,20 +768,30 @@ __global__ void __launch_bounds__(kThreads, 1)
           const bool next = j + 1 < n;
           for (int x = 0; x < w.n_q; ++x) {
             if (next) {
+              TR_T(ts0);
               mbar_wait(&s_empty[x], (tb[x] + j) & 1);
+              TR_ADD(tr_se, ts0);
               if (x == 0) ring_wait(ib + kpos(j + 1));
               tc_fence_after();
+              TR_T(tq0);
               issue_qk(x, ib + kpos(j + 1));
+              TR_ADD(tr_iqk, tq0);
               if (x == w.n_q - 1) {
                 commit(&ring_empty[(ib + kpos(j + 1)) % kRing]);
                 if (j + 1 == n - 1) commit(q_empty);  // the item's last QK^T
               }
             }
+            TR_T(tw0);
             mbar_wait(&p_full[x], (tb[x] + j) & 1);
+            TR_ADD(tr_wait, tw0);
+            TR_T(tw1);
             if (x == 0) ring_wait(ib + vpos(j, n));
+            TR_ADD(tr_kv, tw1);
             if (j == 0 && nb[x] > 0) mbar_wait(&o_free[x], (nb[x] - 1) & 1);  // previous O read out
             tc_fence_after();
+            TR_T(tp0);
             issue_pv(x, ib + vpos(j, n), j == 0);
+            TR_ADD(tr_ipv, tp0);
           }
           commit(&ring_empty[(ib + vpos(j, n)) % kRing]);
         }
@@ -781,6 +804,23 @@ __global__ void __launch_bounds__(kThreads, 1)
         nb[x] += 1;
       }
     }
+#undef TR_T
+#undef TR_ADD
+#ifdef BC_ATTN_TRACE
+    if (prm.trace && lane_id() == 0 && blockIdx.x < 256) {
+      unsigned long long trg1;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(trg1));
+      unsigned long long* r = prm.trace + 32 * 64 + blockIdx.x * 8;
+      r[0] = clock64() - trc0;
+      r[1] = trg1 - trg0;
+      r[2] = tb[0] + tb[1];  // (query tile, key tile) steps processed
+      r[3] = tr_wait;
+      r[4] = tr_kv;
+      r[5] = tr_se;
+      r[6] = tr_iqk;
+      r[7] = tr_ipv;
+    }
+#endif
   } else if (warp >= 4) {
     asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegsSoftmax));
     const int x = (warp >= 8) ? 1 : 0;
@@ -1053,7 +1093,7 @@ int attention_run(const AttnArgs& a, cudaStream_t st) {
 #ifdef BC_ATTN_TRACE
   {
     static unsigned long long* buf = nullptr;
-    if (!buf) cudaMalloc(&buf, 32 * 64 * sizeof(unsigned long long));
+    if (!buf) cudaMalloc(&buf, (32 * 64 + 256 * 8) * sizeof(unsigned long long));
     p.trace = buf;
     bc_attn_trace_ptr = buf;
   }
