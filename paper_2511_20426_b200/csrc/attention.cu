@@ -69,7 +69,11 @@ constexpr int kRegsLaunch = 168;
 constexpr int kRegsCtl = 56;
 constexpr int kRegsSoftmax = 224;
 static_assert(128 * (kRegsLaunch - kRegsCtl) >= 256 * (kRegsSoftmax - kRegsLaunch), "register split");
+#ifndef BC_ATTN_SCHED_POLY
+#define BC_ATTN_SCHED_POLY 0
+#endif
 constexpr int kDefaultPoly = 0;
+constexpr int kSchedPoly = BC_ATTN_SCHED_POLY;  // FMA-pipe exp pairs (of 8) in the balanced kernel
 
 struct Smem {
   static constexpr int qa = 0;
@@ -1126,14 +1130,14 @@ int attention_run(const AttnArgs& a, cudaStream_t st) {
   if (a.balance && g_attn_balance && poly == 0) {
     static PerDeviceOnce sched_attrs;
     BC_RC(per_device_once(sched_attrs, [&]() -> int {
-      BC_CUDA(cudaFuncSetAttribute(attn_sched_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      BC_CUDA(cudaFuncSetAttribute(attn_sched_kernel<kSchedPoly>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    Smem::total + 1024));
       return BC_OK;
     }));
     int ctas = 0;
     const std::shared_ptr<const AttnSched> sch = build_sched(a, p, &ctas);
     if (sch) {
-      attn_sched_kernel<0><<<ctas, kThreads, Smem::total + 1024, st>>>(mq, mkv, p, *sch);
+      attn_sched_kernel<kSchedPoly><<<ctas, kThreads, Smem::total + 1024, st>>>(mq, mkv, p, *sch);
       BC_LAUNCHED();
       return BC_OK;
     }
