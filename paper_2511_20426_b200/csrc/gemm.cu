@@ -510,42 +510,58 @@ int make_tmap_2d(CUtensorMap* map, const void* base, uint64_t inner, uint64_t ou
 
 int num_sms() { return sm_count(); }
 
-int gemm_plan_bn(int M, int N) {
-  // 128x256 tiles amortise the A panel over twice the columns and measured
-  // 10-20% faster per tile than 128x128; fall back to narrower tiles only
-  // when N does not divide or the wide tiling cannot fill one wave.  When
-  // CTA-pair 256-row tiles quantise badly onto the pairs (N = 1536 at
-  // 23,400 rows: 552 tiles = 7.46 waves of 74 pairs), 192-column pair tiles
-  // can fill the last wave better (736 tiles = 9.95 waves): pick the width
-  // with the smaller (waves x width).
-  const int mt = (M + BM - 1) / BM;
-  if (N % 256 == 0 && mt * (N / 256) >= sm_count()) {
-    if (N % 192 == 0) {
-      const int pairs = sm_count() / 2, m2 = (M + 2 * BM - 1) / (2 * BM);
-      const long w256 = (long)((m2 * (N / 256) + pairs - 1) / pairs) * 256;
-      const long w192 = (long)((m2 * (N / 192) + pairs - 1) / pairs) * 192;
-      if (w192 < w256) return 192;
+// Automatic tiling: (tile width, CTAs per tile) minimising
+//   waves x (per-SM columns per tile) x relative cost per column,
+// waves = ceil(tiles / units) over 148 single CTAs or 74 CTA pairs.  The
+// relative costs are measured (scripts/gemm_tiling.py, profiles/
+// r2_gemm_tiling.txt): 256-wide pair tiles amortise best; narrower or
+// single-CTA tiles pay for more A/B panel traffic per column, least when a
+// short-K gated-residual epilogue dominates.  Small M is where the choice
+// matters: the width-1 sequential rows (4680) quantise to 2 waves of pair
+// tiles at N = 1536 but exactly 3 waves of 128-wide single tiles (-13%); a
+// 2925-row G = 8 slice fits one wave of pairs at N = 1536, K = 8960 (-21% vs
+// the previous choice).  Every tiling gives bit-identical results.
+struct Tiling {
+  int bn, cg;
+};
+Tiling gemm_plan(int M, int N, int K, int mode, int only_cg) {
+  const bool epi_bound = mode == kEpiResidualF32 && K <= 2048;
+  struct Cand {
+    int bn, cg;
+    double cost_compute, cost_epi;
+  };
+  static const Cand cands[] = {
+      {256, 2, 1.00, 1.00}, {192, 2, 1.07, 0.99}, {256, 1, 1.10, 1.05}, {128, 1, 1.50, 1.12}};
+  const int sms = sm_count();
+  Tiling best{N % 128 == 0 ? 128 : 64, 1};
+  double best_cost = 1e300;
+  for (const Cand& c : cands) {
+    if (N % c.bn || (only_cg && c.cg != only_cg)) continue;
+    const long units = c.cg == 2 ? sms / 2 : sms;
+    const long tiles = (long)((M + BM * c.cg - 1) / (BM * c.cg)) * (N / c.bn);
+    const long waves = (tiles + units - 1) / units;
+    const double cost = (double)waves * c.bn * (epi_bound ? c.cost_epi : c.cost_compute);
+    if (cost < best_cost) {
+      best_cost = cost;
+      best = Tiling{c.bn, c.cg};
     }
-    return 256;
   }
-  if (N % 128 == 0) return 128;
-  return 64;
+  return best;
 }
 
 int gemm_run(const GemmArgs& g, cudaStream_t st) {
   if (g.K % BK || g.N % 64 || g.M < 1)
     return bc_fail(BC_ERR_CONTRACT, "gemm: need K %% 64 == 0, N %% 64 == 0 (M=%d N=%d K=%d)", g.M, g.N, g.K);
-  const int bn = g.bn ? g.bn : gemm_plan_bn(g.M, g.N);
-  // CTA pairs for wide tiles when they still fill the machine (tuning knob
-  // BC_GEMM_PAIR=0/1 overrides)
-  static const int pair_env = [] {
-    const char* e = getenv("BC_GEMM_PAIR");
-    return e ? atoi(e) : -1;
-  }();
-  const int pair_tiles = ((g.M + 2 * BM - 1) / (2 * BM)) * (g.N / (bn ? bn : 1));
-  const bool pair = (bn == 256 || bn == 192) && g.cg != 1 &&
-                    (g.cg == 2 || bn == 192 || (pair_env >= 0 ? pair_env == 1 : pair_tiles >= sm_count() / 2));
-  const int cg = pair ? 2 : 1;
+  int bn = g.bn, cg = g.cg;
+  if (!bn) {
+    const Tiling t = gemm_plan(g.M, g.N, g.K, g.mode, g.cg);
+    bn = t.bn;
+    if (!cg) cg = t.cg;
+  }
+  // a forced width without a forced pairing: pairs for the widths that have them
+  if (!cg) cg = (bn == 256 || bn == 192) ? 2 : 1;
+  if (cg == 2 && bn != 256 && bn != 192) cg = 1;
+  if (cg == 1 && bn == 192) return bc_fail(BC_ERR_CONTRACT, "gemm: 192-wide tiles need CTA pairs");
   if (g.N % bn || (bn == 192 && cg != 2))
     return bc_fail(BC_ERR_CONTRACT, "gemm: tile width %d does not fit N=%d (192 needs CTA pairs)", bn, g.N);
   CUtensorMap ma, mb;
