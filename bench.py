@@ -740,6 +740,84 @@ def run_ours(args, cfg):
     print(json.dumps(line), flush=True)
 
 
+def run_decode_gpu(args, cfg):
+    """--decode-gpu (N >= 2 ranks): ranks 0..N-2 denoise (temporal
+    parallelism over their own group), rank N-1 only runs the Wan2.1 VAE
+    decoder; every emitted block goes rank 0 -> decode rank through the
+    CUDA-IPC inbox (decode_rank.py).  A step
+    = one generation AND the decode of all its blocks; value = video frames /
+    max over ranks of (denoise time on the denoiser ranks, time of the last
+    decode on the decode rank); generation-only and decode-inclusive
+    streaming FPS reported beside it."""
+    import torch
+    import torch.distributed as dist
+    import paper_2511_20426_b200 as bc
+    from paper_2511_20426_b200 import decode_rank as D
+    from paper_2511_20426_b200.vae import VaeDecoder, VaeWeights, vae_config
+    from paper_2511_20426_b200.wan import ResidentNoiseFeed, WanWeights, run_noise_keys
+
+    C = Ctx()
+    if C.world < 2:
+        raise SystemExit("--decode-gpu needs --gpus >= 2 (denoiser ranks + one decode rank)")
+    is_dec, dec_rank = D.split_ranks(True)
+    hand = D.DecodeHandoff(cfg, dec_rank)
+    frames = cfg.num_blocks * FRAMES_PER_BLOCK
+    if is_dec:
+        vname = "tiny" if args.preset == "tiny" else "wan2.1"
+        dec = VaeDecoder(VaeWeights.random(vae_config(vname, latent_h=cfg.latent_height,
+                                                      latent_w=cfg.latent_width), 3))
+        last = {}
+
+        def run():
+            last["times"] = hand.serve(dec, cfg.num_blocks)[1]
+    else:
+        weights = WanWeights.random(cfg, WEIGHT_SEED)
+        feed = ResidentNoiseFeed(SESSION_SEED, cfg, run_noise_keys(cfg))
+        remote = D.RemoteDecoder(hand)
+
+        def run():
+            return bc.run_cascade(cfg, PROMPT, session_seed=SESSION_SEED, weights=weights,
+                                  noise_feed=feed, decoder=remote)
+    for _ in range(args.warmup):
+        run()
+    C.barrier()
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(C.dev) as clocks:
+        ev0.record()
+        for _ in range(args.steps):
+            run()
+        ev1.record()
+        torch.cuda.synchronize()
+    my_ms = ev0.elapsed_time(ev1)
+    C.barrier()
+    job_ms = C.max(my_ms)
+    gen_ms = C.max(0.0 if is_dec else my_ms)
+    dec_ms = C.max(my_ms if is_dec else 0.0)
+    fps = C.max(D.decoded_fps(last["times"], FRAMES_PER_BLOCK)["streaming_fps_decoded"] if is_dec else 0.0)
+    hand.close()
+    if C.rank != 0:
+        return
+    G = C.world - 1
+    line = {
+        "metric": f"{metric_name(args)}, VAE-decoded on a separate GPU",
+        "value": frames * args.steps / (job_ms / 1e3), "unit": "frames/s", "n_gpus": C.world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": job_ms / args.steps,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic (random-init Wan2.1-shaped DiT and VAE decoder weights)",
+        "config": workload_config(args, cfg, f"{parallelism(G)} + 1 decode GPU (rank {dec_rank})"),
+        "generation_only": {"value": frames * args.steps / (gen_ms / 1e3), "ms_per_step": gen_ms / args.steps},
+        "decode_rank": {"ms_per_step": dec_ms / args.steps, "streaming_fps_decoded": fps,
+                        "handoff": "rank 0 -> decode rank: CUDA-IPC inbox ring (4 x 1.2 MB), "
+                                   "peer copy + cuStreamWriteValue32 / cuStreamWaitValue32 flags"},
+        "clocks": clocks.summary(),
+    }
+    if os.environ.get("BC_FORCE_DEVICE") is not None:
+        line["note"] = ("all ranks time-share ONE GPU (BC_FORCE_DEVICE test hook): a functional run of "
+                        "the multi-GPU path, not a performance number")
+    print(json.dumps(line), flush=True)
+
+
 def relaunch_under_torchrun(args):
     """--gpus N>1 outside torchrun: one process per GPU under
     torch.distributed.run (127.0.0.1 rendezvous); rank 0 prints the line."""
@@ -770,6 +848,8 @@ def main():
                     help="skip the cascade-vs-recache prompt-switch measurement")
     ap.add_argument("--no-sub", action="store_true",
                     help="skip the 14B / LongLive / causal secondary configurations")
+    ap.add_argument("--decode-gpu", action="store_true",
+                    help="N >= 2: the last rank only VAE-decodes (SURVEY 8f rank 1), fed by rank 0")
     args = ap.parse_args()
     if args.impl == "ours" and args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         sys.exit(relaunch_under_torchrun(args))
@@ -778,6 +858,8 @@ def main():
                      attention_mode="bidirectional", window_blocks=7, sink_blocks=args.sink)
     if args.impl == "reference":
         run_reference(args, cfg)
+    elif args.decode_gpu:
+        run_decode_gpu(args, cfg)
     else:
         run_ours(args, cfg)
 

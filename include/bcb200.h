@@ -242,6 +242,13 @@ int bc_ipc_open(const char handle[64], void** ptr);
 int bc_ipc_close(void* ptr);
 int bc_free(void* ptr);
 int bc_memset_async(void* ptr, int value, int64_t bytes, void* stream);
+/* Stream-ordered handoff between ranks (decode GPU inbox): a device copy
+ * (peer / IPC-mapped buffers allowed), and a 32-bit flag write / wait
+ * (value >= `value`) executed by the stream (cuStreamWriteValue32 with a
+ * memory fence / cuStreamWaitValue32). */
+int bc_copy_async(void* dst, const void* src, int64_t bytes, void* stream);
+int bc_stream_write_u32(void* addr, uint32_t value, void* stream);
+int bc_stream_wait_geq_u32(void* addr, uint32_t value, void* stream);
 
 /* ---------------------------------------------------------------------------
  * Building blocks, exported for the parity tests and the multi-GPU executor.

@@ -147,6 +147,9 @@ _SIGS = {
     "bc_ipc_close": (C.c_int, [C.c_void_p]),
     "bc_free": (C.c_int, [C.c_void_p]),
     "bc_memset_async": (C.c_int, [C.c_void_p, C.c_int, C.c_int64, C.c_void_p]),
+    "bc_copy_async": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]),
+    "bc_stream_write_u32": (C.c_int, [C.c_void_p, C.c_uint32, C.c_void_p]),
+    "bc_stream_wait_geq_u32": (C.c_int, [C.c_void_p, C.c_uint32, C.c_void_p]),
     "bc_vae_conv": (C.c_int, [C.POINTER(VaeConvArgs), C.c_void_p]),
     "bc_vae_prep": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
                     + [C.c_int32] * 6 + [C.c_void_p]),

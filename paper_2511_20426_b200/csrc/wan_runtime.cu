@@ -886,3 +886,32 @@ extern "C" int bc_memset_async(void* ptr, int value, int64_t bytes, void* stream
   BC_CUDA(cudaMemsetAsync(ptr, value, (size_t)bytes, (cudaStream_t)stream));
   return BC_OK;
 }
+
+// ---------------------------------------------------------------- stream-ordered handoff primitives
+// (the decode-GPU inbox, decode_rank.py): a copy between (possibly peer /
+// IPC-mapped) device buffers, and 32-bit flag writes / waits executed by the
+// stream itself -- the waiting stream's GPU spins in the front end, not on
+// an SM, so a peer that shares the GPU is never starved.
+extern "C" int bc_copy_async(void* dst, const void* src, int64_t bytes, void* stream) {
+  if (!dst || !src || bytes < 0) return bc_fail(BC_ERR_CONTRACT, "bc_copy_async: bad arguments");
+  BC_CUDA(cudaMemcpyAsync(dst, src, (size_t)bytes, cudaMemcpyDefault, (cudaStream_t)stream));
+  return BC_OK;
+}
+
+extern "C" int bc_stream_write_u32(void* addr, uint32_t value, void* stream) {
+  auto wv = write_value32();
+  if (!wv) return bc_fail(BC_ERR_CUDA, "cuStreamWriteValue32 unavailable");
+  // default flags: a memory fence orders the stream's earlier writes (the
+  // copy) before the flag for every observer
+  const CUresult r = wv((CUstream)stream, (CUdeviceptr)addr, value, CU_STREAM_WRITE_VALUE_DEFAULT);
+  if (r != CUDA_SUCCESS) return bc_fail(BC_ERR_CUDA, "cuStreamWriteValue32 failed (%d)", (int)r);
+  return BC_OK;
+}
+
+extern "C" int bc_stream_wait_geq_u32(void* addr, uint32_t value, void* stream) {
+  auto wt = wait_value32();
+  if (!wt) return bc_fail(BC_ERR_CUDA, "cuStreamWaitValue32 unavailable");
+  const CUresult r = wt((CUstream)stream, (CUdeviceptr)addr, value, CU_STREAM_WAIT_VALUE_GEQ);
+  if (r != CUDA_SUCCESS) return bc_fail(BC_ERR_CUDA, "cuStreamWaitValue32 failed (%d)", (int)r);
+  return BC_OK;
+}

@@ -44,6 +44,17 @@ from .errors import ContractViolation, InvalidInputError
 
 # Tests flip this to run `workers > 1` sessions as emulated ranks on one GPU.
 EMULATE = os.environ.get("BC_EMULATE_RANKS", "0") == "1"
+# Process group of the denoiser ranks when the job also has a decode rank
+# (decode_rank.split_ranks); None: the whole world group denoises.
+DIT_GROUP = None
+
+
+def dit_world() -> int:
+    """Denoiser ranks of the initialised torch.distributed job (0: none)."""
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()):
+        return 0
+    return dist.get_world_size(DIT_GROUP)
 ROW_TILE = 128  # query rows per attention tile: the unit of the rows partition
 ROW_UNIT_SMALL = 16  # unit when a batch has fewer than 2 tiles per rank
 
@@ -334,13 +345,14 @@ class DistWanSession:
         self.torch, self.dist = torch, dist
         self.cfg = config
         self.mode = shard_mode()
-        self.world, self.rank = dist.get_world_size(), dist.get_rank()
+        self.group = DIT_GROUP
+        self.world, self.rank = dist.get_world_size(self.group), dist.get_rank(self.group)
         width = min(config.cascade_width, config.num_blocks)
         n_slots = config.window_blocks + config.sink_blocks + width + 1
         self.state = _RankState(rt.weights, config, width, n_slots, self.world, self.rank, ipc=True)
         mine = (self.rank, self.state.arena_handle, self.state.flags_handle, self.state.y_handle)
         everyone = [None] * self.world
-        dist.all_gather_object(everyone, mine)
+        dist.all_gather_object(everyone, mine, group=self.group)
         self._opened = []
         peers = []
         for r, ah, fh, yh in everyone:
@@ -350,7 +362,7 @@ class DistWanSession:
             self._opened += [a, f, y]
             peers.append((r, a, f, y))
         self.state.attach(peers, rows=self.mode == "rows")
-        dist.barrier()
+        dist.barrier(group=self.group)
         self.slots = SlotAllocator(n_slots)
         self.slot_epoch = SlotEpochs(n_slots)
         self.rep = _Replica(torch, config, width)
@@ -429,7 +441,7 @@ class DistWanSession:
         all of them on the node's shared host cores.  Bit-identical either
         way: each key's draw is a pure function of the key."""
         dist, torch = self.dist, self.torch
-        nccl = dist.get_backend() == "nccl"
+        nccl = dist.get_backend(self.group) == "nccl"
         forced = os.environ.get("BC_NOISE_GATHER") == "1"   # test hook (gloo: gathers on the host)
         if self.mode != "rows" or not (nccl or forced) or not hasattr(self.noise, "stream"):
             self.noise.fetch(keys, dests)
@@ -444,7 +456,7 @@ class DistWanSession:
             if where == "cpu":
                 torch.cuda.current_stream().synchronize()
         gathered = torch.empty((G * chunk,) + tuple(self.shape), dtype=torch.float32, device=where)
-        dist.all_gather_into_tensor(gathered, buf)
+        dist.all_gather_into_tensor(gathered, buf, group=self.group)
         for i, dst in enumerate(dests):   # key i was drawn by rank i % G as its (i // G)-th
             dst.copy_(gathered[(i % G) * chunk + i // G], non_blocking=where == "cuda")
 
@@ -463,6 +475,15 @@ class DistWanSession:
             return self.host_out[block].numpy().reshape(self.cfg.block_size, -1).astype(np.float64)
         return None
 
+    def emitted_device(self, block):
+        """The emitted block's x0 on this rank's device (every rank has every
+        block in the rows partition; in the blocks partition only its owner)."""
+        t = self.rep.final.get(block)
+        if t is None:
+            raise ContractViolation(f"block {block} was not emitted on rank {self.rank} "
+                                    f"(blocks partition: rank {owner(block, self.world)} owns it)")
+        return t
+
     def gather_outputs(self, blocks):
         """Every rank gets every emitted block (rows: already replicated;
         blocks: owner -> all)."""
@@ -470,7 +491,7 @@ class DistWanSession:
             return {b: self.emitted_host(b) for b in blocks}
         mine = {b: self.emitted_host(b) for b in blocks if owner(b, self.world) == self.rank}
         parts = [None] * self.world
-        self.dist.all_gather_object(parts, mine)
+        self.dist.all_gather_object(parts, mine, group=self.group)
         out = {}
         for p in parts:
             out.update(p)
@@ -489,7 +510,7 @@ class DistWanSession:
 
     def close(self):
         self.torch.cuda.synchronize()
-        self.dist.barrier()
+        self.dist.barrier(group=self.group)
         for p in self._opened:
             N.lib().bc_ipc_close(p)
         self._opened = []

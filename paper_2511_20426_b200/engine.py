@@ -117,19 +117,28 @@ class _DecodeLane:
         if config.model != "wan":
             raise InvalidInputError("VAE decode needs the Wan-shaped model (latents (S, 16, h, w))",
                                     fields=["model"])
+        import torch
+        self.torch = torch
+        self.videos, self.marks = {}, []
+        self.dev = dev
+        # decode on a dedicated GPU (decode_rank.RemoteDecoder): hand every
+        # emitted block to the decode rank; its times live on that rank
+        self.remote = decoder if getattr(decoder, "remote", False) else None
+        if self.remote is not None:
+            return
         dc = decoder.cfg
         if (dc.block_size, dc.z_dim, dc.latent_h, dc.latent_w) != (
                 config.block_size, config.latent_channels, config.latent_height, config.latent_width):
             raise InvalidInputError("VAE geometry does not match the run's latents", fields=["decoder"])
-        import torch
-        self.torch = torch
-        self.decoder, self.dev = decoder, dev
-        self.videos, self.marks = {}, []
+        self.decoder = decoder
         decoder.reset()
 
     def emit(self, block, event):
         torch = self.torch
         z = self.dev.emitted_device(block)
+        if self.remote is not None:
+            self.remote.emit(block, z)
+            return
         st = self.decoder.stream
         st.wait_stream(torch.cuda.current_stream())
         z.record_stream(st)                     # the session may free it before the decode ran
@@ -140,6 +149,9 @@ class _DecodeLane:
         self.marks.append((event, s0, s1))
 
     def finish(self):
+        if self.remote is not None:
+            self.remote.finish()
+            return
         self.decoder.stream.synchronize()
         origin = self.dev.events[0]
         for ev, s0, s1 in self.marks:

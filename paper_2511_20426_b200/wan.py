@@ -318,8 +318,7 @@ class WanRuntime:
     def open_session(self, config, conditioning, session_seed, noise_feed=None):
         from . import distributed
         try:
-            import torch.distributed as dist
-            multi = dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1
+            multi = distributed.dit_world() > 1
         except ImportError:  # pragma: no cover
             multi = False
         if multi:

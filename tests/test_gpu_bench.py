@@ -33,3 +33,20 @@ def test_bench_line(gpus):
     else:
         v = d["vae_decode"]
         assert v["ms_per_block"] > 0 and v["cascade_with_decode"]["e2e_fps_decoded"] > 0
+
+
+@pytest.mark.parametrize("gpus", [2, 3])
+def test_bench_decode_gpu_line(gpus):
+    """--decode-gpu: the last rank only VAE-decodes, fed by rank 0 through the
+    IPC inbox; one line, value over the whole job."""
+    env = dict(os.environ, BC_FORCE_DEVICE="0", BC_DIST_BACKEND="gloo")
+    env.pop("WORLD_SIZE", None)
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", str(gpus), "--decode-gpu",
+                          "--preset", "tiny", "--blocks", "9", "--steps", "2", "--warmup", "1"],
+                         capture_output=True, text=True, timeout=600, cwd=ROOT, env=env)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, out.stdout[-2000:]
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == gpus and d["value"] > 0 and d["generation_only"]["value"] >= d["value"] * 0.999
+    assert "decode GPU" in d["config"]["parallelism"] and d["decode_rank"]["streaming_fps_decoded"] > 0
