@@ -117,7 +117,11 @@ def text_states(cond, text_len: int, text_dim: int) -> np.ndarray:
     """Synthetic text-encoder states for a prompt: row r is
     standard_normal(text_dim) from Philox(key = sha256(prompt)[:16] as two
     uint64, counter = [r, 1, 0, 0]).  float32 [text_len][text_dim]."""
-    key = cond.key_words()
+    if hasattr(cond, "key_words"):
+        key = cond.key_words()
+    else:   # the reference's Conditioning (core.py:131-141) keeps the prompt, not the digest
+        import hashlib
+        key = np.frombuffer(hashlib.sha256(cond.prompt.encode("utf-8")).digest()[:16], dtype=np.uint64)
     out = np.empty((text_len, text_dim), dtype=np.float32)
     N.run_noise_tasks([(int(key[0]), int(key[1]), (r, 1, 0, 0), out[r]) for r in range(text_len)], 1)
     return out
@@ -238,6 +242,65 @@ class _Lease:
         return self.ctx.read_kv(slot, layer, which)
 
 
+class _OpSlot:
+    """What an operator-path K/V handle reads through: one slot of the
+    runtime's operator arena at the generation the handle was made in."""
+
+    def __init__(self, op, slot, gen):
+        self.op, self.slot, self.gen = op, slot, gen
+        self.layers = op.ctx.layers
+
+    def valid(self):
+        return self.op.ctx.handle is not None and self.op.gen[self.slot] == self.gen
+
+    def read(self, slot, layer, which):
+        if not self.valid():
+            raise ContractViolation("K/V handle of a recycled operator slot (the block left the "
+                                    "arena); keep its host arrays if it is needed later")
+        return self.op.ctx.read_kv(slot, layer, which)
+
+
+class _OpArena:
+    """Slot bookkeeping of the operator path: generation per slot and a
+    least-recently-used choice of the slot a new block overwrites (never one
+    the current call attends to)."""
+
+    def __init__(self, ctx):
+        self.ctx = ctx
+        self.gen = [0] * ctx.n_slots
+        self.used = [0] * ctx.n_slots   # call counter of the last use
+        self.calls = 0
+        self.uploads = 0                # pool blocks that had to come from host arrays
+
+    def resident_slot(self, kv):
+        """The slot of a still-valid handle of THIS arena, else None.  ``kv``
+        is a SlotKV or any sequence of its per-layer views (the reference
+        KVPool stores ``tuple(kv_layers)``, kvpool.py:51-53)."""
+        ref = getattr(kv, "arena", None)
+        if ref is None and len(kv) and all(getattr(l, "_arena", None) is getattr(kv[0], "_arena", 0) for l in kv):
+            ref = getattr(kv[0], "_arena", None)
+        if isinstance(ref, _OpSlot) and ref.op is self and ref.valid():
+            self.used[ref.slot] = self.calls + 1
+            return ref.slot
+        return None
+
+    def take(self, pinned, block):
+        self.calls += 1
+        free = [s for s in range(self.ctx.n_slots) if s not in pinned]
+        if not free:
+            raise ContractViolation("operator arena exhausted")
+        s = min(free, key=lambda x: self.used[x])
+        self.gen[s] += 1               # whatever the slot held is gone
+        self.used[s] = self.calls
+        return s
+
+    def ref(self, slot):
+        return _OpSlot(self, slot, self.gen[slot])
+
+    def close(self):
+        self.ctx.close()
+
+
 class WanRuntime:
     def __init__(self, weights: WanWeights):
         self.weights = weights
@@ -264,14 +327,30 @@ class WanRuntime:
         self._cached = ((ctx.max_entries, ctx.n_slots), ctx)
 
     def release_cached(self):
-        """Free the cached context's device memory (KV arena + workspace)."""
+        """Free the cached contexts' device memory (KV arena + workspace) of
+        the session path and of the operator path."""
         if self._cached is not None:
             self._cached[1].close()
             self._cached = None
+        if getattr(self, "_op", None) is not None:
+            self._op.close()
+            self._op = None
 
     # reference operator contract (denoiser.forward) ----------------------
     def forward(self, batch, pool_kv, mask):
-        from .denoiser import EntryOutput, LayerKV, visible_block_lists
+        """``denoiser.forward`` for Wan weights (reference ``denoiser.py:299-357``
+        contract).  The operator path keeps one persistent context (arena,
+        workspace, text K/V of the last conditioning) in the runtime, and
+        returns every entry's fresh K/V as a device-resident handle
+        (:class:`~.kvpool.SlotKV` over :class:`_OpSlot`): when the caller --
+        e.g. the reference engine's ``apply_results`` / ``KVPool`` -- hands
+        those handles back as pool KV, the blocks are attended in place (no
+        host round trip of ~0.9 GB per block at 1.3B).  Host-array LayerKV
+        (any other producer) is uploaded into a free slot.  A slot that is
+        recycled bumps its generation, so a stale handle raises instead of
+        reading another block's K/V."""
+        from .denoiser import EntryOutput, visible_block_lists
+        from .kvpool import SlotKV
         torch = N.torch_mod()
         cfg = self.cfg
         S, C, H, W = cfg.block_size, cfg.latent_channels, cfg.latent_height, cfg.latent_width
@@ -279,41 +358,59 @@ class WanRuntime:
             raise ContractViolation("the Wan forward takes one conditioning per call")
         pool_blocks = list(mask.pool_blocks)
         blocks = [e.block_index for e in batch]
-        slot_of = {b: i for i, b in enumerate(pool_blocks + blocks)}
-        ctx = _Ctx(self.weights, len(batch), len(slot_of))
-        try:
-            for b in pool_blocks:
+        op = self._op_arena(len(batch), len(pool_blocks) + len(blocks))
+        slot_of = {}
+        for b in pool_blocks:                   # resident handles first: they pin their slots
+            s_ = op.resident_slot(pool_kv[b])
+            if s_ is not None:
+                slot_of[b] = s_
+        pinned = set(slot_of.values())
+        for b in pool_blocks:
+            if b not in slot_of:                # host arrays (or a foreign / stale handle): upload
+                slot_of[b] = op.take(pinned, b)
+                pinned.add(slot_of[b])
+                op.uploads += 1
                 for layer, kv in enumerate(pool_kv[b]):
                     for which, arr in ((0, kv.keys), (1, kv.values)):
-                        ctx.arena[layer, slot_of[b], which].copy_(
-                            torch.as_tensor(np.asarray(arr, dtype=np.float32)).reshape(ctx.T, ctx.d))
-            ctx.set_text(batch[0].conditioning)
-            host = [not hasattr(e.latents, "is_cuda") for e in batch]
-            lat = [torch.as_tensor(np.asarray(e.latents, dtype=np.float32)).cuda() if h
-                   else e.latents.float() for e, h in zip(batch, host)]
-            lat = [x.reshape(S, C, H, W).contiguous().clone() for x in lat]
-            outs = [torch.empty_like(x) for x in lat]
-            vis = [[slot_of[v] for v in lst] for lst in visible_block_lists(mask)]
-            bt = N.make_batch(S, blocks, [e.noise_level for e in batch],
-                              [slot_of[b] for b in blocks], vis)
-            upd = _make_update([POST_X0] * len(batch), lat, [None] * len(batch), outs,
-                               [None] * len(batch))
-            ctx.step(bt, upd)
-            torch.cuda.current_stream().synchronize()
-            ctx.check_status()
-            results = []
-            for i, e in enumerate(batch):
-                x0 = outs[i].reshape(S, -1)
-                x0 = x0.cpu().numpy() if host[i] else x0
-                kv = tuple(LayerKV(block_index=e.block_index, layer_index=l,
-                                   keys=ctx.read_kv(slot_of[e.block_index], l, 0),
-                                   values=ctx.read_kv(slot_of[e.block_index], l, 1),
-                                   noise_tag=e.noise_level, conditioning_id=e.conditioning.id)
-                           for l in range(cfg.layers))
-                results.append(EntryOutput(block_index=e.block_index, x0=x0, kv=kv))
-            return results
-        finally:
-            ctx.close()
+                        op.ctx.arena[layer, slot_of[b], which].copy_(
+                            torch.as_tensor(np.asarray(arr, dtype=np.float32)).reshape(op.ctx.T, op.ctx.d))
+        for b in blocks:                        # each entry's fresh K/V goes to a slot of its own
+            slot_of[b] = op.take(pinned, b)
+            pinned.add(slot_of[b])
+        op.ctx.set_text(batch[0].conditioning)
+        host = [not hasattr(e.latents, "is_cuda") for e in batch]
+        lat = [torch.as_tensor(np.asarray(e.latents, dtype=np.float32)).cuda() if h
+               else e.latents.float() for e, h in zip(batch, host)]
+        lat = [x.reshape(S, C, H, W).contiguous().clone() for x in lat]
+        outs = [torch.empty_like(x) for x in lat]
+        vis = [[slot_of[v] for v in lst] for lst in visible_block_lists(mask)]
+        bt = N.make_batch(S, blocks, [e.noise_level for e in batch], [slot_of[b] for b in blocks], vis)
+        upd = _make_update([POST_X0] * len(batch), lat, [None] * len(batch), outs, [None] * len(batch))
+        op.ctx.step(bt, upd)
+        torch.cuda.current_stream().synchronize()
+        op.ctx.check_status()
+        results = []
+        for i, e in enumerate(batch):
+            x0 = outs[i].reshape(S, -1)
+            x0 = x0.cpu().numpy().astype(np.float64) if host[i] else x0
+            kv = SlotKV(op.ref(slot_of[e.block_index]), slot_of[e.block_index], e.block_index,
+                        e.noise_level, e.conditioning.id, S)
+            results.append(EntryOutput(block_index=e.block_index, x0=x0, kv=kv))
+        return results
+
+    def _op_arena(self, entries, slots_needed):
+        """The operator path's persistent context, grown when a call needs
+        more entries or slots than it has (the default fits the config's
+        cascade: W + sink + width + 1 slots)."""
+        cfg = self.cfg
+        op = getattr(self, "_op", None)
+        if op is None or op.ctx.max_entries < entries or op.ctx.n_slots < slots_needed:
+            if op is not None:
+                op.close()
+            width = max(entries, min(cfg.cascade_width, cfg.num_blocks))
+            n_slots = max(slots_needed, cfg.window_blocks + cfg.sink_blocks + width + 1)
+            op = self._op = _OpArena(_Ctx(self.weights, width, n_slots))
+        return op
 
     def open_session(self, config, conditioning, session_seed, noise_feed=None):
         from . import distributed
