@@ -16,7 +16,8 @@ import numpy as np
 
 from .errors import ContractViolation, DeviceError, raise_for_status
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libbcb200.so")
+# BC_LIB: a variant build of the same library (scripts/lib_variants.sh); default: the in-tree build
+LIB_PATH = os.environ.get("BC_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "libbcb200.so")
 MAX_ENTRIES = 16
 MAX_VIS = 32
 
