@@ -16,6 +16,11 @@ timeout 900 ncu --profile-from-start off --metrics gpu__time_duration.sum,dram__
 timeout 600 ncu --set full --import-source on -k regex:attn -s 1 -c 1 -o gpurun_out/ev_attn python scripts/attn_one.py > /dev/null 2>&1
 timeout 600 ncu --profile-from-start off --set full --import-source on -k regex:gemm_kernel -s 5 -c 2 -o gpurun_out/ev_gemm_ffn python scripts/profile_iter.py > /dev/null 2>&1
 timeout 600 ncu --profile-from-start off --set full -k regex:"ln_rows|qk_norm|rms_rows" -s 3 -c 3 -o gpurun_out/ev_bw python scripts/profile_iter.py > /dev/null 2>&1
+timeout 900 python scripts/scaling_projection.py 2>/dev/null | tail -1 > gpurun_out/ev_scaling.json
+BC_FORCE_DEVICE=0 BC_DIST_BACKEND=gloo timeout 900 python bench.py --gpus 2 --decode-gpu --steps 1 --warmup 1 \
+  2>>gpurun_out/ev_bench.err | tail -1 > gpurun_out/ev_decode_gpu_one_gpu.json
+timeout 300 python scripts/attn_power.py > gpurun_out/ev_attn_power.txt 2>&1
+timeout 300 python scripts/gemm_tiling.py > gpurun_out/ev_gemm_tiling.txt 2>&1
 for tool in memcheck racecheck synccheck; do
   echo "== $tool"; timeout 900 compute-sanitizer --tool $tool --print-limit 20 python scripts/sanitize_small.py 2>&1 | tail -4
 done > gpurun_out/ev_sanitizers.txt
