@@ -342,3 +342,60 @@ def test_attention_plan_rejects_malformed_batches():
     for q, kv, h in ((0, 256, 2), (128, 0, 2), (128, 256, 0), (128, 256, 256)):
         assert N.lib().bc_attention_plan(C.byref(b), q, kv, h, items.ctypes.data, 64, start.ctypes.data,
                                          C.byref(n_ctas)) == 1
+
+
+class _FakeCtx:
+    """Stands in for wan._Ctx in the operator-arena bookkeeping tests (no GPU)."""
+
+    def __init__(self, n_slots, layers=2):
+        self.n_slots, self.layers, self.handle = n_slots, layers, object()
+        self.reads = []
+
+    def read_kv(self, slot, layer, which):
+        self.reads.append((slot, layer, which))
+        return np.zeros((3, 1, 1))
+
+
+def test_operator_arena_slots_generations_and_residency():
+    """Wan operator path (wan.WanRuntime.forward): a fresh block takes the
+    least recently used slot the call does not attend to; recycling a slot
+    bumps its generation so the old handle raises instead of reading another
+    block's K/V; handles come back resident whether passed as the SlotKV or
+    as the reference KVPool's tuple of its layers (kvpool.py:51-53)."""
+    from paper_2511_20426_b200.errors import ContractViolation
+    from paper_2511_20426_b200.kvpool import SlotKV
+    from paper_2511_20426_b200.wan import _OpArena
+    op = _OpArena(_FakeCtx(4))
+    s0 = op.take(set(), 0)
+    h0 = SlotKV(op.ref(s0), s0, 0, 0.0, "c", 3)
+    assert op.resident_slot(h0) == s0 and op.resident_slot(tuple(h0)) == s0
+    pinned = {s0}
+    s1 = op.take(pinned, 1)
+    assert s1 != s0
+    h1 = SlotKV(op.ref(s1), s1, 1, 0.0, "c", 3)
+    # a call attending to block 0 never hands its slot to a new block
+    for b in range(2, 12):
+        s = op.take({s0}, b)
+        assert s != s0
+    assert op.resident_slot(h0) == s0 and h0[1].keys.shape == (3, 1, 1)
+    # block 1's slot was recycled meanwhile: its handle is stale
+    assert op.resident_slot(h1) is None
+    with pytest.raises(ContractViolation):
+        h1[0].keys
+    # a tuple mixing layers of different handles is not a resident block
+    assert op.resident_slot((h0[0], h1[1])) is None
+    with pytest.raises(ContractViolation):
+        op.take({0, 1, 2, 3}, 99)
+
+
+def test_decoded_fps_definitions():
+    """decode_rank.decoded_fps: end to end = all frames / last decode done;
+    streaming = mean of 12 frames over the intervals ending at blocks 8 and 9
+    (1-indexed) on the decode rank's clock."""
+    from paper_2511_20426_b200.decode_rank import decoded_fps
+    times = [(0.1 * b, 0.1 * b + 0.05) for b in range(13)]
+    times[8] = (0.8, 0.95)         # block 9 (1-indexed) finishes late
+    f = decoded_fps(times, 12)
+    assert f["e2e_fps_decoded"] == pytest.approx(13 * 12 / 1.25)
+    assert f["streaming_fps_decoded"] == pytest.approx((12 / 0.1 + 12 / 0.2) / 2)
+    assert decoded_fps(times[:5], 12)["streaming_fps_decoded"] is None
