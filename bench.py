@@ -508,6 +508,40 @@ def kernel_profile(bc, N, cfg, weights, feed):
     return prof, wall
 
 
+def kernel_times_graphs(bc, cfg, weights, feed, prof):
+    """The same per-class breakdown in the PRODUCT launch mode: one generation
+    launched as CUDA graphs without per-kernel events, kernel durations from
+    CUPTI activity records (torch.profiler); algorithmic flops / bytes per
+    class from the eager pass (they do not depend on the launch mode).
+    Attention launches alternate self / cross within a layer (same kernel)."""
+    import torch
+    from torch.profiler import ProfilerActivity, profile
+    torch.cuda.synchronize()
+    with profile(activities=[ProfilerActivity.CUDA]) as p:
+        bc.run_cascade(cfg, PROMPT, session_seed=SESSION_SEED, weights=weights, noise_feed=feed)
+        torch.cuda.synchronize()
+    evs = sorted((e for e in p.events() if e.device_type == torch.autograd.DeviceType.CUDA
+                  and "bc::" in e.name), key=lambda e: e.time_range.start)
+    out, k = {}, 0
+    for e in evs:
+        if "attn_sched_kernel" in e.name or "attn_kernel" in e.name:
+            c = "self_attention" if k % 2 == 0 else "cross_attention"
+            k += 1
+        elif "gemm_kernel" in e.name:
+            c = "gemm"
+        else:
+            c = "bandwidth"
+        ms, n = out.get(c, (0.0, 0))
+        out[c] = (ms + (e.time_range.end - e.time_range.start) / 1e3, n + 1)
+    res = {}
+    for c, (ms, n) in out.items():
+        fl, by = (prof[c][1], prof[c][2]) if c in prof else (0.0, 0.0)
+        res[c] = {"ms": round(ms, 3), "launches": n,
+                  "tflops": round(fl / (ms / 1e3) / 1e12, 1) if fl > 0 and ms > 0 else None,
+                  "gbs": round(by / (ms / 1e3) / 1e9, 1) if by > 0 and ms > 0 else None}
+    return res
+
+
 def kernels_and_roofline(prof, peaks, peak_kind):
     total = sum(v[0] for v in prof.values())
     kernels = {k: {"ms": round(v[0], 3), "launches": v[3],
@@ -629,6 +663,12 @@ def run_ours(args, cfg):
 
     # ---- per-kernel-class profile: separate eager pass ----
     prof, prof_ms = kernel_profile(bc, N, cfg, weights, feed)
+    graphs = None
+    if world == 1:
+        try:
+            graphs = kernel_times_graphs(bc, cfg, weights, feed, prof)
+        except Exception as exc:   # the breakdown is informational; never lose the line
+            graphs = {"error": f"{type(exc).__name__}: {exc}"[:200]}
 
     # ---- prompt switch at block 8: cascade mode (product: text K/V swap only)
     # vs the KV-recache baseline (paper: ~200 ms stall) ----
@@ -712,7 +752,9 @@ def run_ours(args, cfg):
                                  "eager multi-rank steps, noise pre-resident in HBM",
                         "e2e": "public run_cascade, host noise generated + copied H2D per iteration, "
                                "emitted blocks copied D2H, host clock",
-                        "kernels": "separate eager generation with per-launch CUDA events"},
+                        "kernels": "separate eager generation with per-launch CUDA events",
+                        "kernels_graphs": "one more generation as CUDA graphs (the product mode), kernel "
+                                          "durations from CUPTI activity records (torch.profiler)"},
         "streaming_fps": cas["streaming_fps"],
         "sequential": ({"value": seq["value"], "e2e": seq["e2e"], "streaming_fps": seq["streaming_fps"],
                         "ms_per_step": seq["ms_per_step"], "steps": args.steps, "warmup": args.warmup,
@@ -729,6 +771,7 @@ def run_ours(args, cfg):
         "roofline": roof,
         "kernels": kernels,
         "kernel_profile_run_ms": round(prof_ms, 1),
+        "kernels_graphs": graphs,
         "e2e": {"value": cas["e2e"], "unit": "frames/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h},
         "gpu_launches": cas["launches"],

@@ -33,6 +33,8 @@ def test_bench_line(gpus):
     else:
         v = d["vae_decode"]
         assert v["ms_per_block"] > 0 and v["cascade_with_decode"]["e2e_fps_decoded"] > 0
+        g = d["kernels_graphs"]      # product launch mode, CUPTI kernel durations
+        assert g["self_attention"]["ms"] > 0 and g["gemm"]["launches"] == d["kernels"]["gemm"]["launches"]
 
 
 @pytest.mark.parametrize("gpus", [2, 3])
