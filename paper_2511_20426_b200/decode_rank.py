@@ -53,6 +53,11 @@ def split_ranks(decode_gpu: bool):
     if world < 2:
         raise InvalidInputError("a decode GPU needs at least 2 ranks (denoiser + decoder)",
                                 fields=["decode_gpu"])
+    if world > 2 and distributed.shard_mode() != "rows":
+        # checked on every rank (same environment) before any collective, so
+        # a misconfigured job fails everywhere instead of hanging
+        raise InvalidInputError("a decode GPU needs the rows partition (every denoiser rank "
+                                "holds every emitted block)", fields=["BC_TEMPORAL_SHARD"])
     dec = world - 1
     group = dist.new_group(ranks=list(range(dec)))       # every rank must take part
     distributed.DIT_GROUP = group
@@ -110,11 +115,6 @@ class DecodeHandoff:
             _, _, fh = everyone[producer]
             self.peer_flags = _ipc_open(fh)
             self._opened.append(self.peer_flags)
-        if self.role == "producer":
-            from .distributed import dit_world, shard_mode
-            if dit_world() > 1 and shard_mode() != "rows":
-                raise InvalidInputError("a decode GPU needs the rows partition (every denoiser rank "
-                                        "holds every emitted block)", fields=["BC_TEMPORAL_SHARD"])
         # handoff sequence numbers run on across generations (the flags are
         # monotonic counters): block k of a run is item seq0 + k
         self.sent = 0      # producer: items handed off so far
