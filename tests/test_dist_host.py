@@ -111,3 +111,43 @@ def test_two_rank_host_agreement():
                 for need, m in zip(row, mrow):
                     assert not (m >> r) & 1                       # never wait on yourself
                     assert (need == 0) == (m == 0) and need <= it + 1
+
+
+def _split_worker(rank, world, port, q, shard):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), BC_TEMPORAL_SHARD=shard)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2511_20426_b200 import decode_rank, distributed
+        from paper_2511_20426_b200.errors import InvalidInputError
+        try:
+            is_dec, dec = decode_rank.split_ranks(True)
+        except InvalidInputError:
+            q.put((rank, "rejected"))
+            return
+        # the denoiser group holds ranks 0..N-2; the decode rank is outside it
+        n = dist.get_world_size(distributed.DIT_GROUP) if not is_dec else None
+        q.put((rank, (is_dec, dec, n, distributed.dit_world() if not is_dec else None)))
+        dist.barrier()
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("shard", ["rows", "blocks"])
+def test_decode_rank_split_three_ranks(shard):
+    """decode_rank.split_ranks over gloo, world 3: ranks 0-1 denoise in their
+    own group, rank 2 decodes; the blocks partition is rejected on EVERY rank
+    before any collective (a decode GPU needs every block on rank 0)."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_split_worker, args=(r, 3, port, q, shard)) for r in range(3)]
+    for p in procs:
+        p.start()
+    got = dict(q.get(timeout=120) for _ in range(3))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    if shard == "blocks":
+        assert got == {0: "rejected", 1: "rejected", 2: "rejected"}
+    else:
+        assert got == {0: (False, 2, 2, 2), 1: (False, 2, 2, 2), 2: (True, 2, None, None)}
