@@ -59,14 +59,22 @@ struct ConvCfg {
 #ifndef BC_VAE_SB_MAX
 #define BC_VAE_SB_MAX 8
 #endif
-  static constexpr int kSB0 = (96 * 1024) / kBBytes;
+  // one B stage holds the weights of all kw taps of a (kt, kh, channel
+  // chunk): the MMA issuer then runs kw x R x CK/16 MMAs per barrier wait.
+  // With one tap per stage a group was only R x CK/16 = 4 MMAs (192 cycles
+  // of tensor work at N = 96) and the ~150-cycle issue gap between groups
+  // (commits, the next stage's wait, descriptor setup) left the tensor pipe
+  // ~50% idle -- the pipe queues barely more than one instruction.
+  static constexpr int kTapsPerB = 3;
+  static constexpr int kBStage = kTapsPerB * kBBytes;
+  static constexpr int kSB0 = (96 * 1024) / kBStage;
   static constexpr int kSB = kSB0 < 2 ? 2 : kSB0 > BC_VAE_SB_MAX ? BC_VAE_SB_MAX : kSB0;
-  static constexpr int kSA0 = (kBudget - kSB * kBBytes) / kABytes;
+  static constexpr int kSA0 = (kBudget - kSB * kBStage) / kABytes;
   static constexpr int kSA = kSA0 < 2 ? 2 : kSA0 > BC_VAE_SA_MAX ? BC_VAE_SA_MAX : kSA0;
   static constexpr int kAcc = 2 * R * NMAX <= 512 ? 2 : 1;  // double-buffered accumulators when they fit
   static constexpr int kCols = kAcc * R * NMAX;
   static constexpr int kTmemCols = kCols <= 32 ? 32 : kCols <= 64 ? 64 : kCols <= 128 ? 128 : kCols <= 256 ? 256 : 512;
-  static constexpr size_t kSmem = 1024 + (size_t)kSA * kABytes + (size_t)kSB * kBBytes + 512 + 1024;
+  static constexpr size_t kSmem = 1024 + (size_t)kSA * kABytes + (size_t)kSB * kBStage + 512 + 1024;
   static_assert(kCols <= 512, "TMEM holds 512 fp32 columns");
   static_assert(kSmem <= 227 * 1024, "shared memory");
 };
@@ -77,6 +85,7 @@ struct ConvParams {
   int cin, cout, ncol;  // ncol: output channels per unit (<= NMAX)
   int kt, kh, kw, n_cc;
   int num_mg, num_ng;
+  int ilv_t, ilv_per;   // unit order: ilv_t frame slots of ilv_per row groups (see unit_of)
   const float* bias;
   const float* res;
   float* out32;
@@ -130,6 +139,21 @@ __device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t threads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
 }
 
+// Execution order of the units (R 128-row tiles x ncol channels): unit u
+// -> row group mg = (u_m % ilv_t) * ilv_per + u_m / ilv_t.  With ilv_t = the
+// conv's output frames and ilv_per ~ row groups per frame, the ~148 units in
+// flight cover the same spatial rows of EVERY frame, so the kt = 0/1/2 taps
+// (frames f-2, f-1, f of the input) are read while the neighbouring frames'
+// units still hold them in L2 -- in plain row order the three input windows
+// are a frame (40-80 MB) apart and each input row came from DRAM once per
+// kt.  Returns false for the padding slots of the last frame.
+__device__ __forceinline__ bool unit_of(const ConvParams& p, int u, int& mg, int& ng) {
+  const int um = u / p.num_ng;
+  ng = u - um * p.num_ng;
+  mg = (um % p.ilv_t) * p.ilv_per + um / p.ilv_t;
+  return mg < p.num_mg;
+}
+
 template <int CK, int R, int NMAX>
 __global__ void __launch_bounds__(kConvThreads, 1)
     conv_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_a8,
@@ -140,17 +164,17 @@ __global__ void __launch_bounds__(kConvThreads, 1)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sa = smem;
   uint8_t* sb = smem + SA * Cfg::kABytes;
-  uint64_t* afull = reinterpret_cast<uint64_t*>(sb + SB * Cfg::kBBytes);
+  uint64_t* afull = reinterpret_cast<uint64_t*>(sb + SB * Cfg::kBStage);
   uint64_t* aempty = afull + SA;
   uint64_t* bfull = aempty + SA;
   uint64_t* bempty = bfull + SB;
   uint64_t* tfull = bempty + SB;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-  float* ss_part = reinterpret_cast<float*>(smem + SA * Cfg::kABytes + SB * Cfg::kBBytes + 512);  // [4][2][32]
+  float* ss_part = reinterpret_cast<float*>(smem + SA * Cfg::kABytes + SB * Cfg::kBStage + 512);  // [4][2][32]
 
   const uint32_t warp = warp_id();
-  const int n_units = p.num_mg * p.num_ng;
+  const int n_units = p.ilv_t * p.ilv_per * p.num_ng;
   if (warp == 0 && lane_id() == 0) {
     tma_prefetch(&map_a);
     tma_prefetch(&map_a8);
@@ -181,7 +205,8 @@ __global__ void __launch_bounds__(kConvThreads, 1)
       uint32_t pa = 0, pb = 0;
       const uint32_t a_bytes = (R * 128 + 8) * RB, b_bytes = p.ncol * RB;
       for (int unit = blockIdx.x; unit < n_units; unit += gridDim.x) {
-        const int mg = unit / p.num_ng, ng = unit - mg * p.num_ng;
+        int mg, ng;
+        if (!unit_of(p, unit, mg, ng)) continue;
         const int o0 = p.row0 + mg * R * 128, n0 = ng * p.ncol;
         for (int kt = 0; kt < p.kt; ++kt)
           for (int kh = 0; kh < p.kh; ++kh)
@@ -197,15 +222,16 @@ __global__ void __launch_bounds__(kConvThreads, 1)
                 ia = 0;
                 pa ^= 1;
               }
+              mbar_wait(&bempty[ib], pb ^ 1);
+              mbar_arrive_expect_tx(&bfull[ib], p.kw * b_bytes);
               for (int kw = 0; kw < p.kw; ++kw) {
-                mbar_wait(&bempty[ib], pb ^ 1);
-                mbar_arrive_expect_tx(&bfull[ib], b_bytes);
                 const int tap = (kt * p.kh + kh) * p.kw + kw;
-                tma_load_2d(sb + ib * Cfg::kBBytes, &map_b, &bfull[ib], tap * p.cin + cc * CK, n0);
-                if (++ib == SB) {
-                  ib = 0;
-                  pb ^= 1;
-                }
+                tma_load_2d(sb + ib * Cfg::kBStage + kw * Cfg::kBBytes, &map_b, &bfull[ib], tap * p.cin + cc * CK,
+                            n0);
+              }
+              if (++ib == SB) {
+                ib = 0;
+                pb ^= 1;
               }
             }
       }
@@ -215,9 +241,12 @@ __global__ void __launch_bounds__(kConvThreads, 1)
     const int stages = p.kt * p.kh * p.n_cc;
     int ia = 0, ib = 0, it = 0;
     uint32_t pa = 0, pb = 0;
-    for (int unit = blockIdx.x; unit < n_units; unit += gridDim.x, ++it) {
+    for (int unit = blockIdx.x; unit < n_units; unit += gridDim.x) {
+      int mg, ng;
+      if (!unit_of(p, unit, mg, ng)) continue;
       const int acc = Cfg::kAcc == 2 ? (it & 1) : 0;
       const uint32_t acc_phase = Cfg::kAcc == 2 ? ((it >> 1) & 1) : (it & 1);
+      ++it;
       const uint32_t d_base = tmem_base + acc * (R * NMAX);
       mbar_wait(&tempty[acc], acc_phase ^ 1);
       tc_fence_after();
@@ -225,26 +254,25 @@ __global__ void __launch_bounds__(kConvThreads, 1)
         mbar_wait(&afull[ia], pa);
         tc_fence_after();
         const uint32_t a0 = smem_u32(sa + ia * Cfg::kABytes);
-        for (int kw = 0; kw < p.kw; ++kw) {
-          mbar_wait(&bfull[ib], pb);
-          tc_fence_after();
-          if (elect_one()) {
-            const uint32_t b0 = smem_u32(sb + ib * Cfg::kBBytes);
+        mbar_wait(&bfull[ib], pb);
+        tc_fence_after();
+        if (elect_one()) {
+          const uint32_t b0 = smem_u32(sb + ib * Cfg::kBStage);
+          for (int kw = 0; kw < p.kw; ++kw)
 #pragma unroll
             for (int r = 0; r < R; ++r)
 #pragma unroll
               for (int k = 0; k < CK / 16; ++k)
                 mma_bf16_ss(d_base + r * NMAX, desc_swz(a0 + (r * 128 + kw) * RB + k * 32, RB),
-                            desc_swz(b0 + k * 32, RB), idesc, (s | kw | k) != 0);
-            mma_commit(&bempty[ib]);
-            if (kw == p.kw - 1) mma_commit(&aempty[ia]);
-            if (kw == p.kw - 1 && s == stages - 1) mma_commit(&tfull[acc]);
-          }
-          __syncwarp();
-          if (++ib == SB) {
-            ib = 0;
-            pb ^= 1;
-          }
+                            desc_swz(b0 + kw * Cfg::kBBytes + k * 32, RB), idesc, (s | kw | k) != 0);
+          mma_commit(&bempty[ib]);
+          mma_commit(&aempty[ia]);
+          if (s == stages - 1) mma_commit(&tfull[acc]);
+        }
+        __syncwarp();
+        if (++ib == SB) {
+          ib = 0;
+          pb ^= 1;
         }
         if (++ia == SA) {
           ia = 0;
@@ -267,11 +295,13 @@ __global__ void __launch_bounds__(kConvThreads, 1)
     const float norm_scale = sqrtf((float)p.cout);
     float* ssx = ss_part + quad * 64;
     int it = 0;
-    for (int unit = blockIdx.x; unit < n_units; unit += gridDim.x, ++it) {
-      const int mg = unit / p.num_ng, ng = unit - mg * p.num_ng;
+    for (int unit = blockIdx.x; unit < n_units; unit += gridDim.x) {
+      int mg, ng;
+      if (!unit_of(p, unit, mg, ng)) continue;
       const int o0 = p.row0 + mg * R * 128, n0 = ng * p.ncol;
       const int acc = Cfg::kAcc == 2 ? (it & 1) : 0;
       const uint32_t acc_phase = Cfg::kAcc == 2 ? ((it >> 1) & 1) : (it & 1);
+      ++it;
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
 #pragma unroll 1
@@ -388,6 +418,12 @@ int conv_launch(const bc_vae_conv_args& a, int ncol, cudaStream_t st) {
   const int tiles = (p.rows + 127) / 128;
   p.num_mg = (tiles + R - 1) / R;
   p.num_ng = a.cout / ncol;
+  static const int ilv_env = [] {
+    const char* e = getenv("BC_VAE_ILV");
+    return e ? atoi(e) : 1;
+  }();
+  p.ilv_t = (ilv_env && a.kt > 1 && a.n_out_frames > 1 && p.num_mg >= a.n_out_frames) ? a.n_out_frames : 1;
+  p.ilv_per = (p.num_mg + p.ilv_t - 1) / p.ilv_t;
   p.bias = a.bias;
   p.res = a.res;
   p.out32 = a.out32;
@@ -410,7 +446,7 @@ int conv_launch(const bc_vae_conv_args& a, int ncol, cudaStream_t st) {
                                  (int)Cfg::kSmem));
     return BC_OK;
   }));
-  const int units = p.num_mg * p.num_ng;
+  const int units = p.ilv_t * p.ilv_per * p.num_ng;
   const int sms = current_sm_count();
   conv_kernel<CK, R, NMAX><<<units < sms ? units : sms, kConvThreads, Cfg::kSmem, st>>>(ma, ma8, mb, p);
   BC_LAUNCHED();
