@@ -694,10 +694,16 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
           }
           mbar_wait(&ring_empty[slot], ph ^ 1);
+#ifdef BC_ABL_HALFKV  // timing experiment only (wrong numerics): half the K/V bytes from L2
+          mbar_arrive_expect_tx(&ring_full[slot], kHalf);
+          uint8_t* dst = smem + Smem::ring + slot * kTile;
+          tma_load_4d(dst, &map_kv, &ring_full[slot], 0, w.head, t0, mat);
+#else
           mbar_arrive_expect_tx(&ring_full[slot], kTile);
           uint8_t* dst = smem + Smem::ring + slot * kTile;
           tma_load_4d(dst, &map_kv, &ring_full[slot], 0, w.head, t0, mat);
           tma_load_4d(dst + kHalf, &map_kv, &ring_full[slot], 64, w.head, t0, mat);
+#endif
         }
       }
     }
