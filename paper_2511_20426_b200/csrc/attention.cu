@@ -187,7 +187,21 @@ struct SoftmaxBars {
   uint64_t* s_empty;
   uint64_t* p_full;
   uint64_t* o_ready;
+  // CTA-pair kernel: s_empty / p_full / o_free live in the LEADER CTA and
+  // count one elected arrival per warp of both CTAs (cluster addresses)
+  uint32_t s_empty_cl = 0, p_full_cl = 0, o_free_cl = 0;
 };
+
+// arrive on a softmax-side barrier: every thread locally (count 128), or one
+// elected lane per warp on the leader's barrier (CTA pairs, count 8)
+__device__ __forceinline__ void sm_arrive(uint64_t* local, uint32_t cluster_addr) {
+  if (cluster_addr) {
+    __syncwarp();
+    if (lane_id() == 0) cl_arrive(cluster_addr);
+  } else {
+    mbar_arrive(local);
+  }
+}
 
 
 // One softmax warpgroup: 128 threads, thread <-> query row of its tile.
@@ -219,7 +233,7 @@ __device__ __forceinline__ void softmax_tile(const AttnParams& prm, uint32_t tme
         for (int i = 0; i < 32; ++i) s[k * 32 + i] = __uint_as_float(r[k][i]);
     }
     tc_fence_before();
-    mbar_arrive(b.s_empty);  // S buffer may now be overwritten by the next QK^T
+    sm_arrive(b.s_empty, b.s_empty_cl);  // S buffer may now be overwritten by the next QK^T
     if (quad == 0) ATRACE(4 + tile_x * 8, j);
 #ifdef BC_ATTN_NOSOFTMAX  // timing experiment only: MMA/TMA skeleton
     if (j > 0) mbar_wait(b.o_ready, (j - 1) & 1);
@@ -234,7 +248,7 @@ __device__ __forceinline__ void softmax_tile(const AttnParams& prm, uint32_t tme
 #endif
     fence_async_shared();
     tc_fence_before();
-    mbar_arrive(b.p_full);
+    sm_arrive(b.p_full, b.p_full_cl);
     continue;
 #endif
     if (valid < kKeys) {     // ragged last tile of a slot (warp-uniform)
@@ -350,7 +364,7 @@ __device__ __forceinline__ void softmax_tile(const AttnParams& prm, uint32_t tme
     l_sum = l_sum * alpha + ((sa + sc) + (sb + sd));
     fence_async_shared();
     tc_fence_before();
-    mbar_arrive(b.p_full);
+    sm_arrive(b.p_full, b.p_full_cl);
     if (quad == 0) ATRACE(3 + tile_x * 8, j);
   }
   // epilogue: O / l -> bf16
@@ -386,7 +400,7 @@ __device__ __forceinline__ void softmax_tile(const AttnParams& prm, uint32_t tme
   }
   if (o_free) {  // O is read out: the next work item's first PV may overwrite it
     tc_fence_before();
-    mbar_arrive(o_free);
+    sm_arrive(o_free, b.o_free_cl);
   }
 }
 
@@ -573,6 +587,236 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   if (warp == 1) tmem_dealloc<512>(tmem);
+}
+
+// CTA-pair variant (cluster of 2 on one TPC, tcgen05 cta_group::2): the two
+// CTAs hold two 128-row query tiles each (4 tiles = 512 query rows of one
+// entry and head per cluster) and share every K/V tile: QK^T runs as M=256
+// MMAs with the key tile's 128 rows split 64 / 64 across the pair, PV as
+// M=256 MMAs with V's 128 head-dim columns split 64 / 64.  Each CTA loads
+// only ITS half of every K/V tile (16 KB instead of 32 KB per tile), so the
+// L2 -> SM traffic, the TMA shared-memory writes and the tensor core's
+// B-operand reads per SM halve -- measured, halving the K/V bytes (numerics
+// aside, BC_ABL_HALFKV) lets the power-capped GPU clock 8% higher.  The
+// leader CTA issues all MMAs; TMA loads of both CTAs complete on the
+// leader's barriers; MMA completions are multicast to both CTAs; each CTA's
+// softmax warps signal the leader with one elected arrival per warp.
+// Per-row arithmetic and key order are those of attn_kernel (the pair MMA
+// computes each output element as the single-CTA one does): bit-identical.
+constexpr int kRingP = 6;                 // half-tile ring slots (16 KB each)
+constexpr int kItemP = 16 * 1024;         // a CTA's half of a K or V tile
+constexpr int kHalfK = 64 * 128;          // one 64-column d-half of a 64-key K half-tile (8 KB)
+static_assert(Smem::pa - Smem::ring == kRingP * kItemP, "pair ring fits the single-CTA ring");
+
+template <int kPoly>
+__global__ void __launch_bounds__(kThreads, 1)
+    attn_pair_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_kh,
+                     const __grid_constant__ CUtensorMap map_kv, AttnParams prm) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Smem::bars);
+  uint64_t* q_full = bars + 0;
+  uint64_t* ring_full = bars + 1;    // [6] (leader's are the ones waited on)
+  uint64_t* ring_empty = bars + 7;   // [6] (both CTAs: multicast commits)
+  uint64_t* s_full = bars + 13;      // [2] (both CTAs)
+  uint64_t* s_empty = bars + 15;     // [2] (leader: 8 warp arrivals)
+  uint64_t* p_full = bars + 17;      // [2] (leader: 8 warp arrivals)
+  uint64_t* o_ready = bars + 19;     // [2] (both CTAs)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 24);
+
+  const uint32_t rank = cl_rank();
+  const bool leader = rank == 0;
+  const int item = blockIdx.x >> 1, e = blockIdx.y, head = blockIdx.z;
+  if (prm.q_lo[e] + item * 4 * kRows >= prm.q_hi[e]) return;  // same decision in both CTAs
+  const int q0 = prm.q_lo[e] + (item * 4 + (int)rank * 2) * kRows;  // this CTA's tile A (B = +128)
+  const int n_vis = prm.n_vis[e];
+  const int tiles_per_slot = (prm.kv_tokens + kKeys - 1) / kKeys;
+  const int n_tiles = n_vis * tiles_per_slot;
+  const uint32_t warp = warp_id();
+
+  if (warp == 0 && lane_id() == 0) {
+    tma_prefetch(&map_q);
+    tma_prefetch(&map_kh);
+    tma_prefetch(&map_kv);
+    mbar_init(q_full, 1);
+    for (int i = 0; i < kRingP; ++i) {
+      mbar_init(&ring_full[i], 1);
+      mbar_init(&ring_empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&s_full[i], 1);
+      mbar_init(&s_empty[i], 8);
+      mbar_init(&p_full[i], 8);
+      mbar_init(&o_ready[i], 1);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot))
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  cl_sync();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp < 4) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegsCtl));
+  if (warp == 0) {
+    if (lane_id() == 0) {
+      // Q: both CTAs' two tiles complete on the leader's q_full (absent
+      // tiles load rows past the entry, or TMA's zero fill, and are never
+      // stored)
+      const uint32_t lq = cl_map(q_full, 0);
+      if (leader) mbar_arrive_expect_tx(q_full, 2 * 2 * kTile);
+      const int qrow = prm.q_row[e] + (q0 - prm.q_lo[e]);
+      tma_load_3d_pair(smem + Smem::qa, &map_q, lq, 0, head, qrow);
+      tma_load_3d_pair(smem + Smem::qa + kHalf, &map_q, lq, 64, head, qrow);
+      tma_load_3d_pair(smem + Smem::qb, &map_q, lq, 0, head, qrow + kRows);
+      tma_load_3d_pair(smem + Smem::qb + kHalf, &map_q, lq, 64, head, qrow + kRows);
+      for (int i = 0; i < 2 * n_tiles; ++i) {
+        int j, is_v;
+        ring_item(i, n_tiles, j, is_v);
+        const int slot = i % kRingP;
+        const uint32_t ph = (i / kRingP) & 1;
+        const int kv_slot = prm.vis_slot[e][j / tiles_per_slot];
+        const int t0 = (j % tiles_per_slot) * kKeys;
+        const int mat = prm.mat_base + kv_slot * prm.mat_stride + (is_v ? prm.v_offset : 0);
+        if (!is_v && prm.flags && (j % tiles_per_slot) == 0) {
+          const uint32_t need = prm.need[e][j / tiles_per_slot];
+          if (need) {  // K/V rows of this block come from peer GPUs: wait for each producer
+            const uint32_t ep = need >> 8;
+            const uint32_t* f = prm.flags + (size_t)(prm.flag_base + kv_slot) * prm.n_ranks;
+            for (uint32_t m = need & 0xffu; m; m &= m - 1) spin_until_geq(f + (__ffs(m) - 1), ep, 256);
+            asm volatile("fence.proxy.async.global;" ::: "memory");
+          }
+        }
+        mbar_wait(&ring_empty[slot], ph ^ 1);
+        const uint32_t lb = cl_map(&ring_full[slot], 0);
+        if (leader) mbar_arrive_expect_tx(&ring_full[slot], 2 * kItemP);
+        uint8_t* dst = smem + Smem::ring + slot * kItemP;
+        if (!is_v) {  // K: this CTA's 64 keys, both d halves
+          tma_load_4d_pair(dst, &map_kh, lb, 0, head, t0 + 64 * (int)rank, mat);
+          tma_load_4d_pair(dst + kHalfK, &map_kh, lb, 64, head, t0 + 64 * (int)rank, mat);
+        } else {      // V: all 128 keys, this CTA's 64 head-dim columns
+          tma_load_4d_pair(dst, &map_kv, lb, 64 * (int)rank, head, t0, mat);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (leader) {
+      constexpr uint32_t idesc_qk = idesc_bf16(2 * kRows, kKeys);
+      constexpr uint32_t idesc_pv = idesc_bf16(2 * kRows, kHd, 0, 1);  // B (= V) MN-major
+      const uint32_t sq[2] = {smem_u32(smem + Smem::qa), smem_u32(smem + Smem::qb)};
+      const uint32_t sp[2] = {smem_u32(smem + Smem::pa), smem_u32(smem + Smem::pb)};
+      auto ring_slot = [&](int i) { return smem_u32(smem + Smem::ring + (i % kRingP) * kItemP); };
+      auto issue_qk = [&](int x, int j) {
+        if (elect_one()) {
+          const uint32_t sk = ring_slot(kpos(j));
+#pragma unroll
+          for (int k = 0; k < kHd / 16; ++k) {
+            const uint32_t aoff = (k >> 2) * kHalf + (k & 3) * 32;
+            const uint32_t boff = (k >> 2) * kHalfK + (k & 3) * 32;
+            mma2_bf16_ss(tmem + x * 128, desc_sw128(sq[x] + aoff, 16, 1024), desc_sw128(sk + boff, 16, 1024),
+                         idesc_qk, k != 0);
+          }
+          mma2_commit(&s_full[x]);
+        }
+        __syncwarp();
+      };
+      auto issue_pv = [&](int x, int j) {
+        if (elect_one()) {
+          const uint32_t sv = ring_slot(vpos(j, n_tiles));
+#pragma unroll
+          for (int k = 0; k < kKeys / 16; ++k) {
+            const uint32_t aoff = (k >> 2) * kHalf + (k & 3) * 32;
+            mma2_bf16_ss(tmem + 256 + x * 128, desc_sw128(sp[x] + aoff, 16, 1024),
+                         desc_sw128(sv + k * 2048, 16, 1024), idesc_pv, (j | k) != 0);
+          }
+          mma2_commit(&o_ready[x]);
+        }
+        __syncwarp();
+      };
+      auto release = [&](int i) {
+        if (elect_one()) mma2_commit(&ring_empty[i % kRingP]);
+        __syncwarp();
+      };
+      auto ring_wait = [&](int i) { mbar_wait(&ring_full[i % kRingP], (i / kRingP) & 1); };
+#ifdef BC_ATTN_TRACE
+      const long long trc0 = clock64();
+      long long tw_se = 0, tw_p = 0, tw_k = 0, tw_v = 0, t_iq = 0, t_ip = 0;
+#define PT(v) const long long v = clock64()
+#define PA(acc, v) acc += clock64() - v
+#else
+#define PT(v)
+#define PA(acc, v)
+#endif
+      mbar_wait(q_full, 0);
+      if (n_tiles > 0) {
+        ring_wait(0);
+        tc_fence_after();
+        for (int x = 0; x < 2; ++x) issue_qk(x, 0);
+        release(0);
+      }
+      for (int j = 0; j < n_tiles; ++j) {
+        const bool next = j + 1 < n_tiles;
+        for (int x = 0; x < 2; ++x) {
+          if (next) {
+            PT(a0);
+            cl_wait(&s_empty[x], j & 1);  // both CTAs' softmax x has read S_x(j)
+            PA(tw_se, a0);
+            PT(a1);
+            if (x == 0) ring_wait(kpos(j + 1));
+            PA(tw_k, a1);
+            tc_fence_after();
+            PT(a2);
+            issue_qk(x, j + 1);
+            PA(t_iq, a2);
+            if (x == 1) release(kpos(j + 1));
+          }
+          PT(a3);
+          cl_wait(&p_full[x], j & 1);
+          PA(tw_p, a3);
+          PT(a4);
+          if (x == 0) ring_wait(vpos(j, n_tiles));
+          PA(tw_v, a4);
+          tc_fence_after();
+          PT(a5);
+          issue_pv(x, j);
+          PA(t_ip, a5);
+        }
+        release(vpos(j, n_tiles));
+      }
+#ifdef BC_ATTN_TRACE
+      const int cid = (blockIdx.z * gridDim.y + blockIdx.y) * (gridDim.x >> 1) + (blockIdx.x >> 1);
+      if (prm.trace && lane_id() == 0 && cid < 256) {
+        unsigned long long* r = prm.trace + 32 * 64 + cid * 8;
+        r[0] = clock64() - trc0;
+        r[1] = 0;
+        r[2] = 4ull * n_tiles;  // (query tile, key tile) steps of the cluster
+        r[3] = tw_p;
+        r[4] = tw_k + tw_v;
+        r[5] = tw_se;
+        r[6] = t_iq;
+        r[7] = t_ip;
+      }
+#endif
+#undef PT
+#undef PA
+    }
+  } else if (warp >= 4) {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegsSoftmax));
+    const int x = (warp >= 8) ? 1 : 0;
+    SoftmaxBars b{&s_full[x], &s_empty[x], &p_full[x], &o_ready[x]};
+    b.s_empty_cl = cl_map(&s_empty[x], 0);
+    b.p_full_cl = cl_map(&p_full[x], 0);
+    softmax_tile<kPoly>(prm, tmem + x * 128, tmem + 256 + x * 128, smem + (x ? Smem::pb : Smem::pa), b, n_tiles,
+                        tiles_per_slot, warp & 3, q0 + x * kRows, e, head, x);
+  }
+  tc_fence_before();
+  cl_sync();
+  tc_fence_after();
+  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
 }
 
 // Balanced persistent variant: one CTA per SM runs a
@@ -1129,6 +1373,47 @@ int attention_run(const AttnArgs& a, cudaStream_t st) {
     return BC_OK;
   }));
   if (max_pairs == 0) return BC_OK;  // no query rows in this slice
+  // CTA-pair kernel (BC_ATTN_PAIR=1): clusters of 2 sharing each K/V tile
+  static const int pair_env = [] {
+    const char* env = getenv("BC_ATTN_PAIR");
+    return env ? atoi(env) : 0;
+  }();
+  if (pair_env && poly == 0) {
+    static PerDeviceOnce pair_attrs;
+    BC_RC(per_device_once(pair_attrs, [&]() -> int {
+      BC_CUDA(cudaFuncSetAttribute(attn_pair_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   Smem::total + 1024));
+      return BC_OK;
+    }));
+    CUtensorMap mkh;
+    {
+      cuuint64_t dims[4] = {kHd, (cuuint64_t)a.heads, (cuuint64_t)a.kv_tokens, (cuuint64_t)a.n_mats};
+      cuuint64_t strides[3] = {kHd * 2, row_bytes, row_bytes * (uint64_t)a.kv_tokens};
+      cuuint32_t box[4] = {64, 1, kKeys / 2, 1};
+      int rc = encode(&mkh, a.kv_base, 4, dims, strides, box);
+      if (rc) return rc;
+    }
+    int max_items = 0;
+    for (int e = 0; e < a.n_entries; ++e) {
+      const int items = (p.q_hi[e] - p.q_lo[e] + 4 * kRows - 1) / (4 * kRows);
+      max_items = items > max_items ? items : max_items;
+    }
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(2 * max_items, a.n_entries, a.heads);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = Smem::total + 1024;
+    cfg.stream = st;
+    cudaLaunchAttribute attrs[1];
+    attrs[0].id = cudaLaunchAttributeClusterDimension;
+    attrs[0].val.clusterDim.x = 2;
+    attrs[0].val.clusterDim.y = 1;
+    attrs[0].val.clusterDim.z = 1;
+    cfg.attrs = attrs;
+    cfg.numAttrs = 1;
+    BC_CUDA(cudaLaunchKernelEx(&cfg, attn_pair_kernel<0>, mq, mkh, mkv, p));
+    BC_LAUNCHED();
+    return BC_OK;
+  }
   if (g_attn_balance < 0) {
     const char* env = getenv("BC_ATTN_BALANCE");
     g_attn_balance = env ? atoi(env) : 1;
