@@ -2,6 +2,7 @@
 with nvidia-smi sampling: SM clock, power and throttle reasons under load,
 and TFLOP/s per MHz (the clock-independent figure to compare variants by).
 usage: python scripts/attn_power.py [lib.so ...]"""
+import os
 import subprocess
 import sys
 import threading
@@ -69,4 +70,4 @@ def run(lib, seconds=4.0, n_ent=5, n_vis=13, T=4680, heads=12):
 if __name__ == "__main__":
     libs = sys.argv[1:] or [N.LIB_PATH]
     for lib in libs:
-        run(lib)
+        run(lib, T=int(os.environ.get("BC_POWER_T", "4680")))
