@@ -13,7 +13,9 @@ tests/test_oracle_wan_torch.py), TF32 off, on the same GPU:
   per-step tolerance), v = (x_t - x0)/sigma reported beside it;
 * free-running 13-block runs, o=1 (bidirectional cascade) and o=5 (the
   sequential rollout), final latents rel-L2 <= 1e-2 per block;
-* Wan2.1-14B geometry at its full 40 layers on a reduced latent grid.
+* Wan2.1-14B geometry at its full 40 layers on a reduced latent grid;
+* config 5 (LongLive-style) at full 1.3B depth on a reduced latent grid:
+  80 blocks, rolling window without sink, cascade-mode prompt switches.
 
 Margins go to $BC_PARITY_REPORT (JSON) when set (profiles/r2_wan_parity_full.json).
 """
@@ -137,16 +139,16 @@ def _teacher_forced(monkeypatch, cfg, weights, tap):
     return rows
 
 
-def _free_running(monkeypatch, cfg, weights):
+def _free_running(monkeypatch, cfg, weights, switches=()):
     import paper_2511_20426_b200 as bc
     from paper_2511_20426_b200 import engine
     from oracle.loop import wan_torch_oracle_runtime
-    gpu = bc.run_cascade(cfg, "a lighthouse in a storm", weights=weights)
+    gpu = bc.run_cascade(cfg, "a lighthouse in a storm", weights=weights, switches=list(switches))
     weights.runtime().release_cached()
     _free()
     with monkeypatch.context() as m:
         m.setattr(engine, "_runtime_for", wan_torch_oracle_runtime(weights.t))
-        cpu = bc.run_cascade(cfg, "a lighthouse in a storm", weights=weights)
+        cpu = bc.run_cascade(cfg, "a lighthouse in a storm", weights=weights, switches=list(switches))
     assert gpu.emitted_order == cpu.emitted_order
     assert [e.pool_state for e in gpu.trace.events] == [e.pool_state for e in cpu.trace.events]
     errs = [rel(gpu.outputs[b], cpu.outputs[b]) for b in range(cfg.num_blocks)]
@@ -217,3 +219,23 @@ def test_14b_full_depth_free_running(w14, monkeypatch):
     errs = _free_running(monkeypatch, cfg, w)
     REPORT["14b_L40_16x32_run_o1_bidirectional"] = errs
     assert max(errs) <= RUN_TOL, errs
+
+
+def test_13b_longlive_full_depth(monkeypatch):
+    """BASELINE config 5 at the 1.3B model's full 30 layers (16x32 latent
+    grid): 80 blocks = 240 latent frames, rolling W=7 window without sink,
+    cascade-mode prompt switches at blocks 20 / 40 / 60 (text K/V swap, no
+    KV recache) -- free-running, every block vs the fp32 oracle."""
+    import paper_2511_20426_b200 as bc
+    from paper_2511_20426_b200.wan import WanWeights
+    _free()
+    cfg = bc.wan_config("1.3b", latent_height=16, latent_width=32, total_frames=240, offset=1,
+                        attention_mode="bidirectional", window_blocks=7, sink_blocks=0)
+    w = WanWeights.random(cfg, 7)
+    sw = [bc.SwitchSpec(f"a lighthouse in a storm, scene {k}", "cascade", at_block=k) for k in (20, 40, 60)]
+    try:
+        errs = _free_running(monkeypatch, cfg, w, switches=sw)
+    finally:
+        w.runtime().release_cached()
+    REPORT["1.3b_L30_16x32_longlive_80blocks_sink0_switches"] = errs
+    assert len(errs) == 80 and max(errs) <= RUN_TOL, max(errs)
