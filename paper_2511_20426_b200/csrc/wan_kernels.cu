@@ -639,6 +639,17 @@ int launch_rope_tables(float2* tf, int max_frames, float2* th, int hp, float2* t
   return BC_OK;
 }
 
+__global__ void flag_writes_kernel(FlagWrites f) {
+  __threadfence_system();
+  for (int i = 0; i < f.n; ++i) st_release_sys(f.addr[i], f.v);
+}
+
+int launch_flag_writes(const FlagWrites& f, cudaStream_t st) {
+  flag_writes_kernel<<<1, 1, 0, st>>>(f);
+  BC_LAUNCHED();
+  return BC_OK;
+}
+
 int launch_signal_done(const PeerArgs& p, cudaStream_t st) {
   signal_done_kernel<<<1, 1, 0, st>>>(p);
   BC_LAUNCHED();

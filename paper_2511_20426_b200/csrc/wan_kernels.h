@@ -95,6 +95,15 @@ int launch_head_update(const float* Y, int n, int T, int F, int H, int W, const 
                        cudaStream_t st);
 int launch_mod_combine(const float* base, const float* e0, int L, int n, int d, float* out, cudaStream_t st);
 int launch_signal_done(const PeerArgs& p, cudaStream_t st);
+// release-store `v` to up to kMaxFlagWrites (peer) flag words from one
+// thread after a system fence: the fallback of cuStreamWriteValue32
+constexpr int kMaxFlagWrites = 64;
+struct FlagWrites {
+  uint32_t* addr[kMaxFlagWrites];
+  int n;
+  uint32_t v;
+};
+int launch_flag_writes(const FlagWrites& f, cudaStream_t st);
 int launch_rope_tables(float2* tf, int max_frames, float2* th, int hp, float2* tw, int wp, cudaStream_t st);
 constexpr int kRopeMaxFrames = 4096;
 int launch_check_finite(const EntryPtrs& lat, int n, int n_el, int32_t* status, cudaStream_t st);

@@ -19,6 +19,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <stdlib.h>
@@ -211,6 +212,28 @@ PFN_cuStreamWriteValue32_v11070 write_value32() {
                : nullptr;
   }();
   return fn;
+}
+
+// Publish `v` into (peer) flag words in stream order.  cuStreamWriteValue32
+// (a memory barrier, then the write, executed by the stream itself) is the
+// default; if the driver rejects a peer address the writes go through a
+// 1-thread kernel (system fence + release stores) from then on -- never
+// lost, only a launch more per publication.
+std::atomic<int> g_memops_ok{getenv("BC_NO_MEMOP_WRITES") ? 0 : 1};  // env: force the kernel path (tests)
+int write_flags(cudaStream_t st, const bc::FlagWrites& f) {
+  if (f.n <= 0) return BC_OK;
+  if (g_memops_ok.load(std::memory_order_relaxed)) {
+    auto wv = write_value32();
+    int done = 0;
+    if (wv) {
+      for (; done < f.n; ++done)
+        if (wv((CUstream)st, (CUdeviceptr)f.addr[done], f.v, 0) != CUDA_SUCCESS) break;
+    }
+    if (done == f.n) return BC_OK;
+    (void)cudaGetLastError();
+    g_memops_ok.store(0);
+  }
+  return bc::launch_flag_writes(f, st);
 }
 
 template <typename T>
@@ -519,8 +542,6 @@ int stage_layer_a(bc_wan_ctx* c, int l, cudaStream_t st) {
     // slot's [2][T][d] matrix) into every peer replica, then a stream memory
     // op publishes flags[layer][slot][my_rank] = epoch.  Safe only when the
     // copy runs on a copy engine (see bc_wan_set_peers).
-    auto wv = write_value32();
-    if (!wv) return bc_fail(BC_ERR_CUDA, "cuStreamWriteValue32 unavailable");
     BC_CUDA(cudaEventRecord(c->ev_qk, st));
     BC_CUDA(cudaStreamWaitEvent(c->side, c->ev_qk, 0));
     const size_t row_bytes = (size_t)d * sizeof(__nv_bfloat16);
@@ -545,12 +566,14 @@ int stage_layer_a(bc_wan_ctx* c, int l, cudaStream_t st) {
         }
       }
     }
+    bc::FlagWrites fw{};
+    fw.v = S.epoch;
     for (int pp = 0; pp < c->peers.n_peers; ++pp)
-      for (int k = 0; k < n_used; ++k) {
+      for (int k = 0; k < n_used && fw.n < bc::kMaxFlagWrites; ++k) {
         const size_t fi = ((size_t)l * dm.n_slots + S.batch.slot[e_used[k]]) * c->peers.n_ranks + c->peers.my_rank;
-        CUresult rr = wv((CUstream)c->side, (CUdeviceptr)(c->peers.peer_flags[pp] + fi), S.epoch, 0);
-        if (rr != CUDA_SUCCESS) return bc_fail(BC_ERR_CUDA, "cuStreamWriteValue32 failed (%d)", (int)rr);
+        fw.addr[fw.n++] = c->peers.peer_flags[pp] + fi;
       }
+    RC(write_flags(c->side, fw));
   }
   return BC_OK;
 }
@@ -600,17 +623,17 @@ int stage_head(bc_wan_ctx* c, cudaStream_t st) {
     RC(timed(kGemm, 2.0 * R * 64.0 * d, 0.0, st, [&] { return gemm(c->xn, p.head_w, y, R, 64, d, bc::kEpiStoreF32, p.head_b, nullptr, 0, 1, st); }));
   }
   if (S.rows_mode) {
-    auto wv = write_value32();
-    if (!wv) return bc_fail(BC_ERR_CUDA, "cuStreamWriteValue32 unavailable");
     BC_CUDA(cudaEventRecord(c->ev_qk, st));
     BC_CUDA(cudaStreamWaitEvent(c->side, c->ev_qk, 0));
+    bc::FlagWrites fw{};
+    fw.v = S.epoch;
     for (int pp = 0; pp < c->peers.n_peers; ++pp) {
       if (R > 0)
         BC_CUDA(cudaMemcpyAsync(static_cast<float*>(c->peers.peer_y[pp]) + (size_t)S.row0 * 64, y,
                                 (size_t)R * 64 * sizeof(float), cudaMemcpyDeviceToDevice, c->side));
-      CUresult rr = wv((CUstream)c->side, (CUdeviceptr)(c->peers.peer_yready[pp] + c->peers.my_rank), S.epoch, 0);
-      if (rr != CUDA_SUCCESS) return bc_fail(BC_ERR_CUDA, "cuStreamWriteValue32 failed (%d)", (int)rr);
+      if (fw.n < bc::kMaxFlagWrites) fw.addr[fw.n++] = c->peers.peer_yready[pp] + c->peers.my_rank;
     }
+    RC(write_flags(c->side, fw));
   }
   return BC_OK;
 }
@@ -899,13 +922,14 @@ extern "C" int bc_copy_async(void* dst, const void* src, int64_t bytes, void* st
 }
 
 extern "C" int bc_stream_write_u32(void* addr, uint32_t value, void* stream) {
-  auto wv = write_value32();
-  if (!wv) return bc_fail(BC_ERR_CUDA, "cuStreamWriteValue32 unavailable");
+  if (!addr) return bc_fail(BC_ERR_CONTRACT, "bc_stream_write_u32: null address");
   // default flags: a memory fence orders the stream's earlier writes (the
-  // copy) before the flag for every observer
-  const CUresult r = wv((CUstream)stream, (CUdeviceptr)addr, value, CU_STREAM_WRITE_VALUE_DEFAULT);
-  if (r != CUDA_SUCCESS) return bc_fail(BC_ERR_CUDA, "cuStreamWriteValue32 failed (%d)", (int)r);
-  return BC_OK;
+  // copy) before the flag for every observer (kernel fallback: write_flags)
+  bc::FlagWrites fw{};
+  fw.addr[0] = static_cast<uint32_t*>(addr);
+  fw.n = 1;
+  fw.v = value;
+  return write_flags((cudaStream_t)stream, fw);
 }
 
 extern "C" int bc_stream_wait_geq_u32(void* addr, uint32_t value, void* stream) {

@@ -23,6 +23,8 @@ def _rank(rank, world, port, q, mode, shard):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port),
                       BC_TEMPORAL_SHARD=shard.split("+")[0],
                       BC_NOISE_GATHER="1" if shard.endswith("+gather") else "0")
+    if shard.endswith("+kflags"):   # peer flags published by the kernel fallback, not stream memops
+        os.environ["BC_NO_MEMOP_WRITES"] = "1"
     import torch
     import torch.distributed as dist
     torch.cuda.set_device(0)
@@ -40,7 +42,8 @@ def _rank(rank, world, port, q, mode, shard):
 
 
 @pytest.mark.parametrize("mode,shard", [("bidirectional", "rows"), ("causal", "rows"),
-                                        ("bidirectional", "blocks"), ("bidirectional", "rows+gather")])
+                                        ("bidirectional", "blocks"), ("bidirectional", "rows+gather"),
+                                        ("bidirectional", "rows+kflags")])
 def test_two_processes_one_gpu(mode, shard):
     """rows+gather: the host noise draws are split over the ranks and
     all-gathered (the NCCL path, here over gloo through the host)."""
