@@ -265,6 +265,10 @@ int bc_gemm_bf16(const void* A, const void* B, void* C, int32_t M, int32_t N, in
                  int32_t mode, const float* bias, const float* gate, int32_t gate_stride,
                  int32_t rows_per_gate, void* stream);
 
+/* The tiling bc_gemm_bf16 chooses automatically for this shape / epilogue:
+ * tile width (*bn columns) and CTAs per tile (*cg: 1, or 2 = CTA pair). */
+int bc_gemm_plan(int32_t M, int32_t N, int32_t K, int32_t mode, int32_t* bn, int32_t* cg);
+
 /* Paged flash attention over KV-arena slots (self-attention) or a dense
  * K/V (cross-attention).  q: bf16 [rows][heads][128]; out: bf16 same.
  * For entry e, query rows [e*q_per_entry, (e+1)*q_per_entry) attend to the

@@ -132,6 +132,8 @@ _SIGS = {
     "bc_wan_set_text": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
     "bc_wan_step": (C.c_int, [C.c_void_p, C.POINTER(Batch), C.POINTER(WanUpdate),
                               C.c_void_p, C.c_void_p]),
+    "bc_gemm_plan": (C.c_int, [C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.POINTER(C.c_int32),
+                               C.POINTER(C.c_int32)]),
     "bc_gemm_bf16": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32,
                                C.c_int32, C.c_int32, C.c_void_p, C.c_void_p, C.c_int32,
                                C.c_int32, C.c_void_p]),

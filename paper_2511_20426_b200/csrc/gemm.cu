@@ -583,6 +583,16 @@ int gemm_run(const GemmArgs& g, cudaStream_t st) {
 
 }  // namespace bc
 
+// The automatic tiling bc_gemm_bf16 would use (host logic only: the CPU
+// tests pin the choices for the DiT's shapes).
+extern "C" int bc_gemm_plan(int32_t M, int32_t N, int32_t K, int32_t mode, int32_t* bn, int32_t* cg) {
+  if (!bn || !cg || M < 1 || N % 64 || K % 64) return bc_fail(BC_ERR_CONTRACT, "bc_gemm_plan: bad arguments");
+  const bc::Tiling t = bc::gemm_plan(M, N, K, mode & 0xff, 0);
+  *bn = t.bn;
+  *cg = t.cg;
+  return BC_OK;
+}
+
 extern "C" int bc_gemm_bf16(const void* A, const void* B, void* C, int32_t M, int32_t N, int32_t K,
                             int32_t mode, const float* bias, const float* gate, int32_t gate_stride,
                             int32_t rows_per_gate, void* stream) {

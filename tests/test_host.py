@@ -399,3 +399,24 @@ def test_decoded_fps_definitions():
     assert f["e2e_fps_decoded"] == pytest.approx(13 * 12 / 1.25)
     assert f["streaming_fps_decoded"] == pytest.approx((12 / 0.1 + 12 / 0.2) / 2)
     assert decoded_fps(times[:5], 12)["streaming_fps_decoded"] is None
+
+
+@pytest.mark.parametrize("M,N,K,mode,want", [
+    (23400, 4608, 1536, 0, (256, 2)),   # QKV at width 5
+    (23400, 1536, 1536, 3, (192, 2)),   # o / cross-o (gated residual) at width 5
+    (23400, 8960, 1536, 1, (256, 2)),   # FFN1 (GELU)
+    (23400, 1536, 8960, 3, (192, 2)),   # FFN2 (gated residual)
+    (4680, 1536, 1536, 3, (128, 1)),    # width-1 sequential rows: 3 full waves of single tiles
+    (4680, 1536, 8960, 3, (256, 2)),
+    (2925, 1536, 8960, 3, (256, 2)),    # a G = 8 row slice: one wave of pairs
+])
+def test_gemm_tiling_choices(M, N, K, mode, want):
+    """The cost-model tiling (gemm.cu gemm_plan) picks the tilings measured
+    fastest for the DiT's shapes (scripts/gemm_tiling.py,
+    profiles/r2_gemm_tiling.txt); host logic, no GPU needed."""
+    import ctypes
+    from paper_2511_20426_b200 import _native as nat
+    bn, cg = ctypes.c_int32(), ctypes.c_int32()
+    nat.check(nat.lib().bc_gemm_plan(M, N, K, mode, ctypes.byref(bn), ctypes.byref(cg)), "bc_gemm_plan")
+    assert (bn.value, cg.value) == want
+    assert N % bn.value == 0 and (bn.value != 192 or cg.value == 2)
