@@ -293,8 +293,11 @@ __global__ void rope_table_kernel(float2* tf, int max_frames, float2* th, int hp
   }
 }
 
+#ifndef BC_QK_MINB
+#define BC_QK_MINB 3  // resident CTAs per SM the register budget targets
+#endif
 template <int VPL, int WPR>  // bf16x8 (16 B) vectors per lane, warps per row
-__global__ void __launch_bounds__(256) qk_norm_rope_kernel(const __nv_bfloat16* __restrict__ qkv, int rows, int d, int T,
+__global__ void __launch_bounds__(256, BC_QK_MINB) qk_norm_rope_kernel(const __nv_bfloat16* __restrict__ qkv, int rows, int d, int T,
                                     QkArgs a) {
   __shared__ float red[8];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -302,30 +305,11 @@ __global__ void __launch_bounds__(256) qk_norm_rope_kernel(const __nv_bfloat16* 
   const int row = blockIdx.x * (8 / WPR) + slot;
   const int li = wir * 32 + lane;
   const bool active = row < rows;
-  wait_peers_done(a.peer);
   const int lr = active ? row : 0;            // local row (q / qkv buffers)
-  const int rr = a.row0 + lr;                  // global row of the batch
-  const int e = rr / T, t = rr % T;
-  const int hw = a.hp * a.wp;
-  const int fl = t / hw, rem = t % hw;
-  const int f = a.frame0[e] + fl, ph = rem / a.wp, pw = rem % a.wp;
-  // the row's 64 (cos, sin) pairs -- 22 time, 21 height, 21 width -- staged
-  // in shared memory once, so the per-element lookup is one lane-indexed load
-  // (a per-element 3-way table select diverges inside every warp)
-  __shared__ float2 tab[8][64];
-  {
-    const float2* rf = a.rope_f + (size_t)f * 22;
-    const float2* rh = a.rope_h + (size_t)ph * 21;
-    const float2* rw = a.rope_w + (size_t)pw * 21;
-    for (int pi = li; pi < 64; pi += 32 * WPR) tab[slot][pi] = pi < 22 ? rf[pi] : (pi < 43 ? rh[pi - 22] : rw[pi - 43]);
-  }
-  __syncthreads();
-  const size_t mat = (size_t)T * d;
-  __nv_bfloat16* kdst = a.arena + ((size_t)a.mat_base + (size_t)a.slot[e] * 2) * mat + (size_t)t * d;
-  __nv_bfloat16* vdst = kdst + mat;
+  // all of the row's q, k and v loads are issued first -- before the peer
+  // wait (which only guards the arena stores) and the RoPE table staging,
+  // whose L2 latency then overlaps the row's HBM reads
   const __nv_bfloat16* src = qkv + (size_t)lr * 3 * d;
-  // all of the row's q, k and v loads are issued before the first reduction
-  // (3x the bytes in flight per warp of the q-then-k-then-v order)
   uint4 raw[3][VPL];
 #pragma unroll
   for (int which = 0; which < 3; ++which) {
@@ -336,43 +320,77 @@ __global__ void __launch_bounds__(256) qk_norm_rope_kernel(const __nv_bfloat16* 
       raw[which][i] = (active && idx * 8 < d) ? s4[idx] : make_uint4(0u, 0u, 0u, 0u);
     }
   }
+  wait_peers_done(a.peer);
+  const int rr = a.row0 + lr;                  // global row of the batch
+  const int e = rr / T, t = rr % T;
+  const int hw = a.hp * a.wp;
+  const int fl = t / hw, rem = t % hw;
+  const int f = a.frame0[e] + fl, ph = rem / a.wp, pw = rem % a.wp;
+  // the row's 64 rotation pairs -- 22 time, 21 height, 21 width -- staged in
+  // shared memory once as (cos, sin, -sin, cos), so each pair rotates with
+  // one packed multiply and one packed FMA after a single lane-indexed load
+  // (a per-element 3-way table select diverges inside every warp).  A lane
+  // rotates pairs 4q..4q+3, q = its vector index mod 16; pair 4q+j sits at
+  // tab[j][q] so each of the lane's four loads is a conflict-free 256-byte
+  // sweep (pair-major order made every load 16-way bank-conflicted and the
+  // kernel shared-memory bound)
+  __shared__ float4 tab[8][4][16];
+  {
+    const float2* rf = a.rope_f + (size_t)f * 22;
+    const float2* rh = a.rope_h + (size_t)ph * 21;
+    const float2* rw = a.rope_w + (size_t)pw * 21;
+    for (int pi = li; pi < 64; pi += 32 * WPR) {
+      const float2 cs = pi < 22 ? rf[pi] : (pi < 43 ? rh[pi - 22] : rw[pi - 43]);
+      tab[slot][pi & 3][pi >> 2] = make_float4(cs.x, cs.y, -cs.y, cs.x);
+    }
+  }
+  __syncthreads();
+  const size_t mat = (size_t)T * d;
+  __nv_bfloat16* kdst = a.arena + ((size_t)a.mat_base + (size_t)a.slot[e] * 2) * mat + (size_t)t * d;
+  __nv_bfloat16* vdst = kdst + mat;
   float inv[2];
 #pragma unroll
   for (int which = 0; which < 2; ++which) {
-    float ss = 0.0f;
+    float2 ss2 = make_float2(0.f, 0.f);
 #pragma unroll
     for (int i = 0; i < VPL; ++i) {
-      const __nv_bfloat16* h = reinterpret_cast<const __nv_bfloat16*>(&raw[which][i]);
+      const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&raw[which][i]);
 #pragma unroll
-      for (int j = 0; j < 8; ++j) ss += bf(h[j]) * bf(h[j]);
+      for (int j = 0; j < 4; ++j) {
+        const float2 x = __bfloat1622float2(h[j]);
+        ss2 = __ffma2_rn(x, x, ss2);
+      }
     }
-    inv[which] = rsqrtf(row_reduce<WPR>(ss, red, slot, wir) / d + kEps);
+    inv[which] = rsqrtf(row_reduce<WPR>(ss2.x + ss2.y, red, slot, wir) / d + kEps);
   }
   if (active) {
 #pragma unroll
     for (int which = 0; which < 2; ++which) {
       const float* wgt = which == 0 ? a.norm_q : a.norm_k;
       __nv_bfloat16* dst = which == 0 ? a.qout + (size_t)lr * d : kdst;
+      const float2 inv2 = make_float2(inv[which], inv[which]);
 #pragma unroll
       for (int i = 0; i < VPL; ++i) {
         const int idx = li + 32 * WPR * i;
         if (idx * 8 >= d) continue;
         const int c0 = idx * 8;                 // element index in [0, d)
-        const int pair0 = (c0 & 127) >> 1;      // pair index inside the head
-        const __nv_bfloat16* h = reinterpret_cast<const __nv_bfloat16*>(&raw[which][i]);
+        const int q4 = idx & 15;                // pairs 4 q4 .. 4 q4 + 3 of the head
+        const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&raw[which][i]);
         const float4 w0 = __ldg(reinterpret_cast<const float4*>(wgt + c0));
         const float4 w1 = __ldg(reinterpret_cast<const float4*>(wgt + c0) + 1);
-        const float wv[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+        const float2 wv[4] = {make_float2(w0.x, w0.y), make_float2(w0.z, w0.w), make_float2(w1.x, w1.y),
+                              make_float2(w1.z, w1.w)};
         uint4 u;
-        __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(&u);
+        uint32_t* o = reinterpret_cast<uint32_t*>(&u);
 #pragma unroll
-        for (int j = 0; j < 8; j += 2) {
-          const float x0 = bf(h[j]) * inv[which] * wv[j];
-          const float x1 = bf(h[j + 1]) * inv[which] * wv[j + 1];
-          const int pi = pair0 + j / 2;
-          const float2 cs = tab[slot][pi];
-          o[j] = __float2bfloat16(x0 * cs.x - x1 * cs.y);
-          o[j + 1] = __float2bfloat16(x0 * cs.y + x1 * cs.x);
+        for (int j = 0; j < 4; ++j) {
+          // (x0, x1) = h * inv * w; (y0, y1) = (x0 c - x1 s, x0 s + x1 c)
+          const float2 x = __fmul2_rn(__fmul2_rn(__bfloat1622float2(h[j]), inv2), wv[j]);
+          const float4 cs = tab[slot][j][q4];
+          const float2 y = __ffma2_rn(make_float2(x.x, x.x), make_float2(cs.x, cs.y),
+                                      __fmul2_rn(make_float2(x.y, x.y), make_float2(cs.z, cs.w)));
+          const __nv_bfloat162 yb = __float22bfloat162_rn(y);
+          o[j] = *reinterpret_cast<const uint32_t*>(&yb);
         }
         reinterpret_cast<uint4*>(dst)[idx] = u;
         if (which == 1 && a.peer.push) {  // fresh K -> every peer's replica (NVLink P2P store)
@@ -431,9 +449,12 @@ __global__ void rms_rows_kernel(__nv_bfloat16* x, int rows, int d, int ld, const
   }
   // warp-per-row blocks stage the weight vector in shared memory once (as
   // ln_rows_kernel does its coefficients) while the row loads are in flight
-  __shared__ float4 wsm[WPR == 1 ? 2 * 32 * VPL : 1];
+  // (split by 16-byte half, wsm[h][v] = w[8 v + 4 h .. +4), so a warp's
+  // loads are unit-stride: interleaved halves made every load 2-way
+  // bank-conflicted)
+  __shared__ float4 wsm[2][WPR == 1 ? 32 * VPL : 1];
   if (WPR == 1) {
-    for (int i = threadIdx.x; i * 4 < d; i += blockDim.x) wsm[i] = __ldg(reinterpret_cast<const float4*>(w) + i);
+    for (int i = threadIdx.x; i * 4 < d; i += blockDim.x) wsm[i & 1][i >> 1] = __ldg(reinterpret_cast<const float4*>(w) + i);
     __syncthreads();
   }
   const float inv = rsqrtf(row_reduce<WPR>(ss, red, slot, wir) / d + kEps);
@@ -445,8 +466,8 @@ __global__ void rms_rows_kernel(__nv_bfloat16* x, int rows, int d, int ld, const
     if (idx * 8 >= d) continue;
     // weights as two 16-byte loads (8 scalar loads strided 32 B apart across
     // the warp made this kernel L1-wavefront bound)
-    const float4 w0 = WPR == 1 ? wsm[2 * idx] : __ldg(reinterpret_cast<const float4*>(w) + 2 * idx);
-    const float4 w1 = WPR == 1 ? wsm[2 * idx + 1] : __ldg(reinterpret_cast<const float4*>(w) + 2 * idx + 1);
+    const float4 w0 = WPR == 1 ? wsm[0][idx] : __ldg(reinterpret_cast<const float4*>(w) + 2 * idx);
+    const float4 w1 = WPR == 1 ? wsm[1][idx] : __ldg(reinterpret_cast<const float4*>(w) + 2 * idx + 1);
     const float wv[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
     uint4 u;
     __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(&u);
