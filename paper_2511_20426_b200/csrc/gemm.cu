@@ -30,7 +30,8 @@ namespace {
 constexpr int BM = 128;
 constexpr int BK = 64;  // 64 bf16 = 128 B = one swizzle atom row
 constexpr int kEpiWarps = 8;      // 2 per TMEM lane quadrant (column halves)
-constexpr int kThreads = 64 + 32 * kEpiWarps;
+constexpr int kResWarp = 2 + kEpiWarps;  // residual-tile TMA loader (gated-residual mode)
+constexpr int kThreads = 64 + 32 * kEpiWarps + 32;
 constexpr int kChunk = 16;        // columns per TMEM load / staging round
 constexpr int kStagePitch = 20;   // floats per staged row (16 + 4 pad, 16 B aligned)
 constexpr int kEpiStageBytes = kEpiWarps * 32 * kStagePitch * 4;
@@ -41,16 +42,43 @@ constexpr int kEpiStageBytes = kEpiWarps * 32 * kStagePitch * 4;
 // own 128 x BN accumulator in TMEM; the leader CTA issues the MMAs, both
 // CTAs' TMA loads complete on the leader's mbarrier, commits multicast to
 // both CTAs.  Halves the B traffic per CTA and the smem operand bandwidth.
-template <int BN, int CG>
+//
+// RES (the gated-residual fp32 mode): the C tile is read and written by TMA
+// through a ring of kResSlots slots, each two 128-row x kResCols fp32 boxes
+// (one per epilogue column half, swizzled): a loader warp streams the
+// residual ahead of the epilogue, the epilogue combines in place and
+// TMA-stores the box.  The residual tile's DRAM read no longer sits on the
+// epilogue's critical path (register prefetch one 16-column chunk ahead
+// left the short-K residual GEMMs at ~60% tensor-active).  16-column boxes
+// x 3 slots (48 KB) keep the mainloop ring at 6 stages for 192-wide pair
+// tiles; measured in the step (scripts/bw_breakdown.py): 16 x 3 -3.6% on
+// the residual GEMMs, 16 x 4 and 32 x 2 / 3 (5 / 4 stages) no gain.
+#ifndef BC_GEMM_RES_COLS
+#define BC_GEMM_RES_COLS 16
+#endif
+#ifndef BC_GEMM_RES_SLOTS
+#define BC_GEMM_RES_SLOTS 3
+#endif
+constexpr int kResCols = BC_GEMM_RES_COLS;         // columns per residual box (16 or 32 fp32)
+constexpr int kResSwz = kResCols * 4;              // box row bytes = swizzle span (64 or 128 B)
+constexpr int kResBoxBytes = BM * kResCols * 4;
+constexpr int kResSlots = BC_GEMM_RES_SLOTS;
+static_assert(kResCols == 16 || kResCols == 32, "residual box width");
+template <int BN, int CG, bool RES = false>
 struct GemmCfg {
   static constexpr int kABytes = BM * BK * 2;
   static constexpr int kBBytes = (BN / CG) * BK * 2;
   static constexpr int kStageBytes = kABytes + kBBytes;
-  static constexpr int kStages = (192 * 1024) / kStageBytes > 8 ? 8 : (192 * 1024) / kStageBytes;
+  static constexpr int kResBytes = RES ? kResSlots * 2 * kResBoxBytes : 0;
+  static constexpr int kEpiStage = RES ? 0 : kEpiStageBytes;
+  static constexpr int kRingBudget = RES ? 227 * 1024 - 1024 - 256 - kResBytes : 192 * 1024;
+  static constexpr int kStages = kRingBudget / kStageBytes > 8 ? 8 : kRingBudget / kStageBytes;
   // two accumulators, rounded up to the power-of-two column count
   // tcgen05.alloc requires (BN = 192 -> 512)
   static constexpr int kTmemCols = 2 * BN <= 32 ? 32 : 2 * BN <= 64 ? 64 : 2 * BN <= 128 ? 128 : 2 * BN <= 256 ? 256 : 512;
-  static constexpr size_t kSmem = 1024 /*align slack*/ + (size_t)kStages * kStageBytes + 256 + kEpiStageBytes;
+  static constexpr size_t kSmem = 1024 /*align slack*/ + (size_t)kStages * kStageBytes + kResBytes + 256 + kEpiStage;
+  static_assert(!RES || (BN / 2) % kResCols == 0, "residual boxes tile each column half");
+  static_assert(kSmem <= 227 * 1024, "shared memory");
 };
 
 __device__ __forceinline__ uint32_t cluster_rank() {
@@ -142,21 +170,26 @@ __device__ __forceinline__ float gelu_tanh(float x) {
 template <int BN, int MODE, int CG>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
-                void* __restrict__ c_ptr, int M, int N, int K, const float* __restrict__ bias,
-                const float* __restrict__ gate, int gate_stride, int rows_per_gate, int gate_row0) {
-  using Cfg = GemmCfg<BN, CG>;
+                const __grid_constant__ CUtensorMap map_c, void* __restrict__ c_ptr, int M, int N, int K,
+                const float* __restrict__ bias, const float* __restrict__ gate, int gate_stride, int rows_per_gate,
+                int gate_row0) {
+  constexpr bool RES = MODE == kEpiResidualF32;
+  using Cfg = GemmCfg<BN, CG, RES>;
   constexpr int S = Cfg::kStages;
   constexpr int TM = BM * CG;  // rows per (cluster) tile
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sa = smem;
   uint8_t* sb = smem + S * Cfg::kABytes;
-  float* epi_stage = reinterpret_cast<float*>(smem + S * Cfg::kStageBytes);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * Cfg::kStageBytes + kEpiStageBytes);
+  uint8_t* res_buf = smem + S * Cfg::kStageBytes;  // RES: [slot][half] 128 x 32 fp32 boxes, SW128
+  float* epi_stage = reinterpret_cast<float*>(smem + S * Cfg::kStageBytes + Cfg::kResBytes);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * Cfg::kStageBytes + Cfg::kResBytes + Cfg::kEpiStage);
   uint64_t* empty = full + S;
   uint64_t* tfull = empty + S;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* res_full = tempty + 2;
+  uint64_t* res_empty = res_full + kResSlots;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(res_empty + kResSlots);
 
   const uint32_t warp = warp_id();
   const uint32_t rank = CG == 2 ? cluster_rank() : 0u;
@@ -178,6 +211,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
       mbar_init(&tempty[i], CG == 2 ? CG * kEpiWarps : 32 * kEpiWarps);
+    }
+    if (RES) {
+      tma_prefetch(&map_c);
+      for (int i = 0; i < kResSlots; ++i) {
+        mbar_init(&res_full[i], 1);   // the loader's arrival + both boxes' bytes
+        mbar_init(&res_empty[i], 2);  // each column half's storing thread
+      }
     }
     fence_barrier_init();
   }
@@ -268,13 +308,112 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
     }
+  } else if (warp == kResWarp) {
+    if (RES && lane_id() == 0) {
+      // residual loader: box (tile, step, half) = C[m0 .. +128, n0 + half * BN/2 + step * 32 .. +32]
+      int slot = 0;
+      uint32_t ph = 0;
+      for (int tile = unit; tile < num_tiles; tile += n_units) {
+        int mb, nb;
+        tile_coords(tile, num_m, num_n, mb, nb);
+        const int m0 = mb * TM + (int)rank * BM, n0 = nb * BN;
+        for (int step = 0; step < BN / 2 / kResCols; ++step) {
+          mbar_wait(&res_empty[slot], ph ^ 1);
+          mbar_arrive_expect_tx(&res_full[slot], 2 * kResBoxBytes);
+          uint8_t* dst = res_buf + slot * 2 * kResBoxBytes;
+          tma_load_2d(dst, &map_c, &res_full[slot], n0 + step * kResCols, m0);
+          tma_load_2d(dst + kResBoxBytes, &map_c, &res_full[slot], n0 + BN / 2 + step * kResCols, m0);
+          if (++slot == kResSlots) {
+            slot = 0;
+            ph ^= 1;
+          }
+        }
+      }
+    }
+  } else if (RES) {
+    // gated-residual epilogue: warp w covers TMEM lanes 32*(w%4)..+31 (one
+    // tile row per thread) and one column half; per 32-column step it reads
+    // its row of the residual box from shared memory (swizzled: 16-byte
+    // chunk j of row r at chunk j ^ (r & 7), conflict-free), writes
+    // C = resid + gate * (acc + bias) back in place, and one thread per half
+    // TMA-stores the box once the half's 128 threads are done with it.
+    const int ew = (int)warp - 2;
+    const uint32_t quad = warp & 3;
+    const int half = ew >> 2;
+    const uint32_t row = quad * 32 + lane_id();  // tile row
+    const bool storer = quad == 0 && lane_id() == 0;
+    int slot = 0, pend = -1;
+    uint32_t ph = 0;
+    int it = 0;
+    for (int tile = unit; tile < num_tiles; tile += n_units, ++it) {
+      const int acc = it & 1;
+      const uint32_t acc_phase = (it >> 1) & 1;
+      int mb, nb;
+      tile_coords(tile, num_m, num_n, mb, nb);
+      const int m0 = mb * TM + (int)rank * BM, n0 = nb * BN;
+      const int grow = min(m0 + (int)row, M - 1);
+      const float* grow_ptr = gate ? gate + (size_t)((gate_row0 + grow) / rows_per_gate) * gate_stride : nullptr;
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+#pragma unroll 1
+      for (int step = 0; step < BN / 2 / kResCols; ++step) {
+        const int c = half * (BN / 2) + step * kResCols;  // column within the tile
+        const int col = n0 + c;
+        uint32_t r[kResCols];
+        if constexpr (kResCols == 32)
+          tmem_ld32(tmem_base + ((quad * 32) << 16) + acc * BN + c, *reinterpret_cast<uint32_t(*)[32]>(r));
+        else
+          tmem_ld16(tmem_base + ((quad * 32) << 16) + acc * BN + c, *reinterpret_cast<uint32_t(*)[16]>(r));
+        mbar_wait(&res_full[slot], ph);
+        tmem_ld_wait();
+        const uint32_t box = smem_u32(res_buf + slot * 2 * kResBoxBytes + half * kResBoxBytes) + row * kResSwz;
+        // 128-byte swizzle: chunk j ^ (r & 7); 64-byte: chunk j ^ ((r >> 1) & 3)
+        const uint32_t swz = kResCols == 32 ? (row & 7) : ((row >> 1) & 3);
+#pragma unroll
+        for (int j = 0; j < kResCols / 4; ++j) {
+          const uint32_t a = box + ((j ^ swz) << 4);
+          const float4 res = lds128f(a);
+          const float4 g = grow_ptr ? __ldg(reinterpret_cast<const float4*>(grow_ptr + col) + j)
+                                    : make_float4(1.f, 1.f, 1.f, 1.f);
+          const float4 b = bias ? __ldg(reinterpret_cast<const float4*>(bias + col) + j) : make_float4(0.f, 0.f, 0.f, 0.f);
+          float4 o;
+          o.x = fmaf(g.x, __uint_as_float(r[4 * j + 0]) + b.x, res.x);
+          o.y = fmaf(g.y, __uint_as_float(r[4 * j + 1]) + b.y, res.y);
+          o.z = fmaf(g.z, __uint_as_float(r[4 * j + 2]) + b.z, res.z);
+          o.w = fmaf(g.w, __uint_as_float(r[4 * j + 3]) + b.w, res.w);
+          sts128f(a, o);
+        }
+        fence_async_shared();
+        named_bar_sync(1 + half, 128);
+        if (storer) {
+          tma_store_2d(&map_c, res_buf + slot * 2 * kResBoxBytes + half * kResBoxBytes, col, m0);
+          bulk_commit();
+          // release the previous box once its store has read shared memory
+          if (pend >= 0) {
+            bulk_wait_read<1>();
+            mbar_arrive(&res_empty[pend]);
+          }
+          pend = slot;
+        }
+        if (++slot == kResSlots) {
+          slot = 0;
+          ph ^= 1;
+        }
+      }
+      tc_fence_before();
+      if (CG == 2) {
+        __syncwarp();
+        if (lane_id() == 0) mbar_arrive_remote(map_rank(&tempty[acc], 0));  // leader's barrier
+      } else {
+        mbar_arrive(&tempty[acc]);
+      }
+    }
+    if (storer) bulk_wait<0>();  // C written before the CTA retires
   } else {
     // epilogue: 8 warps; warp w covers TMEM lanes 32*(w%4)..+31 (tile rows)
     // and one column half.  Each 32x16 chunk goes TMEM -> registers (row per
     // lane, + bias / GELU) -> a padded per-warp smem stage -> coalesced
-    // global access (8 rows x 64 B per warp instruction).  For the residual
-    // mode all of a chunk's C / gate loads are issued before any use, so the
-    // read-modify-write runs at memory-level parallelism, not latency.
+    // global stores (8 rows x 64 B per warp instruction).
     const int ew = (int)warp - 2;
     const uint32_t quad = warp & 3;
     const int c_begin = (ew >> 2) * (BN / 2);
@@ -289,41 +428,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       tile_coords(tile, num_m, num_n, mb, nb);
       const int m0 = mb * TM + (int)rank * BM, n0 = nb * BN;
       const int row_base = m0 + (int)quad * 32;
-      // residual epilogue: the C / gate loads of chunk c + 1 are issued before
-      // chunk c is processed (and chunk 0's before the accumulator wait), so
-      // one DRAM round trip per 16-column chunk no longer serialises the
-      // epilogue -- at K = 1536 the epilogue was longer than the mainloop
-      float4 res_n[4], g_n[4];
-      auto load_res = [&](int c) {
-        const int colc = n0 + c;
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const int row = row_base + i * 8 + sub_row;
-          res_n[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-          g_n[i] = make_float4(1.f, 1.f, 1.f, 1.f);
-          if (row < M) {
-            res_n[i] = *reinterpret_cast<const float4*>(static_cast<float*>(c_ptr) + (size_t)row * N + colc + sub_col);
-            if (gate)
-              g_n[i] = __ldg(reinterpret_cast<const float4*>(gate + (size_t)((gate_row0 + row) / rows_per_gate) * gate_stride +
-                                                             colc + sub_col));
-          }
-        }
-      };
-      if (MODE == kEpiResidualF32) load_res(c_begin);
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       if (ew == 0 && lane_id() == 0) GEMM_TRACE(2, it);
 #pragma unroll 1
       for (int c = c_begin; c < c_begin + BN / 2; c += kChunk) {
-        float4 res[4], g[4];
-        if (MODE == kEpiResidualF32) {
-#pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            res[i] = res_n[i];
-            g[i] = g_n[i];
-          }
-          if (c + kChunk < c_begin + BN / 2) load_res(c + kChunk);
-        }
         uint32_t r[16];
         __syncwarp();
         tmem_ld16(tmem_base + ((quad * 32) << 16) + acc * BN + c, r);
@@ -346,36 +455,19 @@ __global__ void __launch_bounds__(kThreads, 1)
           *reinterpret_cast<float4*>(srow + j) = v;
         }
         __syncwarp();
-        if (MODE == kEpiResidualF32) {
 #pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            const int lr = i * 8 + sub_row;
-            const int row = row_base + lr;
-            const float4 v = *reinterpret_cast<const float4*>(stage + lr * kStagePitch + sub_col);
-            if (row < M) {
-              float4 o = res[i];
-              o.x += g[i].x * v.x;
-              o.y += g[i].y * v.y;
-              o.z += g[i].z * v.z;
-              o.w += g[i].w * v.w;
-              *reinterpret_cast<float4*>(static_cast<float*>(c_ptr) + (size_t)row * N + col + sub_col) = o;
-            }
-          }
-        } else {
-#pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            const int lr = i * 8 + sub_row;
-            const int row = row_base + lr;
-            const float4 v = *reinterpret_cast<const float4*>(stage + lr * kStagePitch + sub_col);
-            if (row < M) {
-              if (MODE == kEpiStoreF32) {
-                *reinterpret_cast<float4*>(static_cast<float*>(c_ptr) + (size_t)row * N + col + sub_col) = v;
-              } else {
-                uint2 pk;
-                pk.x = pack_bf16(v.x, v.y);
-                pk.y = pack_bf16(v.z, v.w);
-                *reinterpret_cast<uint2*>(static_cast<__nv_bfloat16*>(c_ptr) + (size_t)row * N + col + sub_col) = pk;
-              }
+        for (int i = 0; i < 4; ++i) {
+          const int lr = i * 8 + sub_row;
+          const int row = row_base + lr;
+          const float4 v = *reinterpret_cast<const float4*>(stage + lr * kStagePitch + sub_col);
+          if (row < M) {
+            if (MODE == kEpiStoreF32) {
+              *reinterpret_cast<float4*>(static_cast<float*>(c_ptr) + (size_t)row * N + col + sub_col) = v;
+            } else {
+              uint2 pk;
+              pk.x = pack_bf16(v.x, v.y);
+              pk.y = pack_bf16(v.z, v.w);
+              *reinterpret_cast<uint2*>(static_cast<__nv_bfloat16*>(c_ptr) + (size_t)row * N + col + sub_col) = pk;
             }
           }
         }
@@ -420,7 +512,11 @@ template <int BN, int MODE, int CG>
 int launch(const CUtensorMap& ma, const CUtensorMap& mb, void* C, int M, int N, int K,
            const float* bias, const float* gate, int gate_stride, int rows_per_gate, int gate_row0,
            cudaStream_t st) {
-  using Cfg = GemmCfg<BN, CG>;
+  using Cfg = GemmCfg<BN, CG, MODE == kEpiResidualF32>;
+  // the residual mode reads / writes C through TMA: fp32 [M][N], 128 x 32 boxes
+  CUtensorMap mc = ma;
+  if (MODE == kEpiResidualF32)
+    BC_RC(make_tmap_2d_f32(&mc, C, (uint64_t)N, (uint64_t)M, (uint64_t)N * 4, kResCols, BM, kResSwz));
   static PerDeviceOnce attrs_once;
   BC_RC(per_device_once(attrs_once, [&]() -> int {
     BC_CUDA(cudaFuncSetAttribute(gemm_kernel<BN, MODE, CG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -464,7 +560,7 @@ int launch(const CUtensorMap& ma, const CUtensorMap& mb, void* C, int M, int N, 
   const int units = units_of[slot] > 0 ? units_of[slot] : sm_count() / CG;
   const int grid = (tiles < units ? tiles : units) * CG;
   cfg.gridDim = dim3(grid);
-  BC_CUDA(cudaLaunchKernelEx(&cfg, gemm_kernel<BN, MODE, CG>, ma, mb, C, M, N, K, bias, gate, gate_stride,
+  BC_CUDA(cudaLaunchKernelEx(&cfg, gemm_kernel<BN, MODE, CG>, ma, mb, mc, C, M, N, K, bias, gate, gate_stride,
                              rows_per_gate, gate_row0));
   BC_LAUNCHED();
   return BC_OK;
@@ -484,8 +580,9 @@ int dispatch_mode(int mode, const CUtensorMap& ma, const CUtensorMap& mb, void* 
 
 }  // namespace
 
-int make_tmap_2d_swz(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer,
-                     uint64_t row_stride_bytes, uint32_t box_inner, uint32_t box_outer, int swizzle_bytes) {
+static int make_tmap_2d_typed(CUtensorMap* map, CUtensorMapDataType dtype, const void* base, uint64_t inner,
+                              uint64_t outer, uint64_t row_stride_bytes, uint32_t box_inner, uint32_t box_outer,
+                              int swizzle_bytes) {
   auto fn = encode_fn();
   if (!fn) return bc_fail(BC_ERR_CUDA, "cuTensorMapEncodeTiled unavailable (driver too old or no GPU)");
   cuuint64_t dims[2] = {inner, outer};
@@ -496,11 +593,23 @@ int make_tmap_2d_swz(CUtensorMap* map, const void* base, uint64_t inner, uint64_
                                  : swizzle_bytes == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
                                  : swizzle_bytes == 32 ? CU_TENSOR_MAP_SWIZZLE_32B
                                                        : CU_TENSOR_MAP_SWIZZLE_NONE;
-  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box,
+  CUresult r = fn(map, dtype, 2, const_cast<void*>(base), dims, strides, box,
                   estr, CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return bc_fail(BC_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
   return BC_OK;
+}
+
+int make_tmap_2d_swz(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer,
+                     uint64_t row_stride_bytes, uint32_t box_inner, uint32_t box_outer, int swizzle_bytes) {
+  return make_tmap_2d_typed(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, base, inner, outer, row_stride_bytes, box_inner,
+                            box_outer, swizzle_bytes);
+}
+
+int make_tmap_2d_f32(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer,
+                     uint64_t row_stride_bytes, uint32_t box_inner, uint32_t box_outer, int swizzle_bytes) {
+  return make_tmap_2d_typed(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, base, inner, outer, row_stride_bytes, box_inner,
+                            box_outer, swizzle_bytes);
 }
 
 int make_tmap_2d(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer,

@@ -34,6 +34,9 @@ int make_tmap_2d(CUtensorMap* map, const void* base, uint64_t inner, uint64_t ou
 // the same with a 128 / 64 / 32-byte (or 0 = no) swizzle
 int make_tmap_2d_swz(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer,
                      uint64_t row_stride_bytes, uint32_t box_inner, uint32_t box_outer, int swizzle_bytes);
+// fp32 (the gated-residual GEMM's C tiles)
+int make_tmap_2d_f32(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer,
+                     uint64_t row_stride_bytes, uint32_t box_inner, uint32_t box_outer, int swizzle_bytes);
 int num_sms();
 
 }  // namespace bc

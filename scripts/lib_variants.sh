@@ -15,7 +15,11 @@ if [ "$cmd" = build ]; then
   for spec in "$@"; do
     name=${spec%%:*}; flags=${spec#*:}
     OUT=$OUTROOT/bcv_$name; mkdir -p $OUT
-    for f in *.cu; do $NV $flags -c $f -o $OUT/${f%.cu}.o 2>/dev/null & done; wait
+    for f in *.cu; do $NV $flags -c $f -o $OUT/${f%.cu}.o 2>$OUT/${f%.cu}.log & done; wait
+    for f in *.cu; do  # a failed compile must not leave a .so with missing symbols
+      [ -f $OUT/${f%.cu}.o ] || { echo "variant $name: $f failed"; cat $OUT/${f%.cu}.log; exit 1; }
+    done
+    rm -f $OUT/*.log
     for f in *.cpp; do g++ -O3 -std=c++17 -fPIC -c $f -o $OUT/${f%.cpp}.o; done
     nvcc -gencode arch=compute_100a,code=sm_100a -shared -o $OUT/libbcb200.so $OUT/*.o -L$NPR -lnpyrandom -lm -lpthread
     rm -f $OUT/*.o

@@ -81,3 +81,31 @@ def test_gemm_tilings_bitwise_equal(M, Nn, K):
         outs.append(C)
     for C in outs[1:]:
         assert torch.equal(C, outs[0])
+
+
+@pytest.mark.parametrize("M,Nn,K", [(4680, 1536, 1536), (777, 1536, 8960), (300, 768, 256)])
+def test_gemm_residual_tilings_bitwise_equal(M, Nn, K):
+    """The gated-residual epilogue (C read and written in place through TMA
+    boxes) gives bit-identical C for every tiling, with and without the
+    bias / gate, including a ragged last row tile."""
+    g = torch.Generator(device="cuda").manual_seed(M * 3 + Nn + K)
+    A = torch.randn(M, K, device="cuda", generator=g).bfloat16()
+    B = (torch.randn(Nn, K, device="cuda", generator=g) / K ** 0.5).bfloat16()
+    bias = torch.randn(Nn, device="cuda", generator=g)
+    rows_per_gate = 211
+    gate = torch.randn((M + rows_per_gate - 1) // rows_per_gate, Nn, device="cuda", generator=g)
+    X0 = torch.randn(M, Nn, device="cuda", generator=g)
+    ref = A.float() @ B.float().T
+    for use_bias, use_gate in ((True, True), (False, False)):
+        want = X0 + (gate.repeat_interleave(rows_per_gate, 0)[:M] if use_gate else 1.0) * (ref + (bias if use_bias else 0.0))
+        outs = []
+        for bn, cg in ((64, 1), (128, 1), (256, 1), (256, 2), (192, 2), (0, 0)):
+            if Nn % (bn or 64):
+                continue
+            X = X0.clone()
+            gemm(A, B, X, 3, bias if use_bias else None, gate if use_gate else None, Nn, rows_per_gate, bn=bn, cg=cg)
+            outs.append(X)
+        assert rel(outs[0], want) < 1e-5
+        for X in outs[1:]:
+            assert torch.equal(X, outs[0])
+
