@@ -1,4 +1,5 @@
-"""Per-kernel breakdown of one 13-block Wan-1.3B cascade in the product launch
+"""Per-kernel breakdown of one 13-block Wan-1.3B cascade (SEQ=1: the
+sequential rollout) in the product launch
 mode (CUDA graphs, no per-kernel events): CUPTI durations (torch.profiler)
 summed by kernel name, with the launch count and the mean / min / max
 duration -- where the bandwidth class's time goes."""
@@ -14,6 +15,8 @@ import paper_2511_20426_b200 as bc
 from paper_2511_20426_b200.wan import ResidentNoiseFeed, WanWeights, run_noise_keys
 
 cfg = bc.wan_config(os.environ.get("PRESET", "1.3b"), total_frames=39)
+if os.environ.get("SEQ"):  # the sequential (width-1) rollout instead of the cascade
+    cfg = bc.with_fields(cfg, offset=cfg.passes)
 w = WanWeights.random(cfg, 7)
 feed = ResidentNoiseFeed(20260809, cfg, run_noise_keys(cfg))
 for _ in range(2):
