@@ -25,13 +25,16 @@ from paper_2511_20426_b200 import _native as N
 N.LIB_PATH = os.environ["BC_TRACE_LIB"]
 import torch
 T, heads, n_ent, n_vis = 4680, 12, 5, 13
-arena = torch.randn(13, 2, T, heads * 128, device="cuda").bfloat16()
+Tk = T
+if os.environ.get("CROSS"):  # the text cross-attention shape: one 512-token K/V slot
+    Tk, n_vis = 512, 1
+arena = torch.randn(n_vis, 2, Tk, heads * 128, device="cuda").bfloat16()
 q = torch.randn(n_ent * T, heads * 128, device="cuda").bfloat16()
 out = torch.empty_like(q)
 b = N.make_batch(3, list(range(n_ent)), [0.0] * n_ent, [0] * n_ent, [list(range(n_vis))] * n_ent)
-mat = T * heads * 128
+mat = Tk * heads * 128
 for _ in range(3):
-    N.check(N.lib().bc_attention_paged(N.ptr(q), N.ptr(arena), N.ptr(arena) + mat * 2, 2 * mat, T, b, T,
+    N.check(N.lib().bc_attention_paged(N.ptr(q), N.ptr(arena), N.ptr(arena) + mat * 2, 2 * mat, Tk, b, T,
                                        heads, N.ptr(out), N.stream_ptr()), "attn")
 buf = (ctypes.c_ulonglong * (32 * 64 + 256 * 8))()
 lib = ctypes.CDLL(N.LIB_PATH)
@@ -43,11 +46,12 @@ t0 = t[t > 0].min()
 names = {0: "A s_full", 4: "A s_read", 1: "A max", 2: "A exp", 5: "A o_rdy", 3: "A p_full",
          8: "B s_full", 12: "B s_read", 9: "B max", 10: "B exp", 13: "B o_rdy", 11: "B p_full", 16: "M s_emptyA", 17: "M QK_A", 18: "M p_fullA", 19: "M PV_A", 20: "M s_emptyB",
          21: "M QK_B", 22: "M p_fullB", 23: "M PV_B", 24: "M K_rdy", 25: "M V_rdy"}
-for j in range(20, 28):
+for j in (range(0, 8) if os.environ.get("CROSS") else range(20, 28)):
     row = {names[k]: int(t[k, j] - t0) for k in names if t[k, j] > 0}
     print(j, sorted(row.items(), key=lambda kv: kv[1]))
 per = [int(t[1, j + 1] - t[1, j]) for j in range(20, 60) if t[1, j + 1] > 0 and t[1, j] > 0]
-print("A token period (cycles):", per, "median", int(np.median(per)))
+if per:
+    print("A token period (cycles):", per, "median", int(np.median(per)))
 c = c[c[:, 0] > 0]
 if len(c):
     cyc, ns, tiles, wait, kv, se, iqk, ipv = c.T
