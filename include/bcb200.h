@@ -258,9 +258,11 @@ int bc_stream_wait_geq_u32(void* addr, uint32_t value, void* stream);
  * 2: C fp32 = acc+bias;       3: C fp32 += gate[row/rows_per_gate] * (acc+bias)
  * K % 64 == 0, N % 64 == 0; lda = ldb = K, ldc = N.
  * Tuning bits above the epilogue (0 = automatic): bits 8-15 force the tile
- * width in units of 64 columns; bits 16-17 = 1 single-CTA tiles, 2 CTA-pair
- * tiles (tcgen05 cta_group::2, 256 rows; needs the width 256).  Results are
- * identical for every choice (fixed K order, no split-K). */
+ * width in units of 64 columns (of 32 columns when bit 18 is set: 224 =
+ * 7 << 8 | 1 << 18); bits 16-17 = 1 single-CTA tiles, 2 CTA-pair tiles
+ * (tcgen05 cta_group::2, 256 rows; widths 256 / 224 / 192, 224 may end in a
+ * ragged, masked column tile).  Results are identical for every choice
+ * (fixed K order, no split-K). */
 int bc_gemm_bf16(const void* A, const void* B, void* C, int32_t M, int32_t N, int32_t K,
                  int32_t mode, const float* bias, const float* gate, int32_t gate_stride,
                  int32_t rows_per_gate, void* stream);

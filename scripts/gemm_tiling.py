@@ -11,12 +11,12 @@ import torch
 sys.path.insert(0, __file__.rsplit("/scripts/", 1)[0])
 from paper_2511_20426_b200 import _native as N  # noqa: E402
 
-TILINGS = [(256, 2), (192, 2), (256, 1), (128, 1)]
+TILINGS = [(256, 2), (224, 2), (192, 2), (256, 1), (128, 1)]
 
 
 def bench(M, Nn, K, mode, bn, cg, A, B, C, gate, iters=30):
     f = lambda: N.check(N.lib().bc_gemm_bf16(N.ptr(A), N.ptr(B), N.ptr(C), M, Nn, K,
-                                             mode | ((bn // 64) << 8) | (cg << 16), 0,
+                                             mode | (((bn // 64) << 8) if bn % 64 == 0 else ((bn // 32) << 8) | (1 << 18)) | (cg << 16), 0,
                                              N.ptr(gate) if gate is not None else 0, Nn if gate is not None else 0,
                                              M, N.stream_ptr()), "gemm")
     for _ in range(3):
@@ -41,7 +41,7 @@ def main():
         gate = torch.ones(1, Nn, device="cuda") if mode == 3 else None
         res = {}
         for bn, cg in TILINGS:
-            if Nn % bn:
+            if Nn % bn and bn != 224:
                 continue
             res[(bn, cg)] = bench(M, Nn, K, mode, bn, cg, A, B, C, gate)
         auto = bench(M, Nn, K, mode, 0, 0, A, B, C, gate)

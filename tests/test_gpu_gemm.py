@@ -14,9 +14,14 @@ def gemm(A, B, C, mode, bias=None, gate=None, gate_stride=0, rows_per_gate=1, bn
     M, K = A.shape
     Nn = B.shape[0]
     N.check(N.lib().bc_gemm_bf16(N.ptr(A), N.ptr(B), N.ptr(C), M, Nn, K,
-                                 mode | ((bn // 64) << 8) | (cg << 16),
+                                 mode | width_bits(bn) | (cg << 16),
                                  N.ptr(bias), N.ptr(gate), gate_stride, rows_per_gate,
                                  N.stream_ptr()), "gemm")
+
+
+def width_bits(bn):
+    """Forced tile width: bits 8-15 in units of 64 columns, or of 32 with bit 18."""
+    return ((bn // 64) << 8) if bn % 64 == 0 else ((bn // 32) << 8) | (1 << 18)
 
 
 def rel(a, b):
@@ -28,10 +33,12 @@ SHAPES = [(128, 256, 64), (300, 128, 128), (4680, 1536, 1536), (1000, 768, 256),
 
 
 @pytest.mark.parametrize("M,Nn,K", SHAPES)
-@pytest.mark.parametrize("bn,cg", [(0, 0), (64, 1), (128, 1), (256, 1), (256, 2), (192, 2)])
+@pytest.mark.parametrize("bn,cg", [(0, 0), (64, 1), (128, 1), (256, 1), (256, 2), (224, 2), (192, 2)])
 def test_gemm_modes(M, Nn, K, bn, cg):
-    """cg = 2: tcgen05.mma.cta_group::2 CTA pairs (256 x 256 / 256 x 192 tiles)."""
-    if bn and Nn % bn:
+    """cg = 2: tcgen05.mma.cta_group::2 CTA pairs (256 x 256 / 224 / 192
+    tiles); 224-wide tiles end in a ragged, masked column tile when 224 does
+    not divide N."""
+    if bn and bn != 224 and Nn % bn:
         pytest.skip("tile width does not divide N")
     g = torch.Generator(device="cuda").manual_seed(M * 7 + Nn + K)
     A = torch.randn(M, K, device="cuda", generator=g).bfloat16()
@@ -73,8 +80,8 @@ def test_gemm_tilings_bitwise_equal(M, Nn, K):
     B = (torch.randn(Nn, K, device="cuda", generator=g) / K ** 0.5).bfloat16()
     bias = torch.randn(Nn, device="cuda", generator=g)
     outs = []
-    for bn, cg in ((64, 1), (128, 1), (256, 1), (256, 2), (192, 2), (0, 0)):
-        if Nn % (bn or 64):
+    for bn, cg in ((64, 1), (128, 1), (256, 1), (256, 2), (224, 2), (192, 2), (0, 0)):
+        if bn != 224 and Nn % (bn or 64):
             continue
         C = torch.empty(M, Nn, device="cuda")
         gemm(A, B, C, 2, bias=bias, bn=bn, cg=cg)
@@ -99,8 +106,8 @@ def test_gemm_residual_tilings_bitwise_equal(M, Nn, K):
     for use_bias, use_gate in ((True, True), (False, False)):
         want = X0 + (gate.repeat_interleave(rows_per_gate, 0)[:M] if use_gate else 1.0) * (ref + (bias if use_bias else 0.0))
         outs = []
-        for bn, cg in ((64, 1), (128, 1), (256, 1), (256, 2), (192, 2), (0, 0)):
-            if Nn % (bn or 64):
+        for bn, cg in ((64, 1), (128, 1), (256, 1), (256, 2), (224, 2), (192, 2), (0, 0)):
+            if bn != 224 and Nn % (bn or 64):
                 continue
             X = X0.clone()
             gemm(A, B, X, 3, bias if use_bias else None, gate if use_gate else None, Nn, rows_per_gate, bn=bn, cg=cg)
