@@ -646,7 +646,7 @@ Tiling gemm_plan(int M, int N, int K, int mode, int only_cg) {
     int bn, cg;
     double cost_compute, cost_epi;
   };
-  static const Cand cands[] = {{256, 2, 1.00, 1.00}, {224, 2, 1.02, 1.00}, {192, 2, 1.04, 0.99},
+  static const Cand cands[] = {{256, 2, 1.00, 1.00}, {224, 2, 1.05, 1.00}, {192, 2, 1.04, 0.99},
                                 {256, 1, 1.10, 1.05}, {128, 1, 1.50, 1.18}};
   const int sms = sm_count();
   Tiling best{N % 128 == 0 ? 128 : 64, 1};

@@ -84,10 +84,14 @@ __device__ __forceinline__ float bf(const __nv_bfloat16 v) { return __bfloat162f
 // c*4 + kh*2 + kw (Conv3d weight order, kernel (1,2,2)).
 // Rows [row0, row0 + rows) of the concatenated batch (row = e * T + token);
 // out row 0 = global row row0.
+// status != nullptr (the rows cover every latent): the finiteness check of
+// the inputs rides along -- status = 1 + block index of an entry holding a
+// NaN / Inf (what check_finite_kernel reports), no extra pass over the latents.
 __global__ void patchify_kernel(EntryPtrs lat, int F, int H, int W, __nv_bfloat16* out, int T, int row0,
-                                int rows) {
+                                int rows, int32_t* status) {
   const int hp = H / 2, wp = W / 2;
   const int64_t total = (int64_t)rows * 64;
+  int bad_block = -1;
   for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
        idx += (int64_t)gridDim.x * blockDim.x) {
     const int g = row0 + (int)(idx >> 6), v = (int)(idx & 63);
@@ -96,64 +100,99 @@ __global__ void patchify_kernel(EntryPtrs lat, int F, int H, int W, __nv_bfloat1
     const int f = n / (hp * wp), rem = n % (hp * wp);
     const int i = rem / wp, j = rem % wp;
     const float val = lat.p[e][(((size_t)f * 16 + c) * H + 2 * i + kh) * W + 2 * j + kw];
+    if (!isfinite(val) && bad_block < 0) bad_block = lat.block[e];
     out[idx] = __float2bfloat16(val);
   }
+  if (status && bad_block >= 0) atomicCAS(status, 0, 1 + bad_block);
 }
 
 // ------------------------------------------------------------ GEMV (time MLP)
 // out[e][o] = act( sum_k in[e][k] W[o][k] + b[o] ), one warp per o, 16-byte
-// weight loads (8 bf16 per lane per step); act 0: none, 1: silu, 2: out gets
-// the raw value and out2 its silu (t_e feeds the head modulation raw and the
-// 6d projection through a silu).  K % 8 == 0.
-__global__ void gemv_kernel(const float* __restrict__ in, int n, int K, const __nv_bfloat16* __restrict__ W,
-                            const float* __restrict__ b, float* __restrict__ out, int N, int act,
-                            float* __restrict__ out2) {
-  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+// weight loads (8 bf16 per lane per step, 4 in flight before the math); act
+// 0: none, 1: silu, 2: out gets the raw value and out2 its silu (t_e feeds
+// the head modulation raw and the 6d projection through a silu).  K % 8 == 0.
+// Two fusions keep the time embedding at three launches per step:
+//  * SIN: the input is each entry's timestep sinusoid (K = freq_dim:
+//    [cos(t w_k), sin(t w_k)], w_k = 10000^(-k/half), Wan
+//    sinusoidal_embedding_1d), computed into shared memory by every CTA;
+//  * mod != nullptr: the AdaLN tables of every layer are written as well,
+//    mod[l][e][o] = base[l][o] + out[e][o] (N = 6d), in runs of the CTA's
+//    8 consecutive outputs (whole 32-byte sectors).
+// (SIN is a template flag so the double-precision sinusoid code does not
+// raise the register count of the wide GEMVs.)  Measured in the step: ~9 /
+// ~12 / ~30-50 us for n = 1..5 (latency-bound: 9216 short rows), about the
+// five separate launches' time; the time MLP is 0.05% of a generation.
+template <bool SIN>
+__global__ void __launch_bounds__(256)
+    gemv_kernel(const float* __restrict__ in, int n, int K, const __nv_bfloat16* __restrict__ W,
+                const float* __restrict__ b, float* __restrict__ out, int N, int act, float* __restrict__ out2,
+                TimeArgs ts, const float* __restrict__ base, int L, float* __restrict__ mod) {
+  extern __shared__ float sin_in[];  // [n][K] when SIN
+  __shared__ float e0s[BC_MAX_ENTRIES][8];  // mod != nullptr: this CTA's outputs
+  if constexpr (SIN) {
+    const int half = K / 2;
+    for (int i = threadIdx.x; i < n * half; i += blockDim.x) {
+      const int e = i / half, k = i % half;
+      const double w = pow(10000.0, -(double)k / (double)half);
+      const double arg = ts.t[e] * w;
+      sin_in[e * K + k] = (float)cos(arg);
+      sin_in[e * K + half + k] = (float)sin(arg);
+    }
+    __syncthreads();
+    in = sin_in;
+  }
+  const int wib = threadIdx.x >> 5;
+  const int row = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
   const int lane = threadIdx.x & 31;
-  if (warp >= N) return;
-  const uint4* w = reinterpret_cast<const uint4*>(W + (size_t)warp * K);
+  if (row >= N && !mod) return;  // (with mod: stay for the CTA barrier below)
+  const uint4* w = reinterpret_cast<const uint4*>(W + (size_t)min(row, N - 1) * K);
   float acc[BC_MAX_ENTRIES];
 #pragma unroll
   for (int e = 0; e < BC_MAX_ENTRIES; ++e) acc[e] = 0.0f;
-  for (int k8 = lane; k8 < K / 8; k8 += 32) {
-    const uint4 u = __ldg(w + k8);
-    const __nv_bfloat16* h = reinterpret_cast<const __nv_bfloat16*>(&u);
-    float wk[8];
+  constexpr int kAhead = 4;
+  const int k8n = K / 8;
+  for (int k0 = lane; k0 < k8n; k0 += 32 * kAhead) {
+    uint4 u[kAhead];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) wk[j] = bf(h[j]);
+    for (int j = 0; j < kAhead; ++j) u[j] = k0 + 32 * j < k8n ? __ldg(w + k0 + 32 * j) : make_uint4(0u, 0u, 0u, 0u);
 #pragma unroll
-    for (int e = 0; e < BC_MAX_ENTRIES; ++e) {
-      if (e < n) {
-        const float4* x = reinterpret_cast<const float4*>(in + (size_t)e * K) + 2 * k8;
-        const float4 x0 = x[0], x1 = x[1];
-        acc[e] += wk[0] * x0.x + wk[1] * x0.y + wk[2] * x0.z + wk[3] * x0.w + wk[4] * x1.x + wk[5] * x1.y +
-                  wk[6] * x1.z + wk[7] * x1.w;
+    for (int j = 0; j < kAhead; ++j) {
+      const int k8 = k0 + 32 * j;
+      const __nv_bfloat16* h = reinterpret_cast<const __nv_bfloat16*>(&u[j]);
+#pragma unroll
+      for (int e = 0; e < BC_MAX_ENTRIES; ++e) {
+        if (e < n && k8 < k8n) {
+          const float4* x = reinterpret_cast<const float4*>(in + (size_t)e * K) + 2 * k8;
+          const float4 x0 = x[0], x1 = x[1];
+          acc[e] += bf(h[0]) * x0.x + bf(h[1]) * x0.y + bf(h[2]) * x0.z + bf(h[3]) * x0.w + bf(h[4]) * x1.x +
+                    bf(h[5]) * x1.y + bf(h[6]) * x1.z + bf(h[7]) * x1.w;
+        }
       }
     }
   }
 #pragma unroll
   for (int e = 0; e < BC_MAX_ENTRIES; ++e) {
     if (e < n) {
-      float v = warp_sum(acc[e]);
-      if (lane == 0) {
-        v += b ? b[warp] : 0.0f;
-        out[(size_t)e * N + warp] = act == 1 ? silu(v) : v;
-        if (act == 2) out2[(size_t)e * N + warp] = silu(v);
+      float v = warp_sum(acc[e]);  // (xor butterfly: every lane holds the sum)
+      v += b ? b[min(row, N - 1)] : 0.0f;
+      const float o = act == 1 ? silu(v) : v;
+      if (lane == 0 && row < N) {
+        out[(size_t)e * N + row] = o;
+        if (act == 2) out2[(size_t)e * N + row] = silu(v);
+        if (mod) e0s[e][wib] = o;
       }
     }
   }
-}
-
-// sinusoid(freq_dim) of each entry's timestep: [cos(t w_k), sin(t w_k)],
-// w_k = 10000^(-k/half)  (Wan sinusoidal_embedding_1d)
-__global__ void timestep_sin_kernel(TimeArgs a, float* out, int freq_dim) {
-  const int e = blockIdx.x;
-  const int half = freq_dim / 2;
-  for (int k = threadIdx.x; k < half; k += blockDim.x) {
-    const double w = pow(10000.0, -(double)k / (double)half);
-    const double arg = a.t[e] * w;
-    out[(size_t)e * freq_dim + k] = (float)cos(arg);
-    out[(size_t)e * freq_dim + half + k] = (float)sin(arg);
+  if (mod) {
+    __syncthreads();
+    const int nw = blockDim.x >> 5;
+    const int o0 = (int)blockIdx.x * nw;
+    const int cnt = min(nw, N - o0);
+    for (int i = threadIdx.x; i < L * n * nw; i += blockDim.x) {
+      const int j = i % nw, le = i / nw;
+      const int e = le % n, l = le / n;
+      if (j < cnt) mod[((size_t)l * n + e) * N + o0 + j] = base[(size_t)l * N + o0 + j] + e0s[e][j];
+    }
   }
 }
 
@@ -545,17 +584,6 @@ __global__ void check_finite_kernel(EntryPtrs lat, int n_el, int32_t* status) {
   if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicCAS(status, 0, 1 + lat.block[e]);
 }
 
-// out[l][e][k][:] = base[l][k][:] + e0[e][k][:]   (all 6 AdaLN chunks, all layers)
-__global__ void mod_combine_kernel(const float* base, const float* e0, int L, int n, int d, float* out) {
-  const int64_t total = (int64_t)L * n * 6 * d;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-    const int c = (int)(i % (6 * d));
-    const int64_t le = i / (6 * d);
-    const int e = (int)(le % n), l = (int)(le / n);
-    out[i] = base[(size_t)l * 6 * d + c] + e0[(size_t)e * 6 * d + c];
-  }
-}
-
 int grid_for(int64_t work, int threads) {
   int64_t g = (work + threads - 1) / threads;
   if (g > 148 * 32) g = 148 * 32;
@@ -565,24 +593,26 @@ int grid_for(int64_t work, int threads) {
 }  // namespace
 
 int launch_patchify(const EntryPtrs& lat, int F, int H, int W, int row0, int rows, __nv_bfloat16* out,
-                    cudaStream_t st) {
+                    int32_t* status, cudaStream_t st) {
   const int T = F * (H / 2) * (W / 2);
-  patchify_kernel<<<grid_for((int64_t)rows * 64, 256), 256, 0, st>>>(lat, F, H, W, out, T, row0, rows);
+  patchify_kernel<<<grid_for((int64_t)rows * 64, 256), 256, 0, st>>>(lat, F, H, W, out, T, row0, rows, status);
   BC_LAUNCHED();
   return BC_OK;
 }
 
 int launch_gemv(const float* in, int n, int K, const __nv_bfloat16* W, const float* b, float* out, int N, int act,
-                float* out2, cudaStream_t st) {
+                float* out2, cudaStream_t st, const TimeArgs* ts, const float* base, int L, float* mod) {
   if (K % 8 || (act == 2 && !out2)) return bc_fail(BC_ERR_CONTRACT, "gemv: K %% 8 != 0 or missing out2");
+  if (!in && (!ts || K % 2 || (size_t)n * K * sizeof(float) > 48 * 1024))
+    return bc_fail(BC_ERR_CONTRACT, "gemv: the sinusoid input needs timesteps and n * K <= 12288");
+  if (mod && (!base || L < 1)) return bc_fail(BC_ERR_CONTRACT, "gemv: modulation tables need base and L");
   const int threads = 256;
-  gemv_kernel<<<(N * 32 + threads - 1) / threads, threads, 0, st>>>(in, n, K, W, b, out, N, act, out2);
-  BC_LAUNCHED();
-  return BC_OK;
-}
-
-int launch_timestep_sin(const TimeArgs& a, int n, float* out, int freq_dim, cudaStream_t st) {
-  timestep_sin_kernel<<<n, 128, 0, st>>>(a, out, freq_dim);
+  const size_t smem = in ? 0 : (size_t)n * K * sizeof(float);
+  const int grid = (N * 32 + threads - 1) / threads;
+  if (in)
+    gemv_kernel<false><<<grid, threads, 0, st>>>(in, n, K, W, b, out, N, act, out2, TimeArgs{}, base, L, mod);
+  else
+    gemv_kernel<true><<<grid, threads, smem, st>>>(in, n, K, W, b, out, N, act, out2, *ts, base, L, mod);
   BC_LAUNCHED();
   return BC_OK;
 }
@@ -683,10 +713,5 @@ int launch_check_finite(const EntryPtrs& lat, int n, int n_el, int32_t* status, 
   return BC_OK;
 }
 
-int launch_mod_combine(const float* base, const float* e0, int L, int n, int d, float* out, cudaStream_t st) {
-  mod_combine_kernel<<<grid_for((int64_t)L * n * 6 * d, 256), 256, 0, st>>>(base, e0, L, n, d, out);
-  BC_LAUNCHED();
-  return BC_OK;
-}
 
 }  // namespace bc

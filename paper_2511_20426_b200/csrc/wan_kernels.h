@@ -77,12 +77,16 @@ struct UpdArgs {
 };
 
 // tokens of global rows [row0, row0 + rows) of the concatenated batch
+// status != nullptr: also the finiteness check of the latents (rows must
+// cover every latent of the batch)
 int launch_patchify(const EntryPtrs& lat, int F, int H, int W, int row0, int rows, __nv_bfloat16* out,
-                    cudaStream_t st);
-// act 0: none, 1: silu, 2: out raw + out2 silu
+                    int32_t* status, cudaStream_t st);
+// act 0: none, 1: silu, 2: out raw + out2 silu.  in == nullptr: the input
+// is the sinusoid (K = freq_dim) of ts->t[e]; mod != nullptr: also
+// mod[l][e][o] = base[l][o] + out[e][o] for l < L (the AdaLN tables)
 int launch_gemv(const float* in, int n, int K, const __nv_bfloat16* W, const float* b, float* out, int N, int act,
-                float* out2, cudaStream_t st);
-int launch_timestep_sin(const TimeArgs& a, int n, float* out, int freq_dim, cudaStream_t st);
+                float* out2, cudaStream_t st, const TimeArgs* ts = nullptr, const float* base = nullptr, int L = 0,
+                float* mod = nullptr);
 int launch_ln_rows(const float* X, __nv_bfloat16* out, int rows, int d, int rows_per_entry, const LnArgs& a,
                    cudaStream_t st);
 int launch_qk_norm_rope(const __nv_bfloat16* qkv, int rows, int d, int T, const QkArgs& a, cudaStream_t st);
@@ -93,7 +97,6 @@ int launch_copy_cols(const __nv_bfloat16* src, int ld_src, int c0, __nv_bfloat16
 int launch_f32_to_bf16(const float* src, __nv_bfloat16* dst, int64_t n, cudaStream_t st);
 int launch_head_update(const float* Y, int n, int T, int F, int H, int W, const UpdArgs& u, int32_t* status,
                        cudaStream_t st);
-int launch_mod_combine(const float* base, const float* e0, int L, int n, int d, float* out, cudaStream_t st);
 int launch_signal_done(const PeerArgs& p, cudaStream_t st);
 // release-store `v` to up to kMaxFlagWrites (peer) flag words from one
 // thread after a system fence: the fallback of cuStreamWriteValue32

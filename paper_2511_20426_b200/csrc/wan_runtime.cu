@@ -50,7 +50,7 @@ struct bc_wan_ctx {
   float* X;
   __nv_bfloat16 *xn, *qkv, *Q, *attn, *H1, *patches;
   float* Y;
-  float *t_sin, *t_h, *t_e, *t_es, *t_e0, *mod_all;
+  float *t_h, *t_e, *t_es, *t_e0, *mod_all;
   __nv_bfloat16 *text_in, *text_h, *ctx, *text_tmp, *textkv;
   float2 *rope_f, *rope_h, *rope_w;
   bool text_ready, rope_ready;
@@ -114,7 +114,6 @@ int64_t carve(bc_wan_ctx* c, const bc_wan_dims& dm, char* base) {
   t->H1 = cv.take<__nv_bfloat16>(R * dm.ffn_dim);
   t->patches = cv.take<__nv_bfloat16>(R * 64);
   t->Y = cv.take<float>(R * 64);
-  t->t_sin = cv.take<float>(E * dm.freq_dim);
   t->t_h = cv.take<float>(E * d);
   t->t_e = cv.take<float>(E * d);
   t->t_es = cv.take<float>(E * d);
@@ -428,22 +427,26 @@ int stage_begin(bc_wan_ctx* c, const bc_batch* batch, const bc_wan_update* upd, 
     lat.p[e] = upd->latents[e];
     lat.block[e] = batch->block_index[e];
   }
-  RC(timed(kBandwidth, 0.0, 4.0 * n * F * 16 * H * W, st, [&] { return bc::launch_check_finite(lat, n, F * 16 * H * W, status, st); }));
+  // the finiteness check of the inputs rides on patchify when this rank's
+  // rows cover the whole batch; a row slice checks every latent separately
+  const bool whole = S.row0 == 0 && R == n * T;
+  if (!whole)
+    RC(timed(kBandwidth, 0.0, 4.0 * n * F * 16 * H * W, st, [&] { return bc::launch_check_finite(lat, n, F * 16 * H * W, status, st); }));
   if (R > 0)
-    RC(timed(kBandwidth, 0.0, 6.0 * R * 64, st, [&] { return bc::launch_patchify(lat, F, H, W, S.row0, R, c->patches, st); }));
+    RC(timed(kBandwidth, 0.0, 6.0 * R * 64, st, [&] { return bc::launch_patchify(lat, F, H, W, S.row0, R, c->patches, whole ? status : nullptr, st); }));
   RC(timed(kGemm, 2.0 * R * d * 64, 0.0, st, [&] { return gemm(c->patches, p.patch_w, c->X, R, d, 64, bc::kEpiStoreF32, p.patch_b, nullptr, 0, 1, st); }));
 
   // time embedding: e = W2 silu(W1 sin(t) + b1) + b2 ; e0 = Wp silu(e) + bp
   bc::TimeArgs ta{};
   for (int e = 0; e < n; ++e) ta.t[e] = batch->level[e];
-  RC(bc::launch_timestep_sin(ta, n, c->t_sin, dm.freq_dim, st));
-  RC(bc::launch_gemv(c->t_sin, n, dm.freq_dim, static_cast<const __nv_bfloat16*>(p.time_w1), p.time_b1, c->t_h, d,
-                     1, nullptr, st));
+  // (three launches: the sinusoid is computed inside the first GEMV, the
+  // per-layer AdaLN tables are written by the last)
+  RC(bc::launch_gemv(nullptr, n, dm.freq_dim, static_cast<const __nv_bfloat16*>(p.time_w1), p.time_b1, c->t_h, d,
+                     1, nullptr, st, &ta));
   RC(bc::launch_gemv(c->t_h, n, d, static_cast<const __nv_bfloat16*>(p.time_w2), p.time_b2, c->t_e, d, 2, c->t_es,
                      st));
   RC(bc::launch_gemv(c->t_es, n, d, static_cast<const __nv_bfloat16*>(p.tproj_w), p.tproj_b, c->t_e0, 6 * d, 0,
-                     nullptr, st));
-  RC(bc::launch_mod_combine(p.modulation, c->t_e0, L, n, d, c->mod_all, st));
+                     nullptr, st, nullptr, p.modulation, L, c->mod_all));
 
   bc::AttnArgs& sa = S.sa;
   sa = bc::AttnArgs{};

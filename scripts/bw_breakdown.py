@@ -34,3 +34,7 @@ print(f"total kernel time {tot:.1f} ms")
 for name, v in sorted(agg.items(), key=lambda kv: -sum(kv[1])):
     print(f"{sum(v):9.2f} ms {100 * sum(v) / tot:5.1f}%  n={len(v):5d}  mean {1e3 * sum(v) / len(v):8.1f} us"
           f"  min {1e3 * min(v):8.1f}  max {1e3 * max(v):8.1f}  {name}")
+if os.environ.get("LIST"):  # per-launch durations of one kernel, in launch order (first 12)
+    evs = sorted((e for e in p.events() if e.device_type == torch.autograd.DeviceType.CUDA
+                  and os.environ["LIST"] in e.name), key=lambda e: e.time_range.start)
+    print(os.environ["LIST"], [round(e.time_range.end - e.time_range.start, 1) for e in evs[:12]], "us")

@@ -249,3 +249,24 @@ def test_wan_graph_launch_bit_identical(tiny):
         N.lib().bc_wan_set_graphs(1)
     for k in a.outputs:
         assert np.array_equal(a.outputs[k], c.outputs[k]) and np.array_equal(b.outputs[k], c.outputs[k])
+
+
+@pytest.mark.parametrize("bad", [0, 2])
+def test_wan_nonfinite_latent_reported(tiny, bad):
+    """A NaN / Inf in one entry's latents is caught on the device (the check
+    rides on the patchify pass) and reported with that entry's block index;
+    the context stays usable for the next step."""
+    import paper_2511_20426_b200 as bc
+    cfg, w, _ = tiny
+    cond = bc.embed_prompt("a lighthouse in a storm", cfg.cond_dim)
+    rng = np.random.default_rng(3)
+    batch = [0, 1, 2]
+    lat = {b: rng.standard_normal((cfg.block_size, cfg.latent_dim)).astype(np.float32) for b in batch}
+    lat[batch[bad]][1, 5] = np.inf if bad else np.nan
+    mask = bc.build_mask(batch, [], "bidirectional", cfg.block_size)
+    with pytest.raises(bc.NumericError) as err:
+        bc.forward(w, [bc.EntryInput(b, lat[b], 500.0, cond) for b in batch], [], mask)
+    assert err.value.block_index == batch[bad]
+    lat[batch[bad]][1, 5] = 0.0
+    outs = bc.forward(w, [bc.EntryInput(b, lat[b], 500.0, cond) for b in batch], [], mask)
+    assert all(np.isfinite(o.x0).all() for o in outs)
