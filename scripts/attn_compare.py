@@ -60,3 +60,39 @@ try:
     print(f"flashinfer single_prefill {ms:8.3f} ms  {flops / ms / 1e9:7.0f} TFLOP/s")
 except Exception as ex:
     print(f"flashinfer unavailable ({type(ex).__name__}: {str(ex)[:120]})")
+# flashinfer's Blackwell kernels on the same shape: the CUTLASS sm100 FMHA
+# (fmha_varlen, JIT-built from flashinfer's bundled CUTLASS) over per-entry
+# KV segments, and the trtllm-gen paged context kernel (prebuilt cubins; on an
+# offline box it reports unavailable)
+qf = q.view(n_ent * T, heads, 128)
+try:
+    from flashinfer.prefill import fmha_varlen
+    kr = k.repeat(n_ent, 1, 1).contiguous()
+    vr = v.repeat(n_ent, 1, 1).contiguous()
+    qo = torch.arange(0, n_ent + 1, device="cuda", dtype=torch.int32) * T
+    kvo = torch.arange(0, n_ent + 1, device="cuda", dtype=torch.int32) * Nk
+    ms = timeit(lambda: fmha_varlen(qf, kr, vr, qo, kvo, max_qo_len=T, causal=False))
+    print(f"flashinfer cutlass sm100 fmha {ms:8.3f} ms  {flops / ms / 1e9:7.0f} TFLOP/s")
+    del kr, vr
+except Exception as ex:
+    print(f"flashinfer cutlass sm100 fmha unavailable ({type(ex).__name__}: {str(ex)[:160]})")
+try:
+    from flashinfer.prefill import trtllm_batch_context_with_kv_cache
+    page = 32
+    n_pages = (Nk + page - 1) // page
+    kc = torch.zeros(n_pages * page, heads, 128, device="cuda", dtype=torch.bfloat16)
+    vc = torch.zeros_like(kc)
+    kc[:Nk] = k
+    vc[:Nk] = v
+    kc = kc.view(n_pages, page, heads, 128).transpose(1, 2).contiguous()  # HND pages
+    vc = vc.view(n_pages, page, heads, 128).transpose(1, 2).contiguous()
+    tables = torch.arange(n_pages, device="cuda", dtype=torch.int32).unsqueeze(0).repeat(n_ent, 1)
+    seq = torch.full((n_ent,), Nk, device="cuda", dtype=torch.int32)
+    cq = torch.arange(0, n_ent + 1, device="cuda", dtype=torch.int32) * T
+    ckv = torch.arange(0, n_ent + 1, device="cuda", dtype=torch.int32) * Nk
+    ws = torch.zeros(256 << 20, device="cuda", dtype=torch.uint8)
+    ms = timeit(lambda: trtllm_batch_context_with_kv_cache(qf, (kc, vc), ws, tables, seq, T, Nk, 128 ** -0.5, 1.0,
+                                                           n_ent, cq, ckv, causal=False))
+    print(f"flashinfer trtllm-gen context {ms:8.3f} ms  {flops / ms / 1e9:7.0f} TFLOP/s")
+except Exception as ex:
+    print(f"flashinfer trtllm-gen context unavailable ({type(ex).__name__}: {str(ex)[:160]})")
