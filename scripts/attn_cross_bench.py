@@ -29,3 +29,60 @@ for _ in range(5):
     best = min(best, s.elapsed_time(e) / 20)
 fl = 4.0 * n_ent * T * Tk * heads * 128
 print(f"cross-attention shape: {best * 1e3:.1f} us  {fl / best / 1e9:.0f} TFLOP/s")
+
+
+def timeit(g):
+    for _ in range(3):
+        g()
+    b2 = 1e9
+    for _ in range(5):
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        for _ in range(20):
+            g()
+        e.record()
+        torch.cuda.synchronize()
+        b2 = min(b2, s.elapsed_time(e) / 20)
+    return b2
+
+
+# the libraries on the same shape (context for the fraction of peak)
+k = kv[0, 0].view(Tk, heads, 128)
+v = kv[0, 1].view(Tk, heads, 128)
+qd = q.view(n_ent, T, heads, 128).transpose(1, 2)
+kd = k.transpose(0, 1).unsqueeze(0).expand(n_ent, -1, -1, -1)
+vd = v.transpose(0, 1).unsqueeze(0).expand(n_ent, -1, -1, -1)
+from torch.nn.attention import SDPBackend, sdpa_kernel  # noqa: E402
+try:
+    with sdpa_kernel(SDPBackend.CUDNN_ATTENTION):
+        ms = timeit(lambda: torch.nn.functional.scaled_dot_product_attention(qd, kd, vd))
+    print(f"torch sdpa cudnn: {ms * 1e3:.1f} us  {fl / ms / 1e9:.0f} TFLOP/s")
+except Exception as ex:
+    print(f"torch sdpa cudnn unavailable ({type(ex).__name__})")
+qf = q.view(n_ent * T, heads, 128)
+try:
+    from flashinfer.prefill import trtllm_batch_context_with_kv_cache
+    page = 32
+    n_pages = Tk // page
+    kc = k.view(n_pages, page, heads, 128).transpose(1, 2).contiguous()
+    vc = v.view(n_pages, page, heads, 128).transpose(1, 2).contiguous()
+    tables = torch.arange(n_pages, device="cuda", dtype=torch.int32).unsqueeze(0).repeat(n_ent, 1)
+    seq = torch.full((n_ent,), Tk, device="cuda", dtype=torch.int32)
+    cq = torch.arange(0, n_ent + 1, device="cuda", dtype=torch.int32) * T
+    ckv = torch.arange(0, n_ent + 1, device="cuda", dtype=torch.int32) * Tk
+    ws = torch.zeros(256 << 20, device="cuda", dtype=torch.uint8)
+    ms = timeit(lambda: trtllm_batch_context_with_kv_cache(qf, (kc, vc), ws, tables, seq, T, Tk, 128 ** -0.5, 1.0,
+                                                           n_ent, cq, ckv, causal=False))
+    print(f"flashinfer trtllm-gen context: {ms * 1e3:.1f} us  {fl / ms / 1e9:.0f} TFLOP/s")
+except Exception as ex:
+    print(f"flashinfer trtllm-gen unavailable ({type(ex).__name__}: {str(ex)[:120]})")
+try:
+    from flashinfer.prefill import fmha_varlen
+    kr = k.repeat(n_ent, 1, 1).contiguous()
+    vr = v.repeat(n_ent, 1, 1).contiguous()
+    qo = torch.arange(0, n_ent + 1, device="cuda", dtype=torch.int32) * T
+    kvo = torch.arange(0, n_ent + 1, device="cuda", dtype=torch.int32) * Tk
+    ms = timeit(lambda: fmha_varlen(qf, kr, vr, qo, kvo, max_qo_len=T, causal=False))
+    print(f"flashinfer cutlass sm100 fmha: {ms * 1e3:.1f} us  {fl / ms / 1e9:.0f} TFLOP/s")
+except Exception as ex:
+    print(f"flashinfer cutlass sm100 fmha unavailable ({type(ex).__name__}: {str(ex)[:120]})")
