@@ -423,3 +423,19 @@ def test_gemm_tiling_choices(M, N, K, mode, want):
     nat.check(nat.lib().bc_gemm_plan(M, N, K, mode, ctypes.byref(bn), ctypes.byref(cg)), "bc_gemm_plan")
     assert (bn.value, cg.value) == want
     assert (N % bn.value == 0 or bn.value == 224) and (bn.value not in (192, 224) or cg.value == 2)
+
+
+def test_attention_sequential_shape_one_pair_one_lone_tile():
+    """The width-1 (sequential rollout) self-attention launch: 12 heads x 37
+    query tiles = 444 tiles on 148 CTAs -- the balanced work list gives every
+    CTA one ping-pong pair and one lone tile (the lone
+    tile's exposed softmax is where the sequential rollout loses ~20% of its
+    attention time; splitting its key range would break P1 bit-exactness)."""
+    import collections
+    items, start = _attention_plan([list(range(8))], 4680, 256, 12)
+    kinds = collections.Counter()
+    for c in range(len(start) - 1):
+        k = sorted("P" if int(w) & 0x80000000 else "X" if int(w) & 0x40000000 else "S"
+                   for w in items[start[c]:start[c + 1]])
+        kinds["".join(k)] += 1
+    assert len(start) - 1 == 148 and kinds == {"PS": 148}
