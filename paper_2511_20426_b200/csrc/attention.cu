@@ -209,7 +209,8 @@ template <int kPoly>
 __device__ __forceinline__ void softmax_tile(const AttnParams& prm, uint32_t tmem_s, uint32_t tmem_o,
                                              uint8_t* sp, SoftmaxBars b, int n_tiles, int tiles_per_slot,
                                              uint32_t quad, int q_tok0, int e, int head, int tile_x,
-                                             uint32_t jb = 0, uint64_t* o_free = nullptr) {
+                                             uint32_t jb = 0, uint64_t* o_free = nullptr,
+                                             const CUtensorMap* map_o = nullptr) {
   const uint32_t row = quad * 32 + lane_id();
   const uint32_t lane_base = (quad * 32) << 16;
   const float c = prm.scale * 1.4426950408889634f;
@@ -346,6 +347,12 @@ __device__ __forceinline__ void softmax_tile(const AttnParams& prm, uint32_t tme
         tmem_st_wait();
       }
     }
+    // map_o: the previous item's O tile left this P buffer by TMA; it must
+    // have been read out before the first P of this item overwrites it
+    if (map_o && j == 0) {
+      if (row == 0) bulk_wait_read<0>();
+      named_bar_sync(1 + tile_x, 128);
+    }
     // P -> smem in the UMMA K-major SW128 layout: half h holds keys
     // [64h, 64h+64); 16-byte chunk q of row r sits at chunk (q ^ (r & 7)).
 #ifndef BC_ABL_STS  // timing ablation only: no P stores
@@ -383,7 +390,31 @@ __device__ __forceinline__ void softmax_tile(const AttnParams& prm, uint32_t tme
 #pragma unroll
   for (int k = 0; k < 4; ++k) tmem_ld32(tmem_o + lane_base + k * 32, r[k]);
   tmem_ld_wait();
-  if (live) {
+  if (map_o && n_tiles > 0 && q_tok0 + kRows <= prm.q_hi[e]) {
+    // whole tile: stage the bf16 rows in this tile's P buffer (free: the
+    // last PV is complete) in the SW128 layout and store them with two TMA
+    // boxes -- 16 shared stores per thread instead of 16 global stores that
+    // each touch 32 rows; one thread waits for the read before the next
+    // item's first P store (above)
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+      const int k = q >> 2, o = 8 * (q & 3);
+      const int half = q >> 3, ch = q & 7;
+      sts128(sp_u32 + half * kHalf + row * 128 + ((ch ^ (row & 7)) << 4),
+             pack_bf16(__uint_as_float(r[k][o + 0]) * inv, __uint_as_float(r[k][o + 1]) * inv),
+             pack_bf16(__uint_as_float(r[k][o + 2]) * inv, __uint_as_float(r[k][o + 3]) * inv),
+             pack_bf16(__uint_as_float(r[k][o + 4]) * inv, __uint_as_float(r[k][o + 5]) * inv),
+             pack_bf16(__uint_as_float(r[k][o + 6]) * inv, __uint_as_float(r[k][o + 7]) * inv));
+    }
+    fence_async_shared();
+    named_bar_sync(1 + tile_x, 128);
+    if (row == 0) {
+      const int orow = prm.q_row[e] + q_tok0 - prm.q_lo[e];
+      tma_store_3d(map_o, sp, 0, head, orow);
+      tma_store_3d(map_o, sp + kHalf, 64, head, orow);
+      bulk_commit();
+    }
+  } else if (live) {
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       uint4* dst = reinterpret_cast<uint4*>(out + k * 32);
@@ -835,7 +866,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 template <int kPoly>
 __global__ void __launch_bounds__(kThreads, 1)
     attn_sched_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_kv,
-                      AttnParams prm, const __grid_constant__ AttnSched sch) {
+                      AttnParams prm, const __grid_constant__ AttnSched sch,
+                      const __grid_constant__ CUtensorMap map_o, int tma_o) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Smem::bars);
@@ -1084,9 +1116,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       const Item w = item(i);
       if (x >= w.n_q) continue;
       softmax_tile<kPoly>(prm, tmem + x * 128, tmem + 256 + x * 128, smem + (x ? Smem::pb : Smem::pa), b,
-                          w.n_tiles, tiles_per_slot, warp & 3, w.q(x), w.e(x), w.head, x, tb, &o_free[x]);
+                          w.n_tiles, tiles_per_slot, warp & 3, w.q(x), w.e(x), w.head, x, tb, &o_free[x],
+                          tma_o ? &map_o : nullptr);
       tb += w.n_tiles;
     }
+    if (tma_o && (warp & 3) == 0 && lane_id() == 0) bulk_wait<0>();  // O stores complete before exit
   }
   tc_fence_before();
   __syncthreads();
@@ -1428,7 +1462,22 @@ int attention_run(const AttnArgs& a, cudaStream_t st) {
     int ctas = 0;
     const std::shared_ptr<const AttnSched> sch = build_sched(a, p, &ctas);
     if (sch) {
-      attn_sched_kernel<kSchedPoly><<<ctas, kThreads, Smem::total + 1024, st>>>(mq, mkv, p, *sch);
+      // O leaves by TMA (BC_ATTN_TMA_O=0: per-thread global stores)
+      static int tma_o = -1;
+      if (tma_o < 0) {
+        const char* env = getenv("BC_ATTN_TMA_O");
+        tma_o = env ? atoi(env) != 0 : 1;
+      }
+      CUtensorMap mo = mq;
+      if (tma_o) {
+        cuuint64_t dims[3] = {kHd, (cuuint64_t)a.heads,
+                              (cuuint64_t)(a.ranged ? a.q_rows : a.n_entries * a.q_tokens)};
+        cuuint64_t strides[2] = {kHd * 2, row_bytes};
+        cuuint32_t box[3] = {64, 1, kRows};
+        int rc = encode(&mo, a.out, 3, dims, strides, box);
+        if (rc) return rc;
+      }
+      attn_sched_kernel<kSchedPoly><<<ctas, kThreads, Smem::total + 1024, st>>>(mq, mkv, p, *sch, mo, tma_o);
       BC_LAUNCHED();
       return BC_OK;
     }
