@@ -372,7 +372,7 @@ class DistWanSession:
         # one pinned staging area for every emitted block (no per-emission
         # cudaHostAlloc, which would serialise against the device)
         self.host_buf = torch.empty((config.num_blocks,) + tuple(self.shape),
-                                    dtype=torch.float32).pin_memory()
+                                    dtype=torch.float32, pin_memory=True)
         self.events = []
         self.set_conditioning(conditioning)
         self._mark()
@@ -551,7 +551,7 @@ class EmulatedRanks:
         # one pinned staging area for every emitted block (no per-emission
         # cudaHostAlloc, which would serialise against the device)
         self.host_buf = torch.empty((config.num_blocks,) + tuple(self.shape),
-                                    dtype=torch.float32).pin_memory()
+                                    dtype=torch.float32, pin_memory=True)
         self.events = []
         self.set_conditioning(conditioning)
         ev = torch.cuda.Event(enable_timing=True)

@@ -437,7 +437,7 @@ class HostNoiseFeed:
         self.stream = NoiseStream(session_seed, cfg.latent_dim)
         self.shape = (cfg.block_size, cfg.latent_channels, cfg.latent_height, cfg.latent_width)
         self.S = cfg.block_size
-        self.ring = [torch.empty(self.shape, dtype=torch.float32).pin_memory() for _ in range(ring)]
+        self.ring = [torch.empty(self.shape, dtype=torch.float32, pin_memory=True) for _ in range(ring)]
         self.events = [None] * ring
         self.next = 0
         self.h2d_bytes = 0
@@ -524,7 +524,7 @@ class WanSession:
         # one pinned staging area for every emitted block (no per-emission
         # cudaHostAlloc, which would serialise against the device)
         self.host_buf = torch.empty((config.num_blocks,) + tuple(self.shape),
-                                    dtype=torch.float32).pin_memory()
+                                    dtype=torch.float32, pin_memory=True)
         self.eps = [torch.empty(self.shape, dtype=torch.float32, device="cuda")
                     for _ in range(width)]
         self.events = []
