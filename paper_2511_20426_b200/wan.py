@@ -521,6 +521,9 @@ class WanSession:
         self.noise = noise_feed if noise_feed is not None else HostNoiseFeed(session_seed, config)
         self.latents, self.final, self.tags = {}, {}, {}
         self.host_out = {}
+        # emitted blocks whose D2H copy is in flight (event) / already
+        # converted to the API's float64 arrays while the device kept working
+        self.host_pending, self.host_f64 = {}, {}
         # one pinned staging area for every emitted block (no per-emission
         # cudaHostAlloc, which would serialise against the device)
         self.host_buf = torch.empty((config.num_blocks,) + tuple(self.shape),
@@ -542,8 +545,17 @@ class WanSession:
         self.cond = cond
         self.ctx.set_text(cond)
 
+    def _convert_landed(self):
+        # host-side float64 conversion of blocks whose D2H copy has landed,
+        # done while the device runs (not all at the end of the run)
+        for b, ev in list(self.host_pending.items()):
+            if ev.query():
+                self.host_f64[b] = self.host_out[b].numpy().reshape(self.cfg.block_size, -1).astype(np.float64)
+                del self.host_pending[b]
+
     def step(self, plan, mask, pool, vis_lists, posts):
         torch = self.torch
+        self._convert_landed()
         init_req, init_dst = [], []
         for e in plan.entries:
             self.slots.acquire(e.block_index)
@@ -582,6 +594,10 @@ class WanSession:
                 host = self.host_buf[e.block_index]
                 host.copy_(self.final[e.block_index], non_blocking=True)
                 self.host_out[e.block_index] = host
+                self.host_f64.pop(e.block_index, None)
+                ev = torch.cuda.Event()
+                ev.record()
+                self.host_pending[e.block_index] = ev
                 self.d2h_bytes += host.numel() * 4
             elif kind == POST_CACHE:
                 self.latents.pop(e.block_index, None)
@@ -620,6 +636,10 @@ class WanSession:
     def emitted_host(self, block):
         self.torch.cuda.current_stream().synchronize()
         self.ctx.check_status()
+        self.host_pending.pop(block, None)
+        cached = self.host_f64.pop(block, None)
+        if cached is not None:
+            return cached
         return self.host_out[block].numpy().reshape(self.cfg.block_size, -1).astype(np.float64)
 
     def emitted_device(self, block):
