@@ -369,6 +369,7 @@ class DistWanSession:
         self.shape = self.rep.shape
         self.noise = noise_feed if noise_feed is not None else HostNoiseFeed(session_seed, config)
         self.tags, self.host_out = {}, {}
+        self.host_pending, self.host_f64 = {}, {}
         # one pinned staging area for every emitted block (no per-emission
         # cudaHostAlloc, which would serialise against the device)
         self.host_buf = torch.empty((config.num_blocks,) + tuple(self.shape),
@@ -398,6 +399,7 @@ class DistWanSession:
 
     def step(self, plan, mask, pool, vis_lists, posts):
         from .wan import POST_EMIT, _make_update
+        self._convert_landed()
         epoch = plan.iteration + 1
         blocks = plan.blocks
         for b in blocks:
@@ -427,6 +429,10 @@ class DistWanSession:
                     host = self.host_buf[b]
                     host.copy_(self.rep.final[b], non_blocking=True)
                     self.host_out[b] = host
+                    self.host_f64.pop(b, None)
+                    ev = self.torch.cuda.Event()
+                    ev.record()
+                    self.host_pending[b] = ev
             self.rep.retire(plan, posts, work.local)
         self.slot_epoch.wrote([self.slots.slot_of(b) for b in blocks], epoch, work.masks)
         for e in plan.entries:
@@ -468,9 +474,21 @@ class DistWanSession:
     def release(self, block):
         self.slots.release(block)
 
+    def _convert_landed(self):
+        # float64 conversion of emitted blocks whose D2H copy has landed,
+        # while the device runs (as WanSession does)
+        for b, ev in list(self.host_pending.items()):
+            if ev.query():
+                self.host_f64[b] = self.host_out[b].numpy().reshape(self.cfg.block_size, -1).astype(np.float64)
+                del self.host_pending[b]
+
     def emitted_host(self, block):
         self.torch.cuda.current_stream().synchronize()
         self.state.ctx.check_status()
+        self.host_pending.pop(block, None)
+        cached = self.host_f64.pop(block, None)
+        if cached is not None:
+            return cached
         if block in self.host_out:
             return self.host_out[block].numpy().reshape(self.cfg.block_size, -1).astype(np.float64)
         return None
