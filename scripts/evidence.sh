@@ -9,6 +9,7 @@ timeout 900 python -m pytest tests -m gpu -q 2>&1 | tail -3 > gpurun_out/ev_test
 timeout 900 python bench.py 2>gpurun_out/ev_bench.err | tail -1 > gpurun_out/ev_bench.json
 timeout 600 python scripts/wan_parity_report.py > gpurun_out/ev_parity.json 2>>gpurun_out/ev_bench.err
 timeout 600 python scripts/attn_compare.py 2>/dev/null | grep -v Warn > gpurun_out/ev_attn_compare.txt
+timeout 600 python scripts/attn_cross_bench.py 2>/dev/null | grep -v -i warn > gpurun_out/ev_attn_cross_compare.txt
 timeout 900 python bench.py --preset 14b --steps 2 --no-cpu --no-switch 2>>gpurun_out/ev_bench.err | tail -1 > gpurun_out/ev_bench_14b.json
 timeout 900 python bench.py --blocks 80 --sink 0 --switch-every 20 --steps 2 --no-cpu --no-seq --no-switch 2>>gpurun_out/ev_bench.err | tail -1 > gpurun_out/ev_bench_longlive.json
 timeout 900 ncu --profile-from-start off --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum \
@@ -21,6 +22,7 @@ BC_FORCE_DEVICE=0 BC_DIST_BACKEND=gloo timeout 900 python bench.py --gpus 2 --de
   2>>gpurun_out/ev_bench.err | tail -1 > gpurun_out/ev_decode_gpu_one_gpu.json
 timeout 300 python scripts/attn_power.py > gpurun_out/ev_attn_power.txt 2>&1
 timeout 300 python scripts/gemm_tiling.py > gpurun_out/ev_gemm_tiling.txt 2>&1
+# (compute-sanitizer may be closed on the pool; the loop then records that)
 for tool in memcheck racecheck synccheck; do
   echo "== $tool"; timeout 900 compute-sanitizer --tool $tool --print-limit 20 python scripts/sanitize_small.py 2>&1 | tail -4
 done > gpurun_out/ev_sanitizers.txt
